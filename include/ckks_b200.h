@@ -1,0 +1,140 @@
+/*
+ * ckks_b200.h -- C ABI of libckks_b200.so, the sm_100a engine behind the
+ * rnscope-compatible Python package paper_2512_18345_b200.
+ *
+ * The reference (rnscope 0.1.0, /root/reference/pkg/src/rnscope) has no FFI
+ * layer: its boundary is the Python module API of rns / transform / baseconv /
+ * keyswitch.  Each entry point below names the reference routine whose work it
+ * takes over (paths relative to that package).  The Python side performs the
+ * reference's structural checks and raises its exception types; these
+ * functions only validate what they need to launch safely.
+ *
+ * Conventions
+ *  - all `const uint32_t*` / `uint32_t*` data arguments are DEVICE pointers to
+ *    row-major limb matrices of 32-bit residues in [0, q) (the RNSV wire
+ *    layout, vectors.py:3-14); `row_slot` arguments are DEVICE int32 arrays of
+ *    modulus slots (one per row) obtained from ckks_modulus_register;
+ *  - `stream` is a cudaStream_t passed as void* (0 = default stream); every
+ *    call only enqueues work and is CUDA-graph capturable unless noted;
+ *  - functions return CKKS_OK (0) or a CKKS_ERR_* code; ckks_last_error()
+ *    returns a thread-local description of the last failure;
+ *  - nothing here falls back to the CPU: without a CUDA device
+ *    ckks_ctx_create fails with CKKS_ERR_CUDA.
+ */
+#ifndef CKKS_B200_H
+#define CKKS_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CKKS_OK 0
+#define CKKS_ERR_ARG 1
+#define CKKS_ERR_CUDA 2
+#define CKKS_ERR_UNSUPPORTED 3
+#define CKKS_ERR_STATE 4
+
+typedef struct ckks_ctx ckks_ctx;
+
+/* ABI version of this header; bumped on any signature change. */
+int ckks_abi_version(void);
+const char* ckks_last_error(void);
+
+/* ---- context ---------------------------------------------------------------- */
+
+/* One context per process per GPU: owns the modulus slots, twiddle tables,
+ * conversion tables and key-switch plans (the reference keeps these in
+ * functools.lru_cache: transform.py:121-123,184-186, keyswitch.py:221-223). */
+int ckks_ctx_create(int device, ckks_ctx** out);
+void ckks_ctx_destroy(ckks_ctx* ctx);
+
+/* Register modulus q for ring degree n with psi a primitive 2n-th root of
+ * unity mod q (already squared down to order 2n, transform.py:88-96) and build
+ * its device twiddle tables: fwd[t] = psi^bitrev(t), inv[t] = psi^-bitrev(t),
+ * N^-1 (transform.py:76-118, Modulus rns.py:85-113).  n = 0 or psi = 0
+ * registers the modulus for element-wise / conversion use only.  Idempotent
+ * per (q, n, psi).  Not capturable (allocates, copies). */
+int ckks_modulus_register(ckks_ctx* ctx, uint32_t q, uint32_t n, uint32_t psi, int32_t* slot);
+
+/* Copy a slot's tables back to the host (TwiddleTable.fwd/inv/n_inv,
+ * transform.py:43-64); fwd/inv hold n words each. */
+int ckks_modulus_tables(ckks_ctx* ctx, int32_t slot, uint32_t* fwd, uint32_t* inv, uint32_t* n_inv);
+
+/* ---- transforms: transform.py:203-323 --------------------------------------- */
+
+/* ntt_polynomial (transform.py:279-287): whole transform of `rows` limbs of
+ * degree n; row r uses modulus slot row_slot[r].  in may equal out. */
+int ckks_ntt(ckks_ctx* ctx, const uint32_t* in, uint32_t* out, const int32_t* row_slot, int rows,
+             uint32_t n, int inverse, void* stream);
+
+/* _run_stages over [stage_lo, stage_hi) (transform.py:203-250), the building
+ * block of ntt_two_phase (transform.py:290-323). */
+int ckks_ntt_stages(ckks_ctx* ctx, const uint32_t* in, uint32_t* out, const int32_t* row_slot,
+                    int rows, uint32_t n, int inverse, uint32_t stage_lo, uint32_t stage_hi,
+                    void* stream);
+
+/* ---- element-wise and automorphism: rns.py:243-320 -------------------------- */
+
+/* poly_elementwise (rns.py:243-258); kind 0 add, 1 sub, 2 mul. */
+int ckks_elementwise(ckks_ctx* ctx, const uint32_t* a, const uint32_t* b, uint32_t* out,
+                     const int32_t* row_slot, int rows, size_t cols, int kind, void* stream);
+
+/* automorphism, evaluation domain (rns.py:313-320): out[:, t] = in[:, perm_k(t)]. */
+int ckks_automorphism_eval(ckks_ctx* ctx, const uint32_t* in, uint32_t* out, int rows, uint32_t n,
+                           uint32_t k, void* stream);
+
+/* automorphism, coefficient domain (rns.py:306-312). */
+int ckks_automorphism_coeff(ckks_ctx* ctx, const uint32_t* in, uint32_t* out,
+                            const int32_t* row_slot, int rows, uint32_t n, uint32_t k, void* stream);
+
+/* ---- base conversion: baseconv.py:57-151 ------------------------------------ */
+
+/* build_bconv_table (baseconv.py:57-85) for source slots -> target slots.
+ * Not capturable. */
+int ckks_bconv_table_create(ckks_ctx* ctx, const int32_t* in_slot, int l_in, const int32_t* out_slot,
+                            int l_out, int32_t* table);
+
+/* Host copy of T (l_out x l_in) and inv_qhat (l_in), BConvTable.t / .inv_qhat. */
+int ckks_bconv_table_read(ckks_ctx* ctx, int32_t table, uint32_t* t, uint32_t* inv_qhat);
+
+/* convert (baseconv.py:147-151): in [l_in][cols] -> out [l_out][cols], exact
+ * non-centred fast base conversion. */
+int ckks_bconv(ckks_ctx* ctx, int32_t table, const uint32_t* in, uint32_t* out, size_t cols,
+               void* stream);
+
+/* ---- key switching: keyswitch.py:186-453 ------------------------------------ */
+
+/* _KsTables (keyswitch.py:186-218) plus device workspace for one shape:
+ * `l` active Q limbs (slots q_slot[l]) in digits of `alpha`, P basis p_slot[alpha].
+ * Key matrices passed to this plan are [beta][2][evk_ext][n]; active Q row i is
+ * key row i and P row j is key row evk_p_off + j (evk_ext = L + alpha and
+ * evk_p_off = L for a key generated at the full level L).  Not capturable. */
+int ckks_ks_plan_create(ckks_ctx* ctx, uint32_t n, int l, int alpha, const int32_t* q_slot,
+                        const int32_t* p_slot, int evk_ext, int evk_p_off, int32_t* plan);
+
+/* keyswitch_stage1 (keyswitch.py:297-315): a [l][n] evaluation domain ->
+ * raised [beta][l+alpha][n], digit limbs carried through. */
+int ckks_ks_stage1(ckks_ctx* ctx, int32_t plan, const uint32_t* a, uint32_t* raised, void* stream);
+
+/* keyswitch_stage2 / stage2_p_part / stage2_q_part (keyswitch.py:318-384) on
+ * extended-basis rows [row_lo, row_hi): acc_a, acc_b are [row_hi-row_lo][n]. */
+int ckks_ks_stage2(ckks_ctx* ctx, int32_t plan, const uint32_t* raised, const uint32_t* evk,
+                   int row_lo, int row_hi, uint32_t* acc_a, uint32_t* acc_b, void* stream);
+
+/* keyswitch_stage3 (keyswitch.py:422-441): ModDown of both accumulator halves. */
+int ckks_ks_stage3(ckks_ctx* ctx, int32_t plan, const uint32_t* q_a, const uint32_t* q_b,
+                   const uint32_t* p_a, const uint32_t* p_b, uint32_t* out_a, uint32_t* out_b,
+                   void* stream);
+
+/* keyswitch (keyswitch.py:444-453): all three stages on the plan's workspace;
+ * out_b = delta.b + ct_b when ct_b is non-null.  evk as for the plan. */
+int ckks_keyswitch(ckks_ctx* ctx, int32_t plan, const uint32_t* ct_a, const uint32_t* ct_b,
+                   const uint32_t* evk, uint32_t* out_a, uint32_t* out_b, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CKKS_B200_H */

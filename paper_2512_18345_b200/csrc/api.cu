@@ -1,0 +1,603 @@
+// api.cu -- context, table construction and the extern "C" surface declared
+// in include/ckks_b200.h.  Host code here is setup only (tables are built once
+// per modulus / basis pair / key-switch shape and cached on the device); the
+// hot calls at the bottom just enqueue kernels on the caller's stream.
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <tuple>
+#include <vector>
+
+#include "common.cuh"
+#include "internal.h"
+#include "../../include/ckks_b200.h"
+
+namespace ckks {
+
+static thread_local char g_err[512] = "";
+
+void set_last_error(const char* fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof(g_err), fmt, ap);
+    va_end(ap);
+}
+
+// ---- host number theory (setup only) -----------------------------------------------
+static inline uint32_t h_mulmod(uint32_t a, uint32_t b, uint32_t q) {
+    return (uint32_t)((uint64_t)a * b % q);
+}
+static uint32_t h_powmod(uint32_t b, uint64_t e, uint32_t q) {
+    uint64_t acc = 1 % q, x = b % q;
+    for (; e; e >>= 1) {
+        if (e & 1) acc = acc * x % q;
+        x = x * x % q;
+    }
+    return (uint32_t)acc;
+}
+static inline uint32_t h_inv(uint32_t a, uint32_t q) { return h_powmod(a, (uint64_t)q - 2, q); }
+static inline uint32_t h_shoup(uint32_t w, uint32_t q) { return (uint32_t)(((uint64_t)w << 32) / q); }
+static uint32_t h_bitrev(uint32_t x, uint32_t bits) {
+    uint32_t r = 0;
+    for (uint32_t i = 0; i < bits; ++i) { r = (r << 1) | (x & 1); x >>= 1; }
+    return r;
+}
+static bool h_is_prime(uint32_t n) {
+    if (n < 2) return false;
+    for (uint32_t p : {2u, 3u, 5u, 7u, 11u, 13u, 17u, 19u, 23u, 29u, 31u, 37u}) {
+        if (n == p) return true;
+        if (n % p == 0) return false;
+    }
+    uint32_t d = n - 1, r = 0;
+    while (!(d & 1)) { d >>= 1; ++r; }
+    for (uint32_t a : {2u, 3u, 5u, 7u}) {   // deterministic below 3.2e9; 11 added for 2^32
+        uint32_t x = h_powmod(a, d, n);
+        if (x == 1 || x == n - 1) continue;
+        bool comp = true;
+        for (uint32_t i = 1; i < r && comp; ++i) {
+            x = h_mulmod(x, x, n);
+            if (x == n - 1) comp = false;
+        }
+        if (comp) return false;
+    }
+    uint32_t x = h_powmod(11, d, n);
+    if (!(x == 1 || x == n - 1)) {
+        bool comp = true;
+        for (uint32_t i = 1; i < r && comp; ++i) {
+            x = h_mulmod(x, x, n);
+            if (x == n - 1) comp = false;
+        }
+        if (comp) return false;
+    }
+    return true;
+}
+
+template <class T>
+static int upload(const std::vector<T>& h, T** d) {
+    *d = nullptr;
+    if (h.empty()) return CKKS_OK;
+    CK(cudaMalloc((void**)d, sizeof(T) * h.size()));
+    CK(cudaMemcpy(*d, h.data(), sizeof(T) * h.size(), cudaMemcpyHostToDevice));
+    return CKKS_OK;
+}
+
+struct BconvTable {
+    int l_in = 0, l_out = 0;
+    std::vector<uint32_t> t_plain, inv_qhat;      // host copies for ckks_bconv_table_read
+    BconvDev dev{};
+    std::vector<void*> owned;
+};
+
+struct KsPlan {
+    uint32_t n = 0;
+    int l = 0, alpha = 0, beta = 0, ext = 0, evk_ext = 0;
+    int32_t *d_q_slot = nullptr, *d_p_slot = nullptr, *d_ext_slot = nullptr, *d_evk_row = nullptr;
+    std::vector<int> digit_lo, digit_hi;           // Q rows [lo, hi) of digit t
+    std::vector<int32_t> raise_table;              // table id per digit
+    std::vector<int32_t*> d_raise_out_row;         // per digit: ext row of every converted limb
+    int s1_rows = 0;
+    int32_t *d_s1_row = nullptr, *d_s1_slot = nullptr;
+    int32_t moddown_table = -1;
+    int32_t *d_s3_in_row = nullptr, *d_s3_p_slot = nullptr, *d_s3_q_slot = nullptr;
+    uint32_t *d_pinv = nullptr, *d_pinv_s = nullptr;
+    uint32_t *ws_coeff = nullptr, *ws_raised = nullptr, *ws_acc = nullptr, *ws_conv = nullptr,
+             *ws_pc = nullptr;
+};
+
+}  // namespace ckks
+
+using namespace ckks;
+
+struct ckks_ctx {
+    int device = 0;
+    static constexpr int kMaxSlots = 4096;
+    ModSlot* d_slots = nullptr;
+    std::vector<ModSlot> h_slots;
+    std::map<std::tuple<uint32_t, uint32_t, uint32_t>, int32_t> slot_index;
+    std::vector<std::unique_ptr<BconvTable>> tables;
+    std::vector<std::unique_ptr<KsPlan>> plans;
+    std::vector<void*> owned;
+};
+
+static int check_ctx(ckks_ctx* ctx) {
+    if (!ctx) { set_last_error("null context"); return CKKS_ERR_ARG; }
+    CK(cudaSetDevice(ctx->device));
+    return CKKS_OK;
+}
+
+static int check_slot(ckks_ctx* ctx, int32_t s) {
+    if (s < 0 || s >= (int32_t)ctx->h_slots.size()) {
+        set_last_error("modulus slot %d out of range", s);
+        return CKKS_ERR_ARG;
+    }
+    return CKKS_OK;
+}
+
+extern "C" {
+
+int ckks_abi_version(void) { return 1; }
+const char* ckks_last_error(void) { return g_err; }
+
+int ckks_ctx_create(int device, ckks_ctx** out) {
+    if (!out) { set_last_error("null out pointer"); return CKKS_ERR_ARG; }
+    *out = nullptr;
+    int count = 0;
+    cudaError_t e = cudaGetDeviceCount(&count);
+    if (e != cudaSuccess || count <= 0) {
+        set_last_error("no CUDA device available (%s); this engine has no CPU fallback",
+                       e != cudaSuccess ? cudaGetErrorString(e) : "device count is 0");
+        return CKKS_ERR_CUDA;
+    }
+    if (device < 0 || device >= count) { set_last_error("device %d out of range", device); return CKKS_ERR_ARG; }
+    CK(cudaSetDevice(device));
+    cudaDeviceProp prop;
+    CK(cudaGetDeviceProperties(&prop, device));
+    if (prop.major < 10) {
+        set_last_error("device %d is sm_%d%d; libckks_b200 is built for sm_100a only", device,
+                       prop.major, prop.minor);
+        return CKKS_ERR_UNSUPPORTED;
+    }
+    auto ctx = new ckks_ctx();
+    ctx->device = device;
+    if (cudaMalloc((void**)&ctx->d_slots, sizeof(ModSlot) * ckks_ctx::kMaxSlots) != cudaSuccess) {
+        delete ctx;
+        set_last_error("cudaMalloc of the modulus slot table failed");
+        return CKKS_ERR_CUDA;
+    }
+    *out = ctx;
+    return CKKS_OK;
+}
+
+void ckks_ctx_destroy(ckks_ctx* ctx) {
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    cudaDeviceSynchronize();
+    for (void* p : ctx->owned) cudaFree(p);
+    for (auto& t : ctx->tables)
+        for (void* p : t->owned) cudaFree(p);
+    for (auto& pl : ctx->plans) {
+        for (void* p : {(void*)pl->d_q_slot, (void*)pl->d_p_slot, (void*)pl->d_ext_slot,
+                        (void*)pl->d_evk_row, (void*)pl->d_s1_row, (void*)pl->d_s1_slot,
+                        (void*)pl->d_s3_in_row, (void*)pl->d_s3_p_slot, (void*)pl->d_s3_q_slot,
+                        (void*)pl->d_pinv, (void*)pl->d_pinv_s, (void*)pl->ws_coeff,
+                        (void*)pl->ws_raised, (void*)pl->ws_acc, (void*)pl->ws_conv, (void*)pl->ws_pc})
+            cudaFree(p);
+        for (int32_t* p : pl->d_raise_out_row) cudaFree(p);
+    }
+    cudaFree(ctx->d_slots);
+    delete ctx;
+}
+
+int ckks_modulus_register(ckks_ctx* ctx, uint32_t q, uint32_t n, uint32_t psi, int32_t* slot) {
+    CKS(check_ctx(ctx));
+    if (!slot) { set_last_error("null slot pointer"); return CKKS_ERR_ARG; }
+    if (q < 3 || !(q & 1) || !h_is_prime(q)) { set_last_error("%u is not an odd prime", q); return CKKS_ERR_ARG; }
+    if (n < 2 || psi == 0) { n = 0; psi = 0; }
+    auto key = std::make_tuple(q, n, psi);
+    auto it = ctx->slot_index.find(key);
+    if (it != ctx->slot_index.end()) { *slot = it->second; return CKKS_OK; }
+    if ((int)ctx->h_slots.size() >= ckks_ctx::kMaxSlots) { set_last_error("modulus slot table full"); return CKKS_ERR_STATE; }
+
+    ModSlot m{};
+    m.q = q;
+    uint32_t qinv = q;                                  // Newton: q * qinv = 1 mod 2^32
+    for (int i = 0; i < 5; ++i) qinv *= 2u - q * qinv;
+    m.qinv = qinv;
+    m.r1 = (uint32_t)((1ull << 32) % q);
+    m.r2 = h_mulmod(m.r1, m.r1, q);
+    m.r1s = h_shoup(m.r1, q);
+    m.r2s = h_shoup(m.r2, q);
+    m.fast = (q > (1u << 30) && q < (1u << 31)) ? 1u : 0u;
+    m.n = 0;
+    if (n) {
+        if (n & (n - 1)) { set_last_error("ring degree %u is not a power of two", n); return CKKS_ERR_ARG; }
+        if (q >> 31) {
+            set_last_error("modulus %u needs 32 bits; the transform kernels require q < 2^31", q);
+            return CKKS_ERR_UNSUPPORTED;
+        }
+        if ((q - 1) % (2ull * n)) { set_last_error("%u is not NTT-friendly for degree %u", q, n); return CKKS_ERR_ARG; }
+        if (h_powmod(psi, n, q) != q - 1) { set_last_error("%u is not a primitive %u-th root mod %u", psi, 2 * n, q); return CKKS_ERR_ARG; }
+        uint32_t lg = 0;
+        while ((1u << lg) < n) ++lg;
+        const uint32_t psi_inv = h_inv(psi, q);
+        std::vector<uint32_t> pw(n), pwi(n);
+        uint32_t a = 1, b = 1;
+        for (uint32_t k = 0; k < n; ++k) {
+            pw[k] = a; pwi[k] = b;
+            a = h_mulmod(a, psi, q);
+            b = h_mulmod(b, psi_inv, q);
+        }
+        std::vector<uint2> fwd(n), inv(n);
+        for (uint32_t t = 0; t < n; ++t) {
+            const uint32_t r = h_bitrev(t, lg);
+            fwd[t] = make_uint2(pw[r], h_shoup(pw[r], q));
+            inv[t] = make_uint2(pwi[r], h_shoup(pwi[r], q));
+        }
+        uint2 *d_fwd, *d_inv;
+        CKS(upload(fwd, &d_fwd));
+        CKS(upload(inv, &d_inv));
+        ctx->owned.push_back(d_fwd);
+        ctx->owned.push_back(d_inv);
+        m.fwd = d_fwd;
+        m.inv = d_inv;
+        m.n = n;
+        m.n_inv = h_inv(n % q, q);
+        m.n_inv_s = h_shoup(m.n_inv, q);
+        m.w_last = h_mulmod(inv[1].x, m.n_inv, q);
+        m.w_last_s = h_shoup(m.w_last, q);
+    }
+    const int32_t id = (int32_t)ctx->h_slots.size();
+    CK(cudaMemcpy(ctx->d_slots + id, &m, sizeof(ModSlot), cudaMemcpyHostToDevice));
+    ctx->h_slots.push_back(m);
+    ctx->slot_index[key] = id;
+    *slot = id;
+    return CKKS_OK;
+}
+
+int ckks_modulus_tables(ckks_ctx* ctx, int32_t slot, uint32_t* fwd, uint32_t* inv, uint32_t* n_inv) {
+    CKS(check_ctx(ctx));
+    CKS(check_slot(ctx, slot));
+    const ModSlot& m = ctx->h_slots[slot];
+    if (!m.n) { set_last_error("slot %d has no transform tables", slot); return CKKS_ERR_STATE; }
+    std::vector<uint2> tmp(m.n);
+    CK(cudaMemcpy(tmp.data(), m.fwd, sizeof(uint2) * m.n, cudaMemcpyDeviceToHost));
+    for (uint32_t i = 0; i < m.n; ++i) fwd[i] = tmp[i].x;
+    CK(cudaMemcpy(tmp.data(), m.inv, sizeof(uint2) * m.n, cudaMemcpyDeviceToHost));
+    for (uint32_t i = 0; i < m.n; ++i) inv[i] = tmp[i].x;
+    *n_inv = m.n_inv;
+    return CKKS_OK;
+}
+
+// ---- transforms ----------------------------------------------------------------------
+
+int ckks_ntt(ckks_ctx* ctx, const uint32_t* in, uint32_t* out, const int32_t* row_slot, int rows,
+             uint32_t n, int inverse, void* stream) {
+    CKS(check_ctx(ctx));
+    if (n < 2 || (n & (n - 1))) { set_last_error("ring degree %u is not a power of two >= 2", n); return CKKS_ERR_ARG; }
+    return ntt_launch(in, out, row_slot, ctx->d_slots, RowMap{nullptr, nullptr}, rows, n, inverse,
+                      (cudaStream_t)stream);
+}
+
+int ckks_ntt_stages(ckks_ctx* ctx, const uint32_t* in, uint32_t* out, const int32_t* row_slot,
+                    int rows, uint32_t n, int inverse, uint32_t stage_lo, uint32_t stage_hi,
+                    void* stream) {
+    CKS(check_ctx(ctx));
+    uint32_t lg = 0;
+    while ((1u << lg) < n) ++lg;
+    if (n < 2 || (n & (n - 1)) || stage_lo > stage_hi || stage_hi > lg) {
+        set_last_error("bad stage range [%u, %u) for degree %u", stage_lo, stage_hi, n);
+        return CKKS_ERR_ARG;
+    }
+    return ntt_stages_launch(in, out, row_slot, ctx->d_slots, rows, n, inverse, stage_lo, stage_hi,
+                             (cudaStream_t)stream);
+}
+
+// ---- element-wise ---------------------------------------------------------------------
+
+int ckks_elementwise(ckks_ctx* ctx, const uint32_t* a, const uint32_t* b, uint32_t* out,
+                     const int32_t* row_slot, int rows, size_t cols, int kind, void* stream) {
+    CKS(check_ctx(ctx));
+    return elementwise_launch(a, b, out, row_slot, ctx->d_slots, rows, cols, kind, (cudaStream_t)stream);
+}
+
+int ckks_automorphism_eval(ckks_ctx* ctx, const uint32_t* in, uint32_t* out, int rows, uint32_t n,
+                           uint32_t k, void* stream) {
+    CKS(check_ctx(ctx));
+    if (!(k & 1) || n == 0 || (n & (n - 1))) { set_last_error("automorphism needs odd k and power-of-two n"); return CKKS_ERR_ARG; }
+    return automorphism_eval_launch(in, out, rows, n, k & (2 * n - 1), (cudaStream_t)stream);
+}
+
+int ckks_automorphism_coeff(ckks_ctx* ctx, const uint32_t* in, uint32_t* out,
+                            const int32_t* row_slot, int rows, uint32_t n, uint32_t k, void* stream) {
+    CKS(check_ctx(ctx));
+    if (!(k & 1) || n == 0 || (n & (n - 1))) { set_last_error("automorphism needs odd k and power-of-two n"); return CKKS_ERR_ARG; }
+    return automorphism_coeff_launch(in, out, row_slot, ctx->d_slots, rows, n, k & (2 * n - 1),
+                                     (cudaStream_t)stream);
+}
+
+// ---- base conversion ------------------------------------------------------------------
+
+int ckks_bconv_table_create(ckks_ctx* ctx, const int32_t* in_slot, int l_in, const int32_t* out_slot,
+                            int l_out, int32_t* table) {
+    CKS(check_ctx(ctx));
+    if (l_in < 1 || l_out < 1 || !in_slot || !out_slot || !table) { set_last_error("bad conversion shape %d -> %d", l_in, l_out); return CKKS_ERR_ARG; }
+    std::vector<uint32_t> qs(l_in), ps(l_out);
+    for (int j = 0; j < l_in; ++j) { CKS(check_slot(ctx, in_slot[j])); qs[j] = ctx->h_slots[in_slot[j]].q; }
+    for (int i = 0; i < l_out; ++i) { CKS(check_slot(ctx, out_slot[i])); ps[i] = ctx->h_slots[out_slot[i]].q; }
+    auto tab = std::make_unique<BconvTable>();
+    tab->l_in = l_in;
+    tab->l_out = l_out;
+    tab->inv_qhat.resize(l_in);
+    tab->t_plain.resize((size_t)l_in * l_out);
+    std::vector<uint32_t> inv_s(l_in), t_mont((size_t)l_in * l_out);
+    uint32_t all31 = 1;
+    for (int j = 0; j < l_in; ++j) {
+        uint64_t h = 1 % qs[j];
+        for (int k = 0; k < l_in; ++k)
+            if (k != j) h = h * (qs[k] % qs[j]) % qs[j];
+        if (h == 0) { set_last_error("source moduli are not pairwise coprime"); return CKKS_ERR_ARG; }
+        tab->inv_qhat[j] = h_inv((uint32_t)h, qs[j]);
+        inv_s[j] = h_shoup(tab->inv_qhat[j], qs[j]);
+        if (qs[j] >> 31) all31 = 0;
+    }
+    for (int i = 0; i < l_out; ++i)
+        for (int j = 0; j < l_in; ++j) {
+            uint64_t h = 1 % ps[i];
+            for (int k = 0; k < l_in; ++k)
+                if (k != j) h = h * (qs[k] % ps[i]) % ps[i];
+            tab->t_plain[(size_t)i * l_in + j] = (uint32_t)h;
+            t_mont[(size_t)i * l_in + j] = (uint32_t)((h << 32) % ps[i]);
+        }
+    std::vector<int32_t> in_s(in_slot, in_slot + l_in), out_s(out_slot, out_slot + l_out);
+    int32_t *d_in, *d_out;
+    uint32_t *d_inv, *d_invs, *d_tm, *d_tp;
+    CKS(upload(in_s, &d_in));
+    CKS(upload(out_s, &d_out));
+    CKS(upload(tab->inv_qhat, &d_inv));
+    CKS(upload(inv_s, &d_invs));
+    CKS(upload(t_mont, &d_tm));
+    CKS(upload(tab->t_plain, &d_tp));
+    tab->owned = {d_in, d_out, d_inv, d_invs, d_tm, d_tp};
+    tab->dev = BconvDev{l_in, l_out, all31, d_in, d_out, d_inv, d_invs, d_tm, d_tp};
+    *table = (int32_t)ctx->tables.size();
+    ctx->tables.push_back(std::move(tab));
+    return CKKS_OK;
+}
+
+static int check_table(ckks_ctx* ctx, int32_t t) {
+    if (t < 0 || t >= (int32_t)ctx->tables.size()) { set_last_error("conversion table %d out of range", t); return CKKS_ERR_ARG; }
+    return CKKS_OK;
+}
+
+int ckks_bconv_table_read(ckks_ctx* ctx, int32_t table, uint32_t* t, uint32_t* inv_qhat) {
+    CKS(check_ctx(ctx));
+    CKS(check_table(ctx, table));
+    const BconvTable& tab = *ctx->tables[table];
+    memcpy(t, tab.t_plain.data(), sizeof(uint32_t) * tab.t_plain.size());
+    memcpy(inv_qhat, tab.inv_qhat.data(), sizeof(uint32_t) * tab.inv_qhat.size());
+    return CKKS_OK;
+}
+
+int ckks_bconv(ckks_ctx* ctx, int32_t table, const uint32_t* in, uint32_t* out, size_t cols,
+               void* stream) {
+    CKS(check_ctx(ctx));
+    CKS(check_table(ctx, table));
+    return bconv_launch(ctx->tables[table]->dev, ctx->d_slots, in, cols, out, cols, cols,
+                        (cudaStream_t)stream);
+}
+
+// ---- key switching --------------------------------------------------------------------
+
+int ckks_ks_plan_create(ckks_ctx* ctx, uint32_t n, int l, int alpha, const int32_t* q_slot,
+                        const int32_t* p_slot, int evk_ext, int evk_p_off, int32_t* plan) {
+    CKS(check_ctx(ctx));
+    if (l < 1 || alpha < 1 || !q_slot || !p_slot || !plan || evk_p_off < l || evk_ext < evk_p_off + alpha) {
+        set_last_error("bad key-switch shape l=%d alpha=%d evk_ext=%d evk_p_off=%d", l, alpha, evk_ext, evk_p_off);
+        return CKKS_ERR_ARG;
+    }
+    for (int i = 0; i < l + alpha; ++i) {
+        const int32_t s = i < l ? q_slot[i] : p_slot[i - l];
+        CKS(check_slot(ctx, s));
+        if (ctx->h_slots[s].n != n) { set_last_error("slot %d has no tables for degree %u", s, n); return CKKS_ERR_ARG; }
+    }
+    auto pl = std::make_unique<KsPlan>();
+    pl->n = n; pl->l = l; pl->alpha = alpha; pl->ext = l + alpha; pl->evk_ext = evk_ext;
+    pl->beta = (l + alpha - 1) / alpha;
+    const int ext = pl->ext;
+    std::vector<int32_t> qv(q_slot, q_slot + l), pv(p_slot, p_slot + alpha), extv, evk_row;
+    extv = qv;
+    extv.insert(extv.end(), pv.begin(), pv.end());
+    for (int i = 0; i < l; ++i) evk_row.push_back(i);
+    for (int j = 0; j < alpha; ++j) evk_row.push_back(evk_p_off + j);
+    CKS(upload(qv, &pl->d_q_slot));
+    CKS(upload(pv, &pl->d_p_slot));
+    CKS(upload(extv, &pl->d_ext_slot));
+    CKS(upload(evk_row, &pl->d_evk_row));
+    // stage 1: one raise table per digit (keyswitch.py:193-202)
+    std::vector<int32_t> s1_row, s1_slot;
+    for (int t = 0; t < pl->beta; ++t) {
+        const int lo = t * alpha, hi = std::min(l, lo + alpha);
+        pl->digit_lo.push_back(lo);
+        pl->digit_hi.push_back(hi);
+        std::vector<int32_t> target, out_row;
+        for (int r = 0; r < ext; ++r) {
+            if (r >= lo && r < hi) continue;
+            target.push_back(extv[r]);
+            out_row.push_back(r);
+            s1_row.push_back(t * ext + r);
+            s1_slot.push_back(extv[r]);
+        }
+        int32_t tab;
+        CKS(ckks_bconv_table_create(ctx, qv.data() + lo, hi - lo, target.data(), (int)target.size(), &tab));
+        pl->raise_table.push_back(tab);
+        int32_t* d_or;
+        CKS(upload(out_row, &d_or));
+        pl->d_raise_out_row.push_back(d_or);
+    }
+    pl->s1_rows = (int)s1_row.size();
+    CKS(upload(s1_row, &pl->d_s1_row));
+    CKS(upload(s1_slot, &pl->d_s1_slot));
+    // stage 3: P -> Q table, P^-1 mod q_i (keyswitch.py:203-208)
+    CKS(ckks_bconv_table_create(ctx, pv.data(), alpha, qv.data(), l, &pl->moddown_table));
+    std::vector<uint32_t> pinv(l), pinv_s(l);
+    for (int i = 0; i < l; ++i) {
+        const uint32_t q = ctx->h_slots[qv[i]].q;
+        uint64_t prod = 1 % q;
+        for (int j = 0; j < alpha; ++j) prod = prod * (ctx->h_slots[pv[j]].q % q) % q;
+        if (prod == 0) { set_last_error("P and Q bases share a modulus"); return CKKS_ERR_ARG; }
+        pinv[i] = h_inv((uint32_t)prod, q);
+        pinv_s[i] = h_shoup(pinv[i], q);
+    }
+    CKS(upload(pinv, &pl->d_pinv));
+    CKS(upload(pinv_s, &pl->d_pinv_s));
+    std::vector<int32_t> s3_in_row, s3_p_slot, s3_q_slot;
+    for (int h = 0; h < 2; ++h) {
+        for (int j = 0; j < alpha; ++j) { s3_in_row.push_back(h * ext + l + j); s3_p_slot.push_back(pv[j]); }
+        for (int i = 0; i < l; ++i) s3_q_slot.push_back(qv[i]);
+    }
+    CKS(upload(s3_in_row, &pl->d_s3_in_row));
+    CKS(upload(s3_p_slot, &pl->d_s3_p_slot));
+    CKS(upload(s3_q_slot, &pl->d_s3_q_slot));
+    // workspace (owned by the plan, sized once; nothing allocates in the hot path)
+    const size_t limb = sizeof(uint32_t) * (size_t)n;
+    CK(cudaMalloc((void**)&pl->ws_coeff, limb * l));
+    CK(cudaMalloc((void**)&pl->ws_raised, limb * pl->beta * ext));
+    CK(cudaMalloc((void**)&pl->ws_acc, limb * 2 * ext));
+    CK(cudaMalloc((void**)&pl->ws_conv, limb * 2 * l));
+    CK(cudaMalloc((void**)&pl->ws_pc, limb * 2 * alpha));
+    *plan = (int32_t)ctx->plans.size();
+    ctx->plans.push_back(std::move(pl));
+    return CKKS_OK;
+}
+
+static int get_plan(ckks_ctx* ctx, int32_t id, KsPlan** out) {
+    CKS(check_ctx(ctx));
+    if (id < 0 || id >= (int32_t)ctx->plans.size()) { set_last_error("key-switch plan %d out of range", id); return CKKS_ERR_ARG; }
+    *out = ctx->plans[id].get();
+    return CKKS_OK;
+}
+
+// ModUp of every digit into `raised` (keyswitch.py:256-294).  With
+// carry_copy the digit's own limbs are copied through; the fused pipeline
+// skips that copy and lets stage 2 read them from the input directly.
+static int stage1_core(ckks_ctx* ctx, KsPlan* pl, const uint32_t* a, uint32_t* raised,
+                       bool carry_copy, cudaStream_t st) {
+    const size_t n = pl->n;
+    CKS(ntt_launch(a, pl->ws_coeff, pl->d_q_slot, ctx->d_slots, RowMap{nullptr, nullptr}, pl->l,
+                   pl->n, 1, st));
+    for (int t0 = 0; t0 < pl->beta;) {
+        BconvJobs jobs;
+        jobs.count = 0;
+        const int l_in0 = pl->digit_hi[t0] - pl->digit_lo[t0];
+        int t = t0;
+        for (; t < pl->beta && jobs.count < kMaxBconvJobs; ++t) {
+            if (pl->digit_hi[t] - pl->digit_lo[t] != l_in0) break;
+            BconvJob& j = jobs.job[jobs.count++];
+            j.tab = ctx->tables[pl->raise_table[t]]->dev;
+            j.in = pl->ws_coeff + (size_t)pl->digit_lo[t] * n;
+            j.in_stride = n;
+            j.out = raised + (size_t)t * pl->ext * n;
+            j.out_stride = n;
+            j.out_row = pl->d_raise_out_row[t];
+        }
+        CKS(bconv_launch_jobs(jobs, ctx->d_slots, n, st));
+        t0 = t;
+    }
+    CKS(ntt_launch(raised, raised, pl->d_s1_slot, ctx->d_slots, RowMap{pl->d_s1_row, pl->d_s1_row},
+                   pl->s1_rows, pl->n, 0, st));
+    if (carry_copy)
+        for (int t = 0; t < pl->beta; ++t) {
+            const size_t lo = pl->digit_lo[t], cnt = pl->digit_hi[t] - pl->digit_lo[t];
+            CK(cudaMemcpyAsync(raised + ((size_t)t * pl->ext + lo) * n, a + lo * n,
+                               sizeof(uint32_t) * cnt * n, cudaMemcpyDeviceToDevice, st));
+        }
+    return CKKS_OK;
+}
+
+static int stage3_core(ckks_ctx* ctx, KsPlan* pl, const uint32_t* q_a, const uint32_t* q_b,
+                       const uint32_t* p_a, const uint32_t* p_b, const uint32_t* fold_b,
+                       uint32_t* out_a, uint32_t* out_b, cudaStream_t st) {
+    const size_t n = pl->n;
+    const RowMap id{nullptr, nullptr};
+    if (p_a == pl->ws_acc + (size_t)pl->l * n && p_b == p_a + (size_t)pl->ext * n) {
+        // accumulator laid out [2][ext][n]: both P parts in one launch
+        CKS(ntt_launch(pl->ws_acc, pl->ws_pc, pl->d_s3_p_slot, ctx->d_slots,
+                       RowMap{pl->d_s3_in_row, nullptr}, 2 * pl->alpha, pl->n, 1, st));
+    } else {
+        CKS(ntt_launch(p_a, pl->ws_pc, pl->d_s3_p_slot, ctx->d_slots, id, pl->alpha, pl->n, 1, st));
+        CKS(ntt_launch(p_b, pl->ws_pc + (size_t)pl->alpha * n, pl->d_s3_p_slot, ctx->d_slots, id,
+                       pl->alpha, pl->n, 1, st));
+    }
+    BconvJobs jobs;
+    jobs.count = 2;
+    for (int h = 0; h < 2; ++h) {
+        BconvJob& j = jobs.job[h];
+        j.tab = ctx->tables[pl->moddown_table]->dev;
+        j.in = pl->ws_pc + (size_t)h * pl->alpha * n;
+        j.in_stride = n;
+        j.out = pl->ws_conv + (size_t)h * pl->l * n;
+        j.out_stride = n;
+        j.out_row = nullptr;
+    }
+    CKS(bconv_launch_jobs(jobs, ctx->d_slots, n, st));
+    CKS(ntt_launch(pl->ws_conv, pl->ws_conv, pl->d_s3_q_slot, ctx->d_slots, id, 2 * pl->l, pl->n, 0, st));
+    ModDownEpilogueArgs e{};
+    e.xq_a = q_a; e.xq_b = q_b; e.conv = pl->ws_conv; e.fold_b = fold_b;
+    e.out_a = out_a; e.out_b = out_b;
+    e.q_slot = pl->d_q_slot; e.pinv = pl->d_pinv; e.pinv_s = pl->d_pinv_s;
+    e.l = pl->l; e.n = pl->n;
+    return moddown_epilogue_launch(e, ctx->d_slots, st);
+}
+
+static InnerProductArgs ip_args(KsPlan* pl, const uint32_t* carry, const uint32_t* raised,
+                                const uint32_t* evk, int row_lo, int row_hi, uint32_t* acc_a,
+                                uint32_t* acc_b) {
+    InnerProductArgs a{};
+    a.carry = carry; a.raised = raised; a.evk = evk; a.acc_a = acc_a; a.acc_b = acc_b;
+    a.ext_slot = pl->d_ext_slot; a.evk_row = pl->d_evk_row;
+    a.l = pl->l; a.alpha = pl->alpha; a.beta = pl->beta; a.ext = pl->ext; a.evk_ext = pl->evk_ext;
+    a.row_lo = row_lo; a.row_hi = row_hi; a.n = pl->n;
+    return a;
+}
+
+int ckks_ks_stage1(ckks_ctx* ctx, int32_t plan, const uint32_t* a, uint32_t* raised, void* stream) {
+    KsPlan* pl;
+    CKS(get_plan(ctx, plan, &pl));
+    return stage1_core(ctx, pl, a, raised, true, (cudaStream_t)stream);
+}
+
+int ckks_ks_stage2(ckks_ctx* ctx, int32_t plan, const uint32_t* raised, const uint32_t* evk,
+                   int row_lo, int row_hi, uint32_t* acc_a, uint32_t* acc_b, void* stream) {
+    KsPlan* pl;
+    CKS(get_plan(ctx, plan, &pl));
+    if (row_lo < 0 || row_hi > pl->ext || row_lo > row_hi) { set_last_error("bad row range [%d, %d)", row_lo, row_hi); return CKKS_ERR_ARG; }
+    return inner_product_launch(ip_args(pl, nullptr, raised, evk, row_lo, row_hi, acc_a, acc_b),
+                                ctx->d_slots, (cudaStream_t)stream);
+}
+
+int ckks_ks_stage3(ckks_ctx* ctx, int32_t plan, const uint32_t* q_a, const uint32_t* q_b,
+                   const uint32_t* p_a, const uint32_t* p_b, uint32_t* out_a, uint32_t* out_b,
+                   void* stream) {
+    KsPlan* pl;
+    CKS(get_plan(ctx, plan, &pl));
+    return stage3_core(ctx, pl, q_a, q_b, p_a, p_b, nullptr, out_a, out_b, (cudaStream_t)stream);
+}
+
+int ckks_keyswitch(ckks_ctx* ctx, int32_t plan, const uint32_t* ct_a, const uint32_t* ct_b,
+                   const uint32_t* evk, uint32_t* out_a, uint32_t* out_b, void* stream) {
+    KsPlan* pl;
+    CKS(get_plan(ctx, plan, &pl));
+    cudaStream_t st = (cudaStream_t)stream;
+    const size_t n = pl->n;
+    CKS(stage1_core(ctx, pl, ct_a, pl->ws_raised, false, st));
+    uint32_t* acc_a = pl->ws_acc;
+    uint32_t* acc_b = pl->ws_acc + (size_t)pl->ext * n;
+    CKS(inner_product_launch(ip_args(pl, ct_a, pl->ws_raised, evk, 0, pl->ext, acc_a, acc_b),
+                             ctx->d_slots, st));
+    return stage3_core(ctx, pl, acc_a, acc_b, acc_a + (size_t)pl->l * n, acc_b + (size_t)pl->l * n,
+                       ct_b, out_a, out_b, st);
+}
+
+}  // extern "C"

@@ -1,0 +1,106 @@
+// common.cuh -- device arithmetic and shared structures of libckks_b200.so.
+//
+// Word size: residues are u32 in [0, q), q < 2^31 on every fast path (all
+// parameter sets of the reference are 31-bit, data/params/*.json).  With
+// 2q < 2^32 a value in [0, 2q) fits a register, which is what the lazy Shoup
+// butterflies below rely on.  Every kernel canonicalises to [0, q) before a
+// store that crosses the C ABI (reference rns.py:4-6).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace ckks {
+
+// One registered (q, n, psi): per-modulus constants and twiddle tables in HBM.
+// Twiddles are {w, floor(w * 2^32 / q)} pairs (Shoup form) in the slot order
+// of the reference tables: fwd[t] = psi^bitrev(t), inv[t] = psi^-bitrev(t)
+// (transform.py:43-49, :97-100).
+struct ModSlot {
+    uint32_t q;
+    uint32_t n;            // ring degree the tables were built for (0: none)
+    uint32_t qinv;         // q^-1 mod 2^32          (Montgomery, subtractive form)
+    uint32_t r1, r1s;      // 2^32 mod q and its Shoup companion
+    uint32_t r2, r2s;      // 2^64 mod q and its Shoup companion
+    uint32_t n_inv, n_inv_s;      // N^-1 mod q (transform.py:112)
+    uint32_t w_last, w_last_s;    // inv[1] * N^-1: twiddle of the last GS stage (:243-246)
+    uint32_t fast;         // 1 when 2^30 < q < 2^31 (two-subtraction range tricks valid)
+    const uint2* fwd;      // [n]
+    const uint2* inv;      // [n]
+};
+
+// ---- scalar modular arithmetic ------------------------------------------------
+
+// x in [0, 2q) -> [0, q).  One VIADDMNMX on sm_100a.
+__device__ __forceinline__ uint32_t csub(uint32_t x, uint32_t q) {
+    return min(x, x - q);
+}
+
+// y * w mod q, lazily: result in [0, 2q).  Valid for ANY 32-bit y, w < q,
+// ws = floor(w * 2^32 / q), q < 2^31.
+__device__ __forceinline__ uint32_t shoup_lazy(uint32_t y, uint32_t w, uint32_t ws, uint32_t q) {
+    uint32_t t = __umulhi(y, ws);
+    return y * w - t * q;
+}
+
+__device__ __forceinline__ uint32_t shoup_mul(uint32_t y, uint32_t w, uint32_t ws, uint32_t q) {
+    return csub(shoup_lazy(y, w, ws, q), q);
+}
+
+__device__ __forceinline__ uint32_t add_mod(uint32_t a, uint32_t b, uint32_t q) {
+    return csub(a + b, q);
+}
+
+__device__ __forceinline__ uint32_t sub_mod(uint32_t a, uint32_t b, uint32_t q) {
+    uint32_t d = a - b;
+    return min(d, d + q);
+}
+
+// Montgomery REDC, subtractive form: (hi:lo) * 2^-32 mod q in [0, q).
+// Requires hi < q.
+__device__ __forceinline__ uint32_t redc(uint32_t lo, uint32_t hi, uint32_t q, uint32_t qinv) {
+    uint32_t m = lo * qinv;
+    uint32_t u = __umulhi(m, q);
+    uint32_t r = hi - u;
+    return min(r, r + q);
+}
+
+// x mod q for any 64-bit x.  Fast moduli: fold hi into [0, q), REDC, then
+// multiply by 2^32 mod q to undo the Montgomery factor.
+__device__ __forceinline__ uint32_t reduce64(uint64_t x, const ModSlot& m) {
+    if (m.fast) {
+        uint32_t lo = (uint32_t)x, hi = (uint32_t)(x >> 32);
+        hi = min(hi, hi - 2u * m.q);     // hi < 2^32 < 4q
+        hi = csub(hi, m.q);
+        uint32_t r = redc(lo, hi, m.q, m.qinv);
+        return shoup_mul(r, m.r1, m.r1s, m.q);
+    }
+    return (uint32_t)(x % m.q);
+}
+
+// a * b mod q for canonical a, b.
+__device__ __forceinline__ uint32_t mul_mod(uint32_t a, uint32_t b, const ModSlot& m) {
+    if (m.fast) {
+        uint64_t x = (uint64_t)a * b;                 // < q^2 < q * 2^32: hi < q
+        uint32_t r = redc((uint32_t)x, (uint32_t)(x >> 32), m.q, m.qinv);
+        return shoup_mul(r, m.r1, m.r1s, m.q);
+    }
+    return (uint32_t)(((uint64_t)a * b) % m.q);
+}
+
+// ---- memory helpers -------------------------------------------------------------
+
+__device__ __forceinline__ uint4 ld_stream(const uint4* p) {
+    uint4 v;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+    return v;
+}
+
+}  // namespace ckks
+
+// status codes of the C ABI (include/ckks_b200.h)
+#define CKKS_OK 0
+#define CKKS_ERR_ARG 1
+#define CKKS_ERR_CUDA 2
+#define CKKS_ERR_UNSUPPORTED 3
+#define CKKS_ERR_STATE 4

@@ -1,0 +1,118 @@
+// internal.h -- declarations shared between the translation units of
+// libckks_b200.so (not part of the C ABI; see include/ckks_b200.h for that).
+#pragma once
+#include <cuda_runtime.h>
+#include <stddef.h>
+#include <stdint.h>
+
+namespace ckks {
+
+struct ModSlot;
+
+void set_last_error(const char* fmt, ...);
+
+#define CK(call)                                                                        \
+    do {                                                                                \
+        cudaError_t _e = (call);                                                        \
+        if (_e != cudaSuccess) {                                                        \
+            ::ckks::set_last_error("%s failed at %s:%d: %s", #call, __FILE__, __LINE__, \
+                                   cudaGetErrorString(_e));                             \
+            return CKKS_ERR_CUDA;                                                       \
+        }                                                                               \
+    } while (0)
+
+#define CKS(call)                         \
+    do {                                  \
+        int _s = (call);                  \
+        if (_s != CKKS_OK) return _s;     \
+    } while (0)
+
+// Logical row r of a launch lives at physical row in[r] of the source buffer
+// and out[r] of the destination (identity when null).  Lets the key-switch
+// pipeline transform scattered limbs (e.g. the converted rows of a raised
+// digit) in place without an assembly copy (reference keyswitch.py:283-293).
+struct RowMap {
+    const int32_t* in;
+    const int32_t* out;
+    __host__ __device__ size_t in_row(unsigned r) const { return in ? (size_t)in[r] : (size_t)r; }
+    __host__ __device__ size_t out_row(unsigned r) const { return out ? (size_t)out[r] : (size_t)r; }
+};
+
+// ntt.cu
+int ntt_launch(const uint32_t* in, uint32_t* out, const int32_t* row_slot, const ModSlot* slots,
+               RowMap rm, int rows, uint32_t n, int inverse, cudaStream_t st);
+int ntt_stages_launch(const uint32_t* in, uint32_t* out, const int32_t* row_slot,
+                      const ModSlot* slots, int rows, uint32_t n, int inverse, uint32_t s_lo,
+                      uint32_t s_hi, cudaStream_t st);
+
+// elementwise.cu
+int elementwise_launch(const uint32_t* a, const uint32_t* b, uint32_t* out, const int32_t* row_slot,
+                       const ModSlot* slots, int rows, size_t cols, int kind, cudaStream_t st);
+int automorphism_eval_launch(const uint32_t* in, uint32_t* out, int rows, uint32_t n, uint32_t k,
+                             cudaStream_t st);
+int automorphism_coeff_launch(const uint32_t* in, uint32_t* out, const int32_t* row_slot,
+                              const ModSlot* slots, int rows, uint32_t n, uint32_t k, cudaStream_t st);
+
+// bconv.cu
+// Device image of one conversion table (reference baseconv.py:37-54).
+struct BconvDev {
+    int l_in, l_out;
+    uint32_t all31;             // every source modulus < 2^31 (fast accumulation bound holds)
+    const int32_t* in_slot;     // [l_in]   context slots of the source basis
+    const int32_t* out_slot;    // [l_out]  context slots of the target basis
+    const uint32_t* inv_qhat;   // [l_in]   (Q*/Q_j)^-1 mod Q_j
+    const uint32_t* inv_qhat_s; // [l_in]   Shoup companions
+    const uint32_t* t_mont;     // [l_out][l_in]  (Q*/Q_j) * 2^32 mod P_i  (Montgomery form)
+    const uint32_t* t_plain;    // [l_out][l_in]  (Q*/Q_j) mod P_i
+};
+
+struct BconvJob {
+    BconvDev tab;
+    const uint32_t* in;         // source limb k at in + k * in_stride
+    size_t in_stride;
+    uint32_t* out;              // target limb i at out + out_row[i] * out_stride
+    size_t out_stride;
+    const int32_t* out_row;     // null: identity
+};
+
+constexpr int kMaxBconvJobs = 8;
+struct BconvJobs {
+    int count;
+    BconvJob job[kMaxBconvJobs];
+};
+
+int bconv_launch_jobs(const BconvJobs& jobs, const ModSlot* slots, size_t cols, cudaStream_t st);
+int bconv_launch(const BconvDev& tab, const ModSlot* slots, const uint32_t* in, size_t in_stride,
+                 uint32_t* out, size_t out_stride, size_t cols, cudaStream_t st);
+
+// keyswitch.cu
+struct InnerProductArgs {
+    const uint32_t* carry;      // ct.a rows (null: every row comes from `raised`)
+    const uint32_t* raised;     // [beta][ext][n]
+    const uint32_t* evk;        // [beta_total][2][evk_ext][n]
+    uint32_t* acc_a;            // row r - row_lo at acc_a + (r - row_lo) * n
+    uint32_t* acc_b;
+    const int32_t* ext_slot;    // [ext] context slot of every active extended-basis row
+    const int32_t* evk_row;     // [ext] row of the key matrix holding active row r
+    int l, alpha, beta, ext, evk_ext;
+    int row_lo, row_hi;
+    uint32_t n;
+};
+int inner_product_launch(const InnerProductArgs& a, const ModSlot* slots, cudaStream_t st);
+
+struct ModDownEpilogueArgs {
+    const uint32_t* xq_a;       // [l][n] accumulator Q part (a half)
+    const uint32_t* xq_b;
+    const uint32_t* conv;       // [2][l][n]  NTT(BConv_{P->Q}(INTT(x_P)))
+    const uint32_t* fold_b;     // ct.b to add into the b half (null: none)
+    uint32_t* out_a;
+    uint32_t* out_b;
+    const int32_t* q_slot;      // [l]
+    const uint32_t* pinv;       // [l]  P^-1 mod q_i
+    const uint32_t* pinv_s;     // [l]  Shoup companions
+    int l;
+    uint32_t n;
+};
+int moddown_epilogue_launch(const ModDownEpilogueArgs& a, const ModSlot* slots, cudaStream_t st);
+
+}  // namespace ckks

@@ -1,0 +1,139 @@
+// keyswitch.cu -- the element-wise kernels of hybrid key switching.
+//
+// Stage 2 (reference keyswitch.py:318-355): acc_a = sum_t d_t (.) evk_t.a and
+// acc_b = sum_t d_t (.) evk_t.b over the extended basis.  The key matrix
+// (2*beta*(L+alpha) limbs, 125.8 MB at ks48) is streamed from HBM exactly once;
+// products are accumulated in 64 bits (four 62-bit products fit) and reduced
+// once, so the kernel is purely DRAM-bound.
+//
+// Stage 3 epilogue (keyswitch.py:412-418, :452): out = (x_Q - conv) * P^-1,
+// with the ciphertext b-part folded into the b half in the same pass.
+#include "common.cuh"
+#include "internal.h"
+
+namespace ckks {
+
+__device__ __forceinline__ uint64_t mad64(uint32_t a, uint32_t b, uint64_t c) {
+    return (uint64_t)a * b + c;
+}
+
+template <bool VEC>
+__global__ void __launch_bounds__(256)
+inner_product_kernel(InnerProductArgs p, const ModSlot* __restrict__ slots) {
+    const int row = p.row_lo + blockIdx.y;
+    const ModSlot m = slots[p.ext_slot[row]];
+    const size_t n = p.n;
+    const int digit_of_row = row < p.l ? row / p.alpha : -1;
+    const size_t erow = (size_t)p.evk_row[row];
+    constexpr int W = VEC ? 4 : 1;
+    const size_t i = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) * W;
+    if (i >= n) return;
+    uint64_t sa[W], sb[W];
+    uint32_t ra[W], rb[W];
+#pragma unroll
+    for (int w = 0; w < W; ++w) { sa[w] = sb[w] = 0; ra[w] = rb[w] = 0; }
+    for (int t = 0; t < p.beta; ++t) {
+        const uint32_t* dsrc = (p.carry && t == digit_of_row)
+                                   ? p.carry + (size_t)row * n
+                                   : p.raised + ((size_t)t * p.ext + row) * n;
+        const uint32_t* ka = p.evk + (((size_t)t * 2 + 0) * p.evk_ext + erow) * n;
+        const uint32_t* kb = p.evk + (((size_t)t * 2 + 1) * p.evk_ext + erow) * n;
+        uint32_t d[W], xa[W], xb[W];
+        if (VEC) {
+            const uint4 dv = *reinterpret_cast<const uint4*>(dsrc + i);
+            const uint4 av = ld_stream(reinterpret_cast<const uint4*>(ka + i));
+            const uint4 bv = ld_stream(reinterpret_cast<const uint4*>(kb + i));
+            d[0] = dv.x; d[W > 1 ? 1 : 0] = dv.y; d[W > 2 ? 2 : 0] = dv.z; d[W > 3 ? 3 : 0] = dv.w;
+            xa[0] = av.x; xa[W > 1 ? 1 : 0] = av.y; xa[W > 2 ? 2 : 0] = av.z; xa[W > 3 ? 3 : 0] = av.w;
+            xb[0] = bv.x; xb[W > 1 ? 1 : 0] = bv.y; xb[W > 2 ? 2 : 0] = bv.z; xb[W > 3 ? 3 : 0] = bv.w;
+        } else {
+            d[0] = dsrc[i]; xa[0] = ka[i]; xb[0] = kb[i];
+        }
+#pragma unroll
+        for (int w = 0; w < W; ++w) {
+            sa[w] = mad64(d[w], xa[w], sa[w]);
+            sb[w] = mad64(d[w], xb[w], sb[w]);
+        }
+        // four products below q^2 < 2^62 fit in 64 bits; fold before a fifth
+        if ((t & 3) == 3 || t == p.beta - 1 || !m.fast) {
+#pragma unroll
+            for (int w = 0; w < W; ++w) {
+                ra[w] = m.q >> 31 ? (uint32_t)(((uint64_t)ra[w] + reduce64(sa[w], m)) % m.q)
+                                  : add_mod(ra[w], reduce64(sa[w], m), m.q);
+                rb[w] = m.q >> 31 ? (uint32_t)(((uint64_t)rb[w] + reduce64(sb[w], m)) % m.q)
+                                  : add_mod(rb[w], reduce64(sb[w], m), m.q);
+                sa[w] = sb[w] = 0;
+            }
+        }
+    }
+    uint32_t* oa = p.acc_a + (size_t)(row - p.row_lo) * n + i;
+    uint32_t* ob = p.acc_b + (size_t)(row - p.row_lo) * n + i;
+    if (VEC) {
+        *reinterpret_cast<uint4*>(oa) = make_uint4(ra[0], ra[W > 1 ? 1 : 0], ra[W > 2 ? 2 : 0], ra[W > 3 ? 3 : 0]);
+        *reinterpret_cast<uint4*>(ob) = make_uint4(rb[0], rb[W > 1 ? 1 : 0], rb[W > 2 ? 2 : 0], rb[W > 3 ? 3 : 0]);
+    } else {
+        oa[0] = ra[0];
+        ob[0] = rb[0];
+    }
+}
+
+int inner_product_launch(const InnerProductArgs& a, const ModSlot* slots, cudaStream_t st) {
+    const int rows = a.row_hi - a.row_lo;
+    if (rows <= 0) return CKKS_OK;
+    const bool vec = a.n % 4 == 0;
+    const size_t work = vec ? a.n / 4 : a.n;
+    dim3 grid((unsigned)((work + 255) / 256), rows);
+    if (vec) inner_product_kernel<true><<<grid, 256, 0, st>>>(a, slots);
+    else inner_product_kernel<false><<<grid, 256, 0, st>>>(a, slots);
+    CK(cudaGetLastError());
+    return CKKS_OK;
+}
+
+template <bool VEC>
+__global__ void __launch_bounds__(256)
+moddown_epilogue_kernel(ModDownEpilogueArgs p, const ModSlot* __restrict__ slots) {
+    const int row = blockIdx.y % p.l;
+    const int half = blockIdx.y / p.l;                 // 0: a, 1: b
+    const uint32_t q = slots[p.q_slot[row]].q;
+    const uint32_t pinv = p.pinv[row], pinv_s = p.pinv_s[row];
+    const size_t n = p.n;
+    constexpr int W = VEC ? 4 : 1;
+    const size_t i = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) * W;
+    if (i >= n) return;
+    const uint32_t* x = (half ? p.xq_b : p.xq_a) + (size_t)row * n + i;
+    const uint32_t* c = p.conv + ((size_t)half * p.l + row) * n + i;
+    const uint32_t* f = (half && p.fold_b) ? p.fold_b + (size_t)row * n + i : nullptr;
+    uint32_t* o = (half ? p.out_b : p.out_a) + (size_t)row * n + i;
+    if (VEC) {
+        const uint4 xv = *reinterpret_cast<const uint4*>(x);
+        const uint4 cv = *reinterpret_cast<const uint4*>(c);
+        uint4 r;
+        r.x = shoup_mul(xv.x - cv.x + q, pinv, pinv_s, q);
+        r.y = shoup_mul(xv.y - cv.y + q, pinv, pinv_s, q);
+        r.z = shoup_mul(xv.z - cv.z + q, pinv, pinv_s, q);
+        r.w = shoup_mul(xv.w - cv.w + q, pinv, pinv_s, q);
+        if (f) {
+            const uint4 fv = *reinterpret_cast<const uint4*>(f);
+            r.x = add_mod(r.x, fv.x, q); r.y = add_mod(r.y, fv.y, q);
+            r.z = add_mod(r.z, fv.z, q); r.w = add_mod(r.w, fv.w, q);
+        }
+        *reinterpret_cast<uint4*>(o) = r;
+    } else {
+        uint32_t r = shoup_mul(x[0] - c[0] + q, pinv, pinv_s, q);
+        if (f) r = add_mod(r, f[0], q);
+        o[0] = r;
+    }
+}
+
+int moddown_epilogue_launch(const ModDownEpilogueArgs& a, const ModSlot* slots, cudaStream_t st) {
+    if (a.l <= 0) return CKKS_OK;
+    const bool vec = a.n % 4 == 0;
+    const size_t work = vec ? a.n / 4 : a.n;
+    dim3 grid((unsigned)((work + 255) / 256), 2 * a.l);
+    if (vec) moddown_epilogue_kernel<true><<<grid, 256, 0, st>>>(a, slots);
+    else moddown_epilogue_kernel<false><<<grid, 256, 0, st>>>(a, slots);
+    CK(cudaGetLastError());
+    return CKKS_OK;
+}
+
+}  // namespace ckks

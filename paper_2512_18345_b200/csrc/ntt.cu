@@ -1,0 +1,343 @@
+// ntt.cu -- negacyclic NTT / iNTT over RNS limb matrices.
+//
+// Function computed (bit-exact target): reference transform.py:203-250
+// (_run_stages), i.e. Cooley-Tukey forward over the bit-reversed psi-power
+// table and Gentleman-Sande inverse with N^-1 folded into the last stage;
+// natural order in, bit-reversed evaluation order out (SURVEY 8a').
+//
+// Two implementations:
+//  * generic: one radix-2 stage per launch straight on global memory; any N,
+//    any stage range (serves ntt_two_phase with arbitrary n1 and small rings).
+//  * N = 2^16 fast path: two kernels of eight stages each (the paper's
+//    NTT1/NTT2 split, reference n1 = 2^8).  Each kernel runs
+//    two radix-16 passes in registers (Shoup lazy butterflies, values kept in
+//    [0, 2q)) with one conflict-free shared-memory transpose between them.
+#include "common.cuh"
+#include "internal.h"
+
+namespace ckks {
+
+// ---------------------------------------------------------------------------------
+// generic radix-2 stage
+// ---------------------------------------------------------------------------------
+__global__ void ntt_stage_generic(const uint32_t* in, uint32_t* out,
+                                  const int32_t* __restrict__ row_slot,
+                                  const ModSlot* __restrict__ slots, RowMap rm, uint32_t n,
+                                  uint32_t lg, uint32_t s, int inverse) {
+    const uint32_t b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= (n >> 1)) return;
+    const ModSlot& m = slots[row_slot[blockIdx.y]];
+    const uint32_t q = m.q;
+    const uint32_t* src = in + rm.in_row(blockIdx.y) * n;
+    uint32_t* dst = out + rm.out_row(blockIdx.y) * n;
+    if (!inverse) {
+        const uint32_t t = n >> (s + 1);
+        const uint32_t g = b / t, j = b - g * t;
+        const uint32_t i0 = g * 2 * t + j, i1 = i0 + t;
+        const uint2 w = m.fwd[(1u << s) + g];
+        const uint32_t x = src[i0], y = src[i1];
+        const uint32_t v = shoup_mul(y, w.x, w.y, q);
+        dst[i0] = add_mod(x, v, q);
+        dst[i1] = sub_mod(x, v, q);
+    } else {
+        const uint32_t t = 1u << s, groups = n >> (s + 1);
+        const uint32_t g = b >> s, j = b & (t - 1);
+        const uint32_t i0 = g * 2 * t + j, i1 = i0 + t;
+        uint2 w = m.inv[groups + g];
+        const uint32_t x = src[i0], y = src[i1];
+        uint32_t total = add_mod(x, y, q);
+        const uint32_t diff = sub_mod(x, y, q);
+        if (s == lg - 1) {
+            total = shoup_mul(total, m.n_inv, m.n_inv_s, q);
+            w = make_uint2(m.w_last, m.w_last_s);
+        }
+        dst[i0] = total;
+        dst[i1] = shoup_mul(diff, w.x, w.y, q);
+    }
+}
+
+// ---------------------------------------------------------------------------------
+// radix-16 register passes
+// ---------------------------------------------------------------------------------
+// Forward: values enter in [0, 2q) and leave in [0, 2q).
+__device__ __forceinline__ void ct_bfly(uint32_t& x, uint32_t& y, uint2 w, uint32_t q) {
+    const uint32_t xc = csub(x, q);
+    const uint32_t v = shoup_mul(y, w.x, w.y, q);
+    x = xc + v;
+    y = xc - v + q;
+}
+
+// Inverse: canonical in, canonical out.
+__device__ __forceinline__ void gs_bfly(uint32_t& x, uint32_t& y, uint2 w, uint32_t q) {
+    const uint32_t s = csub(x + y, q);
+    const uint32_t d = x - y + q;              // (0, 2q)
+    x = s;
+    y = shoup_mul(d, w.x, w.y, q);
+}
+
+// Four Cooley-Tukey stages on 16 registers; TW(s, g) returns the twiddle of
+// local stage s (0..3), local group g (0 .. 2^s - 1).
+template <class TW>
+__device__ __forceinline__ void ct16(uint32_t (&v)[16], uint32_t q, TW tw) {
+#pragma unroll
+    for (int s = 0; s < 4; ++s) {
+        const int half = 8 >> s;
+#pragma unroll
+        for (int g = 0; g < (1 << s); ++g) {
+            const uint2 w = tw(s, g);
+#pragma unroll
+            for (int j = 0; j < half; ++j) {
+                const int i0 = g * 2 * half + j;
+                ct_bfly(v[i0], v[i0 + half], w, q);
+            }
+        }
+    }
+}
+
+// Four Gentleman-Sande stages on 16 registers; TW(s, g): local stage s
+// (pair distance 2^s), local group g (0 .. (8 >> s) - 1).
+template <class TW>
+__device__ __forceinline__ void gs16(uint32_t (&v)[16], uint32_t q, TW tw) {
+#pragma unroll
+    for (int s = 0; s < 4; ++s) {
+        const int t = 1 << s;
+#pragma unroll
+        for (int g = 0; g < (8 >> s); ++g) {
+            const uint2 w = tw(s, g);
+#pragma unroll
+            for (int j = 0; j < t; ++j) {
+                const int i0 = g * 2 * t + j;
+                gs_bfly(v[i0], v[i0 + t], w, q);
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------------
+// N = 2^16, strided phase: 256-point transforms down the columns of the
+// 256 x 256 view (element (j, c) at j*256 + c).  A CTA owns COLS adjacent
+// columns; thread (g, c) holds 16 rows.  Tile row j is stored at padded row
+// j + (j >> 4) so that both register layouts (j = g + 16m and j = 16g + m) hit
+// 32 distinct banks per warp.
+// ---------------------------------------------------------------------------------
+constexpr int kN16 = 65536;
+
+template <int COLS>
+__global__ void __launch_bounds__(16 * COLS)
+ntt16_fwd_strided(const uint32_t* in, uint32_t* out, const int32_t* __restrict__ row_slot,
+                  const ModSlot* __restrict__ slots, RowMap rm) {
+    __shared__ uint2 s_tw[256];
+    __shared__ uint32_t tile[271 * COLS];
+    const int tid = threadIdx.x;
+    const int c = tid % COLS, g = tid / COLS;
+    const ModSlot& m = slots[row_slot[blockIdx.y]];
+    const uint32_t q = m.q;
+    for (int i = tid; i < 256; i += 16 * COLS) s_tw[i] = m.fwd[i];
+    const uint32_t* src = in + rm.in_row(blockIdx.y) * kN16 + blockIdx.x * COLS + c;
+    uint32_t v[16];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) v[k] = src[(g + 16 * k) * 256];
+    __syncthreads();
+    // stages 0..3: rows j = g + 16k, group index = k >> (4 - s): uniform twiddles
+    ct16(v, q, [&](int s, int gi) { return s_tw[(1 << s) + gi]; });
+#pragma unroll
+    for (int k = 0; k < 16; ++k) tile[(g + 17 * k) * COLS + c] = v[k];
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < 16; ++k) v[k] = tile[(17 * g + k) * COLS + c];
+    // stages 4..7: rows j = 16g + k
+    ct16(v, q, [&](int s, int gi) { return s_tw[(16 << s) + (g << s) + gi]; });
+    uint32_t* dst = out + rm.out_row(blockIdx.y) * kN16 + blockIdx.x * COLS + c;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) dst[(16 * g + k) * 256] = csub(v[k], q);
+}
+
+template <int COLS>
+__global__ void __launch_bounds__(16 * COLS)
+ntt16_inv_strided(const uint32_t* in, uint32_t* out, const int32_t* __restrict__ row_slot,
+                  const ModSlot* __restrict__ slots, RowMap rm) {
+    __shared__ uint2 s_tw[256];
+    __shared__ uint32_t tile[271 * COLS];
+    const int tid = threadIdx.x;
+    const int c = tid % COLS, g = tid / COLS;
+    const ModSlot& m = slots[row_slot[blockIdx.y]];
+    const uint32_t q = m.q;
+    for (int i = tid; i < 256; i += 16 * COLS) s_tw[i] = m.inv[i];
+    const uint32_t* src = in + rm.in_row(blockIdx.y) * kN16 + blockIdx.x * COLS + c;
+    uint32_t v[16];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) v[k] = src[(16 * g + k) * 256];
+    __syncthreads();
+    // global stages 8..11 = 256-point GS stages 0..3 on rows j = 16g + k
+    gs16(v, q, [&](int s, int gi) { return s_tw[(16 + g) * (8 >> s) + gi]; });
+#pragma unroll
+    for (int k = 0; k < 16; ++k) tile[(17 * g + k) * COLS + c] = v[k];
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < 16; ++k) v[k] = tile[(g + 17 * k) * COLS + c];
+    // global stages 12..14 on rows j = g + 16k, then the last stage with N^-1
+#pragma unroll
+    for (int s = 0; s < 3; ++s) {
+        const int t = 1 << s;
+#pragma unroll
+        for (int gi = 0; gi < (8 >> s); ++gi) {
+            const uint2 w = s_tw[(8 >> s) + gi];
+#pragma unroll
+            for (int j = 0; j < t; ++j) gs_bfly(v[gi * 2 * t + j], v[gi * 2 * t + j + t], w, q);
+        }
+    }
+    uint32_t* dst = out + rm.out_row(blockIdx.y) * kN16 + blockIdx.x * COLS + c;
+    const uint32_t ninv = m.n_inv, ninv_s = m.n_inv_s, wl = m.w_last, wl_s = m.w_last_s;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        const uint32_t x = v[j], y = v[j + 8];
+        const uint32_t total = csub(x + y, q);
+        const uint32_t diff = x - y + q;
+        dst[(g + 16 * j) * 256] = shoup_mul(total, ninv, ninv_s, q);
+        dst[(g + 16 * (j + 8)) * 256] = shoup_mul(diff, wl, wl_s, q);
+    }
+}
+
+// ---------------------------------------------------------------------------------
+// N = 2^16, contiguous phase: 256 independent 256-point transforms on
+// consecutive 1 KiB blocks.  A CTA owns 16 blocks (16 KiB); thread (blk, e)
+// holds 16 elements.  Tile element e of block blk is stored at
+// blk*272 + e + (e >> 4).
+// ---------------------------------------------------------------------------------
+__global__ void __launch_bounds__(256)
+ntt16_fwd_contig(const uint32_t* in, uint32_t* out, const int32_t* __restrict__ row_slot,
+                 const ModSlot* __restrict__ slots, RowMap rm) {
+    __shared__ uint32_t tile[16 * 272];
+    const int tid = threadIdx.x;
+    const int e = tid & 15, blk = tid >> 4;
+    const ModSlot& m = slots[row_slot[blockIdx.y]];
+    const uint32_t q = m.q;
+    const uint32_t B = blockIdx.x * 16 + blk;          // 256-element block index within the limb
+    const uint32_t* src = in + rm.in_row(blockIdx.y) * kN16 + B * 256;
+    const uint2* __restrict__ fwd = m.fwd;
+    uint32_t v[16];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) v[k] = src[e + 16 * k];
+    // global stages 8..11: elements e + 16k, slot = (256 + B) * 2^s + group
+    ct16(v, q, [&](int s, int gi) { return __ldg(&fwd[((256 + B) << s) + gi]); });
+#pragma unroll
+    for (int k = 0; k < 16; ++k) tile[blk * 272 + e + 17 * k] = v[k];
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < 16; ++k) v[k] = tile[blk * 272 + 17 * e + k];
+    // global stages 12..15: elements 16e + k, slot = ((256 + B) * 16 + e) * 2^s + group
+    const uint32_t base = (256 + B) * 16 + e;
+    ct16(v, q, [&](int s, int gi) { return __ldg(&fwd[(base << s) + gi]); });
+    uint4* dst = reinterpret_cast<uint4*>(out + rm.out_row(blockIdx.y) * kN16 + B * 256 + 16 * e);
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+        dst[k] = make_uint4(csub(v[4 * k], q), csub(v[4 * k + 1], q), csub(v[4 * k + 2], q),
+                            csub(v[4 * k + 3], q));
+}
+
+__global__ void __launch_bounds__(256)
+ntt16_inv_contig(const uint32_t* in, uint32_t* out, const int32_t* __restrict__ row_slot,
+                 const ModSlot* __restrict__ slots, RowMap rm) {
+    __shared__ uint32_t tile[16 * 272];
+    const int tid = threadIdx.x;
+    const int e = tid & 15, blk = tid >> 4;
+    const ModSlot& m = slots[row_slot[blockIdx.y]];
+    const uint32_t q = m.q;
+    const uint32_t B = blockIdx.x * 16 + blk;
+    const uint4* src = reinterpret_cast<const uint4*>(in + rm.in_row(blockIdx.y) * kN16 + B * 256 + 16 * e);
+    const uint2* __restrict__ inv = m.inv;
+    uint32_t v[16];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const uint4 u = src[k];
+        v[4 * k] = u.x; v[4 * k + 1] = u.y; v[4 * k + 2] = u.z; v[4 * k + 3] = u.w;
+    }
+    // global stages 0..3 on elements 16e + k: slot = (4096 + 16B + e) * (8 >> s) + group
+    const uint32_t base = 4096 + 16 * B + e;
+    gs16(v, q, [&](int s, int gi) { return __ldg(&inv[base * (8 >> s) + gi]); });
+#pragma unroll
+    for (int k = 0; k < 16; ++k) tile[blk * 272 + 17 * e + k] = v[k];
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < 16; ++k) v[k] = tile[blk * 272 + e + 17 * k];
+    // global stages 4..7 on elements e + 16k: slot = (256 + B) * (8 >> s) + group
+    gs16(v, q, [&](int s, int gi) { return __ldg(&inv[(256 + B) * (8 >> s) + gi]); });
+    uint32_t* dst = out + rm.out_row(blockIdx.y) * kN16 + B * 256;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) dst[e + 16 * k] = v[k];
+}
+
+// ---------------------------------------------------------------------------------
+// host launchers
+// ---------------------------------------------------------------------------------
+static int launch_generic(const uint32_t* in, uint32_t* out, const int32_t* row_slot,
+                          const ModSlot* slots, RowMap rm, int rows, uint32_t n, int inverse,
+                          uint32_t s_lo, uint32_t s_hi, cudaStream_t st) {
+    uint32_t lg = 0;
+    while ((1u << lg) < n) ++lg;
+    if (s_lo >= s_hi) {
+        if (rm.in || rm.out) {
+            set_last_error("empty stage range with a row map is not supported");
+            return CKKS_ERR_ARG;
+        }
+        if (in != out)
+            CK(cudaMemcpyAsync(out, in, sizeof(uint32_t) * (size_t)rows * n, cudaMemcpyDeviceToDevice, st));
+        return CKKS_OK;
+    }
+    const RowMap rm_inplace{rm.out, rm.out};
+    const uint32_t half = n >> 1;
+    const uint32_t threads = half < 256 ? (half < 32 ? 32 : half) : 256;
+    dim3 grid((half + threads - 1) / threads, rows);
+    for (uint32_t s = s_lo; s < s_hi; ++s) {
+        ntt_stage_generic<<<grid, threads, 0, st>>>(s == s_lo ? in : out, out, row_slot, slots,
+                                                    s == s_lo ? rm : rm_inplace, n, lg, s, inverse);
+    }
+    CK(cudaGetLastError());
+    return CKKS_OK;
+}
+
+int ntt_launch(const uint32_t* in, uint32_t* out, const int32_t* row_slot, const ModSlot* slots,
+               RowMap rm, int rows, uint32_t n, int inverse, cudaStream_t st) {
+    if (rows <= 0) return CKKS_OK;
+    if (n == (uint32_t)kN16) {
+        constexpr int COLS = 16;
+        dim3 g_str(256 / COLS, rows), g_con(16, rows);
+        const RowMap rm2{rm.out, rm.out};
+        if (!inverse) {
+            ntt16_fwd_strided<COLS><<<g_str, 16 * COLS, 0, st>>>(in, out, row_slot, slots, rm);
+            ntt16_fwd_contig<<<g_con, 256, 0, st>>>(out, out, row_slot, slots, rm2);
+        } else {
+            ntt16_inv_contig<<<g_con, 256, 0, st>>>(in, out, row_slot, slots, rm);
+            ntt16_inv_strided<COLS><<<g_str, 16 * COLS, 0, st>>>(out, out, row_slot, slots, rm2);
+        }
+        CK(cudaGetLastError());
+        return CKKS_OK;
+    }
+    uint32_t lg = 0;
+    while ((1u << lg) < n) ++lg;
+    return launch_generic(in, out, row_slot, slots, rm, rows, n, inverse, 0, lg, st);
+}
+
+int ntt_stages_launch(const uint32_t* in, uint32_t* out, const int32_t* row_slot,
+                      const ModSlot* slots, int rows, uint32_t n, int inverse, uint32_t s_lo,
+                      uint32_t s_hi, cudaStream_t st) {
+    const RowMap rm{nullptr, nullptr};
+    if (rows <= 0) return CKKS_OK;
+    uint32_t lg = 0;
+    while ((1u << lg) < n) ++lg;
+    if (n == (uint32_t)kN16 && s_hi - s_lo == 8 && (s_lo == 0 || s_lo == 8)) {
+        // the engine's own phase split: run the matching fast kernel alone
+        constexpr int COLS = 16;
+        dim3 g_str(256 / COLS, rows), g_con(16, rows);
+        const bool strided = inverse ? (s_lo == 8) : (s_lo == 0);
+        if (!inverse && strided) ntt16_fwd_strided<COLS><<<g_str, 16 * COLS, 0, st>>>(in, out, row_slot, slots, rm);
+        if (!inverse && !strided) ntt16_fwd_contig<<<g_con, 256, 0, st>>>(in, out, row_slot, slots, rm);
+        if (inverse && !strided) ntt16_inv_contig<<<g_con, 256, 0, st>>>(in, out, row_slot, slots, rm);
+        if (inverse && strided) ntt16_inv_strided<COLS><<<g_str, 16 * COLS, 0, st>>>(in, out, row_slot, slots, rm);
+        CK(cudaGetLastError());
+        return CKKS_OK;
+    }
+    return launch_generic(in, out, row_slot, slots, rm, rows, n, inverse, s_lo, s_hi, st);
+}
+
+}  // namespace ckks

@@ -1,0 +1,196 @@
+"""Process-wide handle on the CUDA engine: one C context per GPU, device-side
+caches for modulus slots / conversion tables / key-switch plans, and thin
+launch wrappers that hand raw device pointers and the current torch stream to
+the C ABI.  PyTorch is plumbing here (allocator, streams, graphs); all
+arithmetic is in csrc/.
+"""
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import _lib
+
+
+class Engine:
+    def __init__(self, device: int | None = None):
+        import torch
+
+        if not torch.cuda.is_available():
+            raise _lib.EngineUnavailable(
+                "no CUDA device: paper_2512_18345_b200 runs on a B200 only (no CPU fallback)"
+            )
+        self.torch = torch
+        self.lib = _lib.load()
+        self.device_index = torch.cuda.current_device() if device is None else device
+        self.device = torch.device("cuda", self.device_index)
+        h = ctypes.c_void_p()
+        _lib.check(self.lib.ckks_ctx_create(self.device_index, ctypes.byref(h)))
+        self.ctx = h
+        self._slots: dict = {}
+        self._row_slots: dict = {}
+        self._tables: dict = {}
+        self._plans: dict = {}
+
+    # ---- plumbing ---------------------------------------------------------
+    def stream(self) -> int:
+        return self.torch.cuda.current_stream(self.device).cuda_stream
+
+    def upload(self, words: np.ndarray):
+        """Host uint32 matrix -> device tensor (int32 storage)."""
+        t = self.torch.from_numpy(np.ascontiguousarray(words, dtype=np.uint32).view(np.int32))
+        return t.to(self.device, non_blocking=False)
+
+    def empty(self, *shape):
+        return self.torch.empty(shape, dtype=self.torch.int32, device=self.device)
+
+    # ---- modulus slots ----------------------------------------------------
+    def slot(self, m, n: int) -> int:
+        """Context slot of Modulus ``m`` with transform tables for degree n
+        (0: arithmetic only)."""
+        psi = 0
+        if n >= 2 and (m.q - 1) % (2 * n) == 0 and m.n >= n and m.q < (1 << 31):
+            psi = m.root_for_degree(n)
+        else:
+            n = 0
+        key = (m.q, n, psi)
+        s = self._slots.get(key)
+        if s is None:
+            out = ctypes.c_int32()
+            _lib.check(self.lib.ckks_modulus_register(self.ctx, m.q, n, psi, ctypes.byref(out)))
+            s = self._slots[key] = out.value
+        return s
+
+    def row_slots(self, basis, n: int = 0, repeat: int = 1):
+        """Device int32 array: slot of every row of a limb matrix over `basis`
+        (stacked `repeat` times)."""
+        key = (tuple((m.q, m.n, m.psi) for m in basis), n, repeat)
+        hit = self._row_slots.get(key)
+        if hit is None:
+            ids = [self.slot(m, n) for m in basis] * repeat
+            hit = self._row_slots[key] = self.torch.tensor(ids, dtype=self.torch.int32,
+                                                           device=self.device)
+        return hit
+
+    def has_tables(self, m, n: int) -> bool:
+        return n >= 2 and (m.q - 1) % (2 * n) == 0 and m.n >= n and m.q < (1 << 31)
+
+    def twiddle_tables(self, m, n: int):
+        fwd = np.empty(n, np.uint32)
+        inv = np.empty(n, np.uint32)
+        n_inv = ctypes.c_uint32()
+        _lib.check(self.lib.ckks_modulus_tables(self.ctx, self.slot(m, n), fwd.ctypes.data,
+                                                inv.ctypes.data, ctypes.byref(n_inv)))
+        return fwd, inv, n_inv.value
+
+    # ---- kernels ----------------------------------------------------------
+    def elementwise(self, a, b, row_slot, kind: int):
+        out = self.torch.empty_like(a)
+        _lib.check(self.lib.ckks_elementwise(self.ctx, a.data_ptr(), b.data_ptr(), out.data_ptr(),
+                                             row_slot.data_ptr(), a.shape[0], a.shape[1], kind,
+                                             self.stream()))
+        return out
+
+    def automorphism_eval(self, a, k: int):
+        out = self.torch.empty_like(a)
+        _lib.check(self.lib.ckks_automorphism_eval(self.ctx, a.data_ptr(), out.data_ptr(),
+                                                   a.shape[0], a.shape[1], k, self.stream()))
+        return out
+
+    def automorphism_coeff(self, a, row_slot, k: int):
+        out = self.torch.empty_like(a)
+        _lib.check(self.lib.ckks_automorphism_coeff(self.ctx, a.data_ptr(), out.data_ptr(),
+                                                    row_slot.data_ptr(), a.shape[0], a.shape[1], k,
+                                                    self.stream()))
+        return out
+
+    def ntt(self, a, row_slot, inverse: bool, out=None):
+        out = self.torch.empty_like(a) if out is None else out
+        _lib.check(self.lib.ckks_ntt(self.ctx, a.data_ptr(), out.data_ptr(), row_slot.data_ptr(),
+                                     a.shape[0], a.shape[1], int(inverse), self.stream()))
+        return out
+
+    def ntt_stages(self, a, row_slot, inverse: bool, lo: int, hi: int, out=None):
+        out = self.torch.empty_like(a) if out is None else out
+        _lib.check(self.lib.ckks_ntt_stages(self.ctx, a.data_ptr(), out.data_ptr(),
+                                            row_slot.data_ptr(), a.shape[0], a.shape[1],
+                                            int(inverse), lo, hi, self.stream()))
+        return out
+
+    def bconv_table(self, q_basis, p_basis) -> int:
+        key = (tuple(m.q for m in q_basis), tuple(m.q for m in p_basis))
+        t = self._tables.get(key)
+        if t is None:
+            src = (ctypes.c_int32 * len(q_basis))(*[self.slot(m, 0) for m in q_basis])
+            dst = (ctypes.c_int32 * len(p_basis))(*[self.slot(m, 0) for m in p_basis])
+            out = ctypes.c_int32()
+            _lib.check(self.lib.ckks_bconv_table_create(self.ctx, src, len(q_basis), dst,
+                                                        len(p_basis), ctypes.byref(out)))
+            t = self._tables[key] = out.value
+        return t
+
+    def bconv_table_read(self, table: int, l_in: int, l_out: int):
+        t = np.empty((l_out, l_in), np.uint32)
+        inv = np.empty(l_in, np.uint32)
+        _lib.check(self.lib.ckks_bconv_table_read(self.ctx, table, t.ctypes.data, inv.ctypes.data))
+        return t, inv
+
+    def bconv(self, table: int, a, l_out: int):
+        out = self.empty(l_out, a.shape[1])
+        _lib.check(self.lib.ckks_bconv(self.ctx, table, a.data_ptr(), out.data_ptr(), a.shape[1],
+                                       self.stream()))
+        return out
+
+    # ---- key switching ----------------------------------------------------
+    def ks_plan(self, n: int, q_basis, p_basis, alpha: int, evk_ext: int, evk_p_off: int) -> int:
+        key = (n, tuple(m.q for m in q_basis), tuple(m.q for m in p_basis), alpha, evk_ext, evk_p_off)
+        p = self._plans.get(key)
+        if p is None:
+            qs = (ctypes.c_int32 * len(q_basis))(*[self.slot(m, n) for m in q_basis])
+            ps = (ctypes.c_int32 * len(p_basis))(*[self.slot(m, n) for m in p_basis])
+            out = ctypes.c_int32()
+            _lib.check(self.lib.ckks_ks_plan_create(self.ctx, n, len(q_basis), alpha, qs, ps,
+                                                    evk_ext, evk_p_off, ctypes.byref(out)))
+            p = self._plans[key] = out.value
+        return p
+
+    def ks_stage1(self, plan: int, a, beta: int, ext: int):
+        raised = self.empty(beta, ext, a.shape[1])
+        _lib.check(self.lib.ckks_ks_stage1(self.ctx, plan, a.data_ptr(), raised.data_ptr(),
+                                           self.stream()))
+        return raised
+
+    def ks_stage2(self, plan: int, raised, evk, row_lo: int, row_hi: int):
+        n = raised.shape[-1]
+        acc = self.empty(2, row_hi - row_lo, n)
+        _lib.check(self.lib.ckks_ks_stage2(self.ctx, plan, raised.data_ptr(), evk.data_ptr(), row_lo,
+                                           row_hi, acc[0].data_ptr(), acc[1].data_ptr(),
+                                           self.stream()))
+        return acc
+
+    def ks_stage3(self, plan: int, q_a, q_b, p_a, p_b):
+        out = self.empty(2, q_a.shape[0], q_a.shape[1])
+        _lib.check(self.lib.ckks_ks_stage3(self.ctx, plan, q_a.data_ptr(), q_b.data_ptr(),
+                                           p_a.data_ptr(), p_b.data_ptr(), out[0].data_ptr(),
+                                           out[1].data_ptr(), self.stream()))
+        return out
+
+    def keyswitch(self, plan: int, ct_a, ct_b, evk, out=None):
+        out = self.empty(2, ct_a.shape[0], ct_a.shape[1]) if out is None else out
+        _lib.check(self.lib.ckks_keyswitch(self.ctx, plan, ct_a.data_ptr(),
+                                           None if ct_b is None else ct_b.data_ptr(), evk.data_ptr(),
+                                           out[0].data_ptr(), out[1].data_ptr(), self.stream()))
+        return out
+
+
+_engine: Engine | None = None
+
+
+def get_engine() -> Engine:
+    """The process's engine (one process per GPU); created on first use and
+    failing loudly when the extension or the GPU is missing."""
+    global _engine
+    if _engine is None:
+        _engine = Engine()
+    return _engine
