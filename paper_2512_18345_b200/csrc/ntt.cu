@@ -284,13 +284,21 @@ static int launch_generic(const uint32_t* in, uint32_t* out, const int32_t* row_
             CK(cudaMemcpyAsync(out, in, sizeof(uint32_t) * (size_t)rows * n, cudaMemcpyDeviceToDevice, st));
         return CKKS_OK;
     }
-    const RowMap rm_inplace{rm.out, rm.out};
     const uint32_t half = n >> 1;
     const uint32_t threads = half < 256 ? (half < 32 ? 32 : half) : 256;
-    dim3 grid((half + threads - 1) / threads, rows);
-    for (uint32_t s = s_lo; s < s_hi; ++s) {
-        ntt_stage_generic<<<grid, threads, 0, st>>>(s == s_lo ? in : out, out, row_slot, slots,
-                                                    s == s_lo ? rm : rm_inplace, n, lg, s, inverse);
+    // gridDim.y is capped at 65535: walk tall stacks (e.g. exhaustive small-ring tests) in slabs
+    for (int r0 = 0; r0 < rows; r0 += 65535) {
+        const int cnt = rows - r0 < 65535 ? rows - r0 : 65535;
+        dim3 grid((half + threads - 1) / threads, cnt);
+        const RowMap rm_first{rm.in ? rm.in + r0 : nullptr, rm.out ? rm.out + r0 : nullptr};
+        const RowMap rm_rest{rm_first.out, rm_first.out};
+        const size_t off_in = rm.in ? 0 : (size_t)r0 * n, off_out = rm.out ? 0 : (size_t)r0 * n;
+        for (uint32_t s = s_lo; s < s_hi; ++s) {
+            const bool first = s == s_lo;
+            ntt_stage_generic<<<grid, threads, 0, st>>>(first ? in + off_in : out + off_out,
+                                                        out + off_out, row_slot + r0, slots,
+                                                        first ? rm_first : rm_rest, n, lg, s, inverse);
+        }
     }
     CK(cudaGetLastError());
     return CKKS_OK;
