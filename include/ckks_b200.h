@@ -43,6 +43,14 @@ typedef struct ckks_ctx ckks_ctx;
 int ckks_abi_version(void);
 const char* ckks_last_error(void);
 
+/* Per-kernel device timing, the engine's analogue of the reference's op
+ * counters (instrument.py:11-32).  While enabled, every kernel launch is
+ * bracketed by CUDA events on its stream (do not enable during graph
+ * capture).  ckks_profile_read synchronises and writes one line
+ * "<kernel> <launches> <total_ms>" per kernel class into buf. */
+int ckks_profile_enable(int on);
+int ckks_profile_read(char* buf, size_t cap);
+
 /* ---- context ---------------------------------------------------------------- */
 
 /* One context per process per GPU: owns the modulus slots, twiddle tables,

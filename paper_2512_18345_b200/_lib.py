@@ -17,7 +17,7 @@ ABI_VERSION = 1
 
 # every symbol include/ckks_b200.h declares (checked by tests/test_abi.py)
 SYMBOLS = (
-    "ckks_abi_version", "ckks_last_error", "ckks_ctx_create", "ckks_ctx_destroy",
+    "ckks_abi_version", "ckks_last_error", "ckks_profile_enable", "ckks_profile_read", "ckks_ctx_create", "ckks_ctx_destroy",
     "ckks_modulus_register", "ckks_modulus_tables", "ckks_ntt", "ckks_ntt_stages",
     "ckks_elementwise", "ckks_automorphism_eval", "ckks_automorphism_coeff",
     "ckks_bconv_table_create", "ckks_bconv_table_read", "ckks_bconv",
@@ -58,6 +58,8 @@ def load() -> ctypes.CDLL:
     pi32, pu32 = ctypes.POINTER(i32), ctypes.POINTER(u32)
     L.ckks_abi_version.restype = ctypes.c_int
     L.ckks_last_error.restype = ctypes.c_char_p
+    L.ckks_profile_enable.argtypes = [ctypes.c_int]
+    L.ckks_profile_read.argtypes = [ctypes.c_char_p, sz]
     L.ckks_ctx_create.argtypes = [ctypes.c_int, ctypes.POINTER(vp)]
     L.ckks_ctx_destroy.argtypes = [vp]
     L.ckks_ctx_destroy.restype = None

@@ -7,6 +7,7 @@
 #include <cstring>
 #include <map>
 #include <memory>
+#include <string>
 #include <tuple>
 #include <vector>
 
@@ -23,6 +24,35 @@ void set_last_error(const char* fmt, ...) {
     va_start(ap, fmt);
     vsnprintf(g_err, sizeof(g_err), fmt, ap);
     va_end(ap);
+}
+
+// ---- optional kernel timing ----------------------------------------------------------
+struct ProfRec { int name; cudaEvent_t a, b; };
+static bool g_prof_on = false;
+static std::vector<ProfRec> g_prof;
+static std::vector<std::string> g_prof_names;
+static std::vector<cudaEvent_t> g_prof_pool;
+
+static cudaEvent_t prof_event() {
+    if (!g_prof_pool.empty()) { cudaEvent_t e = g_prof_pool.back(); g_prof_pool.pop_back(); return e; }
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    return e;
+}
+
+ProfScope::ProfScope(const char* name, cudaStream_t stream) : st(stream), live(g_prof_on) {
+    if (!live) return;
+    int id = -1;
+    for (size_t i = 0; i < g_prof_names.size(); ++i)
+        if (g_prof_names[i] == name) id = (int)i;
+    if (id < 0) { id = (int)g_prof_names.size(); g_prof_names.push_back(name); }
+    ProfRec r{id, prof_event(), prof_event()};
+    cudaEventRecord(r.a, st);
+    g_prof.push_back(r);
+}
+
+ProfScope::~ProfScope() {
+    if (live) cudaEventRecord(g_prof.back().b, st);
 }
 
 // ---- host number theory (setup only) -----------------------------------------------
@@ -139,6 +169,35 @@ extern "C" {
 
 int ckks_abi_version(void) { return 1; }
 const char* ckks_last_error(void) { return g_err; }
+
+int ckks_profile_enable(int on) {
+    for (auto& r : g_prof) { g_prof_pool.push_back(r.a); g_prof_pool.push_back(r.b); }
+    g_prof.clear();
+    g_prof_on = on != 0;
+    return CKKS_OK;
+}
+
+int ckks_profile_read(char* buf, size_t cap) {
+    if (!buf || cap == 0) { set_last_error("null profile buffer"); return CKKS_ERR_ARG; }
+    CK(cudaDeviceSynchronize());
+    std::vector<double> total(g_prof_names.size(), 0.0);
+    std::vector<int> count(g_prof_names.size(), 0);
+    for (auto& r : g_prof) {
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, r.a, r.b));
+        total[r.name] += ms;
+        count[r.name] += 1;
+    }
+    size_t at = 0;
+    buf[0] = 0;
+    for (size_t i = 0; i < g_prof_names.size(); ++i) {
+        if (!count[i]) continue;
+        int w = snprintf(buf + at, cap - at, "%s %d %.6f\n", g_prof_names[i].c_str(), count[i], total[i]);
+        if (w < 0 || (size_t)w >= cap - at) break;
+        at += (size_t)w;
+    }
+    return CKKS_OK;
+}
 
 int ckks_ctx_create(int device, ckks_ctx** out) {
     if (!out) { set_last_error("null out pointer"); return CKKS_ERR_ARG; }

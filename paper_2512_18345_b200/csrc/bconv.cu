@@ -104,6 +104,7 @@ int bconv_launch_jobs(const BconvJobs& jobs, const ModSlot* slots, size_t cols, 
         if (sm > 48 * 1024)                                                                \
             CK(cudaFuncSetAttribute(bconv_kernel<LIN>,                                     \
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));\
+        ProfScope ps("bconv", st);                                                      \
         bconv_kernel<LIN><<<grid, 256, sm, st>>>(jobs, slots, cols);                       \
     } while (0)
     if (l_in <= 1) BCONV_GO(1);

@@ -47,11 +47,13 @@ elementwise_scalar(const uint32_t* a, const uint32_t* b, uint32_t* out,
 int elementwise_launch(const uint32_t* a, const uint32_t* b, uint32_t* out, const int32_t* row_slot,
                        const ModSlot* slots, int rows, size_t cols, int kind, cudaStream_t st) {
     if (rows <= 0 || cols == 0) return CKKS_OK;
+    if (rows > 65535) { set_last_error("more than 65535 rows per launch is not supported"); return CKKS_ERR_UNSUPPORTED; }
     const bool vec = (cols % 4 == 0) && (((uintptr_t)a | (uintptr_t)b | (uintptr_t)out) % 16 == 0);
     const size_t work = vec ? cols / 4 : cols;
     unsigned gx = (unsigned)((work + 255) / 256);
     if (gx > 1024) gx = 1024;
     dim3 grid(gx, rows);
+    ProfScope ps("elementwise", st);
 #define EW_DISPATCH(K)                                                                             \
     if (vec)                                                                                       \
         elementwise_vec4<K><<<grid, 256, 0, st>>>((const uint4*)a, (const uint4*)b, (uint4*)out,   \
@@ -89,6 +91,7 @@ automorphism_eval_kernel(const uint32_t* __restrict__ in, uint32_t* __restrict__
 int automorphism_eval_launch(const uint32_t* in, uint32_t* out, int rows, uint32_t n, uint32_t k,
                              cudaStream_t st) {
     if (rows <= 0) return CKKS_OK;
+    if (rows > 65535) { set_last_error("more than 65535 rows per launch is not supported"); return CKKS_ERR_UNSUPPORTED; }
     if (in == out) { set_last_error("automorphism cannot run in place"); return CKKS_ERR_ARG; }
     uint32_t lg = 0;
     while ((1u << lg) < n) ++lg;
@@ -98,6 +101,7 @@ int automorphism_eval_launch(const uint32_t* in, uint32_t* out, int rows, uint32
     }
     unsigned gx = (n + 255) / 256;
     if (gx > 256) gx = 256;
+    ProfScope ps("automorphism_eval", st);
     automorphism_eval_kernel<<<dim3(gx, rows), 256, 0, st>>>(in, out, n, lg, k);
     CK(cudaGetLastError());
     return CKKS_OK;
@@ -123,9 +127,11 @@ automorphism_coeff_kernel(const uint32_t* __restrict__ in, uint32_t* __restrict_
 int automorphism_coeff_launch(const uint32_t* in, uint32_t* out, const int32_t* row_slot,
                               const ModSlot* slots, int rows, uint32_t n, uint32_t k, cudaStream_t st) {
     if (rows <= 0) return CKKS_OK;
+    if (rows > 65535) { set_last_error("more than 65535 rows per launch is not supported"); return CKKS_ERR_UNSUPPORTED; }
     if (in == out) { set_last_error("automorphism cannot run in place"); return CKKS_ERR_ARG; }
     unsigned gx = (n + 255) / 256;
     if (gx > 256) gx = 256;
+    ProfScope ps("automorphism_coeff", st);
     automorphism_coeff_kernel<<<dim3(gx, rows), 256, 0, st>>>(in, out, row_slot, slots, n, k);
     CK(cudaGetLastError());
     return CKKS_OK;

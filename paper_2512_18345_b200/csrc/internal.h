@@ -38,6 +38,15 @@ struct RowMap {
     __host__ __device__ size_t out_row(unsigned r) const { return out ? (size_t)out[r] : (size_t)r; }
 };
 
+// Optional per-kernel timing (api.cu): when enabled through ckks_profile_enable
+// every launch site below is bracketed by CUDA events on its own stream.
+struct ProfScope {
+    cudaStream_t st;
+    bool live;
+    ProfScope(const char* name, cudaStream_t stream);
+    ~ProfScope();
+};
+
 // ntt.cu
 int ntt_launch(const uint32_t* in, uint32_t* out, const int32_t* row_slot, const ModSlot* slots,
                RowMap rm, int rows, uint32_t n, int inverse, cudaStream_t st);
