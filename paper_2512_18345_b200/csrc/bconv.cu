@@ -9,117 +9,254 @@
 // Montgomery REDC, and the table is kept in Montgomery form (T * 2^32 mod P_i)
 // so that the REDC factor cancels and the result is the exact canonical residue.
 //
-// Column-parallel: one thread per column keeps the l_in pre-scaled residues in
-// registers and walks the output limbs; the table row is a broadcast read from
-// shared memory, stores are fully coalesced.  Several conversions (the beta
-// digits of stage 1, the two polynomials of stage 3) run as one launch.
+// Column-parallel: a thread keeps the l_in pre-scaled residues of one or two
+// adjacent columns in registers and walks the output limbs; the table row and
+// the per-limb constants are broadcast reads from shared memory, loads and
+// stores are coalesced.  Several conversions (the beta digits of stage 1, the
+// two polynomials of stage 3) run as one launch (blockIdx.y).
+//
+// bconv_fast: every modulus in (2^30, 2^31) -- all shipped parameter sets.
+// bconv_generic: any modulus < 2^32 (unit-test primes), '%' arithmetic.
+#include <cstdlib>
+
 #include "common.cuh"
 #include "internal.h"
 
 namespace ckks {
 
-struct OutMod {
-    uint32_t q, qinv, fast, pad;
-};
+// Output limbs are split over blockIdx.z in chunks of kOutChunk: one ciphertext has only
+// N = 2^16 columns, too few threads to fill 148 SMs unless the output walk is shared out
+// (the l_in pre-scale is recomputed per chunk: l_in Shoup products against l_in * kOutChunk MACs).
+constexpr int kOutChunk = 64;
 
-template <int LIN>
-__global__ void __launch_bounds__(256)
-bconv_kernel(BconvJobs jobs, const ModSlot* __restrict__ slots, size_t cols) {
-    extern __shared__ uint32_t smem[];
+template <int LIN, int CPT>
+__global__ void __launch_bounds__(128)
+bconv_fast(BconvJobs jobs, const ModSlot* __restrict__ slots, size_t cols) {
+    constexpr int G = (LIN + 3) / 4;         // groups of four terms
+    constexpr int LINP = 4 * G;
+    extern __shared__ uint4 sm4[];
     const BconvJob& job = jobs.job[blockIdx.y];
-    const int l_in = job.tab.l_in, l_out = job.tab.l_out;
-    // shared: table rows padded to LIN words, then per-output modulus constants
-    uint32_t* s_t = smem;                                   // [l_out][LIN]
-    OutMod* s_mod = reinterpret_cast<OutMod*>(smem + (size_t)l_out * LIN);
-    for (int idx = threadIdx.x; idx < l_out * LIN; idx += blockDim.x) {
-        const int i = idx / LIN, k = idx - i * LIN;
-        uint32_t v = 0;
-        if (k < l_in) {
-            const bool fast = slots[job.tab.out_slot[i]].fast;
-            v = fast ? job.tab.t_mont[i * l_in + k] : job.tab.t_plain[i * l_in + k];
-        }
-        s_t[idx] = v;
+    const int l_out = job.tab.l_out;
+    uint4* s_t = sm4;                        // [l_out][G]  Montgomery-form table rows
+    uint4* s_om = sm4 + (size_t)l_out * G;   // [l_out]     {q, qinv, out row, 2q}
+    uint4* s_in = s_om + l_out;              // [LIN]       {q, inv_qhat, shoup(inv_qhat), -}
+    uint32_t* s_tw = reinterpret_cast<uint32_t*>(s_t);
+    for (int idx = threadIdx.x; idx < l_out * LINP; idx += blockDim.x) {
+        const int i = idx / LINP, k = idx - i * LINP;
+        s_tw[idx] = k < LIN ? job.tab.t_mont[i * LIN + k] : 0u;
     }
     for (int i = threadIdx.x; i < l_out; i += blockDim.x) {
         const ModSlot& m = slots[job.tab.out_slot[i]];
-        s_mod[i] = OutMod{m.q, m.qinv, m.fast, 0};
+        s_om[i] = make_uint4(m.q, m.qinv, job.out_row ? (uint32_t)job.out_row[i] : (uint32_t)i, 2u * m.q);
     }
+    for (int k = threadIdx.x; k < LIN; k += blockDim.x)
+        s_in[k] = make_uint4(slots[job.tab.in_slot[k]].q, job.tab.inv_qhat[k], job.tab.inv_qhat_s[k], 0u);
+    __syncthreads();
+
+    const size_t c = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) * CPT;
+    if (c >= cols) return;
+    uint32_t y[CPT][LINP];
+#pragma unroll
+    for (int k = 0; k < LINP; ++k) {
+        if (k < LIN) {
+            const uint4 im = s_in[k];
+            const uint32_t* src = job.in + (size_t)k * job.in_stride + c;
+            if (CPT == 2) {
+                const uint2 a = *reinterpret_cast<const uint2*>(src);
+                y[0][k] = shoup_mul(a.x, im.y, im.z, im.x);
+                y[CPT - 1][k] = shoup_mul(a.y, im.y, im.z, im.x);
+            } else {
+                y[0][k] = shoup_mul(*src, im.y, im.z, im.x);
+            }
+        } else {
+#pragma unroll
+            for (int p = 0; p < CPT; ++p) y[p][k] = 0;
+        }
+    }
+    const int i_lo = blockIdx.z * kOutChunk, i_hi = min(l_out, i_lo + kOutChunk);
+#pragma unroll 2
+    for (int i = i_lo; i < i_hi; ++i) {
+        const uint4 om = s_om[i];
+        uint32_t r[CPT];
+#pragma unroll
+        for (int p = 0; p < CPT; ++p) r[p] = 0;
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+            const uint4 t = s_t[(size_t)i * G + g];
+#pragma unroll
+            for (int p = 0; p < CPT; ++p) {
+                uint64_t s = (uint64_t)t.x * y[p][4 * g];
+                s += (uint64_t)t.y * y[p][4 * g + 1];
+                s += (uint64_t)t.z * y[p][4 * g + 2];
+                s += (uint64_t)t.w * y[p][4 * g + 3];
+                uint32_t hi = (uint32_t)(s >> 32);
+                hi = min(hi, hi - om.w);               // hi < 2^32 < 4q
+                hi = csub(hi, om.x);
+                const uint32_t part = redc((uint32_t)s, hi, om.x, om.y);
+                r[p] = g == 0 ? part : add_mod(r[p], part, om.x);
+            }
+        }
+        uint32_t* dst = job.out + (size_t)om.z * job.out_stride + c;
+        if (CPT == 2) *reinterpret_cast<uint2*>(dst) = make_uint2(r[0], r[CPT - 1]);
+        else *dst = r[0];
+    }
+}
+
+// FP64-pipe variant.  B200 issues DFMA at the same rate as IMAD.lo (64/clk/SM,
+// profiles/microbench) on a pipe that is otherwise idle here, while IMAD.WIDE
+// costs ~2.8 slots of the integer FMA pipe.  Split y = y1 * 2^16 + y0: every
+// T * y0, T * y1 < 2^47 and the 12-term sums stay below 2^51, exact in a
+// double.  Seeding the accumulator with 2^52 leaves the integer sum in the low
+// 52 mantissa bits, so no float->int conversion is issued.  With T in
+// Montgomery form, V = A1_hi * (2^48 mod p) + A1_lo * 2^16 + A0 < 2^51 goes
+// through one REDC and yields the exact canonical residue.
+template <int LIN>
+__global__ void __launch_bounds__(128)
+bconv_f64(BconvJobs jobs, const ModSlot* __restrict__ slots, size_t cols) {
+    constexpr int LINP = (LIN + 1) / 2 * 2;
+    extern __shared__ uint4 sm4[];
+    const BconvJob& job = jobs.job[blockIdx.y];
+    const int l_out = job.tab.l_out;
+    double* s_t = reinterpret_cast<double*>(sm4);                                // [l_out][LINP]
+    uint4* s_om = sm4 + ((size_t)l_out * LINP * sizeof(double)) / sizeof(uint4); // {q, qinv, row, 2^48 mod q}
+    uint4* s_in = s_om + l_out;
+    for (int idx = threadIdx.x; idx < l_out * LINP; idx += blockDim.x) {
+        const int i = idx / LINP, k = idx - i * LINP;
+        s_t[idx] = k < LIN ? (double)job.tab.t_mont[i * LIN + k] : 0.0;
+    }
+    for (int i = threadIdx.x; i < l_out; i += blockDim.x) {
+        const ModSlot& m = slots[job.tab.out_slot[i]];
+        const uint32_t c48 = (uint32_t)(((uint64_t)m.r1 << 16) % m.q);
+        s_om[i] = make_uint4(m.q, m.qinv, job.out_row ? (uint32_t)job.out_row[i] : (uint32_t)i, c48);
+    }
+    for (int k = threadIdx.x; k < LIN; k += blockDim.x)
+        s_in[k] = make_uint4(slots[job.tab.in_slot[k]].q, job.tab.inv_qhat[k], job.tab.inv_qhat_s[k], 0u);
     __syncthreads();
 
     const size_t c = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (c >= cols) return;
-    uint32_t y[LIN];
+    double y0[LINP], y1[LINP];
 #pragma unroll
-    for (int k = 0; k < LIN; ++k) {
-        y[k] = 0;
-        if (k < l_in) {
-            const ModSlot& m = slots[job.tab.in_slot[k]];
-            const uint32_t a = job.in[(size_t)k * job.in_stride + c];
-            y[k] = m.q >> 31 ? (uint32_t)((uint64_t)a * job.tab.inv_qhat[k] % m.q)
-                             : shoup_mul(a, job.tab.inv_qhat[k], job.tab.inv_qhat_s[k], m.q);
+    for (int k = 0; k < LINP; ++k) {
+        y0[k] = y1[k] = 0.0;
+        if (k < LIN) {
+            const uint4 im = s_in[k];
+            const uint32_t y = shoup_mul(job.in[(size_t)k * job.in_stride + c], im.y, im.z, im.x);
+            y0[k] = (double)(y & 0xFFFFu);
+            y1[k] = (double)(y >> 16);
         }
     }
+    const double seed = 4503599627370496.0;     // 2^52
+    const int i_lo = blockIdx.z * kOutChunk, i_hi = min(l_out, i_lo + kOutChunk);
+#pragma unroll 2
+    for (int i = i_lo; i < i_hi; ++i) {
+        const uint4 om = s_om[i];
+        const double2* trow = reinterpret_cast<const double2*>(s_t + (size_t)i * LINP);
+        double a0 = seed, a1 = seed;
+#pragma unroll
+        for (int k = 0; k < LINP; k += 2) {
+            const double2 t = trow[k / 2];
+            a0 = fma(t.x, y0[k], a0);
+            a1 = fma(t.x, y1[k], a1);
+            a0 = fma(t.y, y0[k + 1], a0);
+            a1 = fma(t.y, y1[k + 1], a1);
+        }
+        const uint64_t b0 = (uint64_t)__double_as_longlong(a0) & 0xFFFFFFFFFFFFFull;
+        const uint64_t b1 = (uint64_t)__double_as_longlong(a1) & 0xFFFFFFFFFFFFFull;
+        const uint64_t v = (uint64_t)(uint32_t)(b1 >> 32) * om.w + ((b1 & 0xFFFFFFFFull) << 16) + b0;
+        job.out[(size_t)om.z * job.out_stride + c] = redc((uint32_t)v, (uint32_t)(v >> 32), om.x, om.y);
+    }
+}
+
+// Any modulus below 2^32; one column per thread; exact '%' folds.
+__global__ void __launch_bounds__(128)
+bconv_generic(BconvJobs jobs, const ModSlot* __restrict__ slots, size_t cols) {
+    const BconvJob& job = jobs.job[blockIdx.y];
+    const int l_in = job.tab.l_in, l_out = job.tab.l_out;
+    const size_t c = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= cols) return;
     for (int i = 0; i < l_out; ++i) {
-        const OutMod om = s_mod[i];
-        const uint32_t* trow = s_t + (size_t)i * LIN;
-        uint32_t r = 0;
-        if (om.fast && job.tab.all31) {
-#pragma unroll
-            for (int k0 = 0; k0 < LIN; k0 += 4) {
-                uint64_t s = 0;
-#pragma unroll
-                for (int k = k0; k < k0 + 4 && k < LIN; ++k) s += (uint64_t)trow[k] * y[k];
-                uint32_t hi = (uint32_t)(s >> 32);
-                hi = min(hi, hi - 2u * om.q);
-                hi = csub(hi, om.q);
-                r = add_mod(r, redc((uint32_t)s, hi, om.q, om.qinv), om.q);
-            }
-        } else {
-            // small or 32-bit target modulus (unit tests): exact 128-bit-free fold
-            uint64_t acc = 0;
-#pragma unroll
-            for (int k = 0; k < LIN; ++k) acc = (acc + (uint64_t)trow[k] * y[k] % om.q) % om.q;
-            r = (uint32_t)acc;
+        const uint64_t p = slots[job.tab.out_slot[i]].q;
+        uint64_t acc = 0;
+        for (int k = 0; k < l_in; ++k) {
+            const uint64_t q = slots[job.tab.in_slot[k]].q;
+            const uint64_t y = (uint64_t)job.in[(size_t)k * job.in_stride + c] * job.tab.inv_qhat[k] % q;
+            acc = (acc + (uint64_t)job.tab.t_plain[i * l_in + k] * y % p) % p;
         }
         const size_t orow = job.out_row ? (size_t)job.out_row[i] : (size_t)i;
-        job.out[orow * job.out_stride + c] = r;
+        job.out[orow * job.out_stride + c] = (uint32_t)acc;
     }
+}
+
+static int bconv_variant() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("CKKS_BCONV");
+        v = (e && e[0] == 'f') ? 1 : 0;       // default: IMAD.WIDE kernel; CKKS_BCONV=f64: FP64-pipe kernel
+    }
+    return v;
+}
+
+template <int LIN>
+static int launch_fast(const BconvJobs& jobs, const ModSlot* slots, size_t cols, int l_out_max,
+                       bool pairs, cudaStream_t st) {
+    if (bconv_variant() == 1) {
+        constexpr int LINP = (LIN + 1) / 2 * 2;
+        const size_t sm = sizeof(double) * (size_t)l_out_max * LINP + sizeof(uint4) * ((size_t)l_out_max + LIN);
+        dim3 grid((unsigned)((cols + 127) / 128), jobs.count, (l_out_max + kOutChunk - 1) / kOutChunk);
+        ProfScope ps("bconv", st);
+        if (sm > 48 * 1024)
+            CK(cudaFuncSetAttribute(bconv_f64<LIN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+        bconv_f64<LIN><<<grid, 128, sm, st>>>(jobs, slots, cols);
+        CK(cudaGetLastError());
+        return CKKS_OK;
+    }
+    constexpr int G = (LIN + 3) / 4;
+    const size_t sm = sizeof(uint4) * ((size_t)l_out_max * G + l_out_max + LIN);
+    const size_t work = pairs ? cols / 2 : cols;
+    dim3 grid((unsigned)((work + 127) / 128), jobs.count, (l_out_max + kOutChunk - 1) / kOutChunk);
+    ProfScope ps("bconv", st);
+    if (pairs) {
+        if (sm > 48 * 1024)
+            CK(cudaFuncSetAttribute(bconv_fast<LIN, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+        bconv_fast<LIN, 2><<<grid, 128, sm, st>>>(jobs, slots, cols);
+    } else {
+        if (sm > 48 * 1024)
+            CK(cudaFuncSetAttribute(bconv_fast<LIN, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+        bconv_fast<LIN, 1><<<grid, 128, sm, st>>>(jobs, slots, cols);
+    }
+    CK(cudaGetLastError());
+    return CKKS_OK;
 }
 
 int bconv_launch_jobs(const BconvJobs& jobs, const ModSlot* slots, size_t cols, cudaStream_t st) {
     if (jobs.count <= 0 || cols == 0) return CKKS_OK;
     const int l_in = jobs.job[0].tab.l_in;
     int l_out_max = 0;
+    bool fast = true, pairs = cols % 2 == 0;
     for (int j = 0; j < jobs.count; ++j) {
-        if (jobs.job[j].tab.l_in != l_in) {
+        const BconvJob& jb = jobs.job[j];
+        if (jb.tab.l_in != l_in) {
             set_last_error("stacked conversions must share l_in");
             return CKKS_ERR_ARG;
         }
-        if (jobs.job[j].tab.l_out > l_out_max) l_out_max = jobs.job[j].tab.l_out;
+        if (jb.tab.l_out > l_out_max) l_out_max = jb.tab.l_out;
+        fast = fast && jb.tab.all31;
+        pairs = pairs && (((uintptr_t)jb.in | (uintptr_t)jb.out) % 8 == 0) &&
+                jb.in_stride % 2 == 0 && jb.out_stride % 2 == 0;
     }
-    dim3 grid((unsigned)((cols + 255) / 256), jobs.count);
-#define BCONV_GO(LIN)                                                                      \
-    do {                                                                                   \
-        size_t sm = (size_t)l_out_max * LIN * 4 + (size_t)l_out_max * sizeof(OutMod);      \
-        if (sm > 48 * 1024)                                                                \
-            CK(cudaFuncSetAttribute(bconv_kernel<LIN>,                                     \
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));\
-        ProfScope ps("bconv", st);                                                      \
-        bconv_kernel<LIN><<<grid, 256, sm, st>>>(jobs, slots, cols);                       \
-    } while (0)
-    if (l_in <= 1) BCONV_GO(1);
-    else if (l_in <= 2) BCONV_GO(2);
-    else if (l_in <= 4) BCONV_GO(4);
-    else if (l_in <= 8) BCONV_GO(8);
-    else if (l_in <= 12) BCONV_GO(12);
-    else if (l_in <= 16) BCONV_GO(16);
-    else if (l_in <= 24) BCONV_GO(24);
-    else if (l_in <= 32) BCONV_GO(32);
-    else {
-        set_last_error("base conversion from %d limbs is not supported (max 32)", l_in);
-        return CKKS_ERR_UNSUPPORTED;
+    if (fast && l_in <= 16) {
+        switch (l_in) {
+#define BCONV_CASE(L) case L: return launch_fast<L>(jobs, slots, cols, l_out_max, pairs, st);
+            BCONV_CASE(1) BCONV_CASE(2) BCONV_CASE(3) BCONV_CASE(4) BCONV_CASE(5) BCONV_CASE(6)
+            BCONV_CASE(7) BCONV_CASE(8) BCONV_CASE(9) BCONV_CASE(10) BCONV_CASE(11) BCONV_CASE(12)
+            BCONV_CASE(13) BCONV_CASE(14) BCONV_CASE(15) BCONV_CASE(16)
+#undef BCONV_CASE
+        }
     }
-#undef BCONV_GO
+    dim3 grid((unsigned)((cols + 127) / 128), jobs.count);
+    ProfScope ps("bconv_generic", st);
+    bconv_generic<<<grid, 128, 0, st>>>(jobs, slots, cols);
     CK(cudaGetLastError());
     return CKKS_OK;
 }

@@ -66,7 +66,7 @@ int automorphism_coeff_launch(const uint32_t* in, uint32_t* out, const int32_t* 
 // Device image of one conversion table (reference baseconv.py:37-54).
 struct BconvDev {
     int l_in, l_out;
-    uint32_t all31;             // every source modulus < 2^31 (fast accumulation bound holds)
+    uint32_t all31;             // sources < 2^31 and targets in (2^30, 2^31): bconv_fast applies
     const int32_t* in_slot;     // [l_in]   context slots of the source basis
     const int32_t* out_slot;    // [l_out]  context slots of the target basis
     const uint32_t* inv_qhat;   // [l_in]   (Q*/Q_j)^-1 mod Q_j

@@ -59,59 +59,59 @@ __global__ void ntt_stage_generic(const uint32_t* in, uint32_t* out,
 // ---------------------------------------------------------------------------------
 // radix-16 register passes
 // ---------------------------------------------------------------------------------
-// Forward: values enter in [0, 2q) and leave in [0, 2q).
-__device__ __forceinline__ void ct_bfly(uint32_t& x, uint32_t& y, uint2 w, uint32_t q) {
+// Forward: values enter in [0, 2q) and leave in [0, 2q).  `v` = y * w mod q, canonical.
+__device__ __forceinline__ void ct_bfly(uint32_t& x, uint32_t& y, uint32_t v, uint32_t q) {
     const uint32_t xc = csub(x, q);
-    const uint32_t v = shoup_mul(y, w.x, w.y, q);
     x = xc + v;
     y = xc - v + q;
 }
 
-// Inverse: canonical in, canonical out.
-__device__ __forceinline__ void gs_bfly(uint32_t& x, uint32_t& y, uint2 w, uint32_t q) {
-    const uint32_t s = csub(x + y, q);
-    const uint32_t d = x - y + q;              // (0, 2q)
-    x = s;
-    y = shoup_mul(d, w.x, w.y, q);
-}
-
-// Four Cooley-Tukey stages on 16 registers; TW(s, g) returns the twiddle of
-// local stage s (0..3), local group g (0 .. 2^s - 1).
-template <class TW>
-__device__ __forceinline__ void ct16(uint32_t (&v)[16], uint32_t q, TW tw) {
+// Four Cooley-Tukey stages on 16 registers.  MUL(s, g, y) returns y * w mod q in
+// [0, q) for the twiddle of local stage s (0..3), local group g (0 .. 2^s - 1).
+template <class MUL>
+__device__ __forceinline__ void ct16(uint32_t (&v)[16], uint32_t q, MUL mul) {
 #pragma unroll
     for (int s = 0; s < 4; ++s) {
         const int half = 8 >> s;
 #pragma unroll
         for (int g = 0; g < (1 << s); ++g) {
-            const uint2 w = tw(s, g);
 #pragma unroll
             for (int j = 0; j < half; ++j) {
                 const int i0 = g * 2 * half + j;
-                ct_bfly(v[i0], v[i0 + half], w, q);
+                ct_bfly(v[i0], v[i0 + half], mul(s, g, v[i0 + half]), q);
             }
         }
     }
 }
 
-// Four Gentleman-Sande stages on 16 registers; TW(s, g): local stage s
-// (pair distance 2^s), local group g (0 .. (8 >> s) - 1).
-template <class TW>
-__device__ __forceinline__ void gs16(uint32_t (&v)[16], uint32_t q, TW tw) {
+// Four Gentleman-Sande stages on 16 registers, canonical in and out.
+// MUL(s, g, d): d * w mod q in [0, q) for local stage s (pair distance 2^s),
+// local group g (0 .. (8 >> s) - 1); d may be any 32-bit value.
+template <class MUL>
+__device__ __forceinline__ void gs16(uint32_t (&v)[16], uint32_t q, MUL mul, int stages = 4) {
 #pragma unroll
     for (int s = 0; s < 4; ++s) {
+        if (s >= stages) break;
         const int t = 1 << s;
 #pragma unroll
         for (int g = 0; g < (8 >> s); ++g) {
-            const uint2 w = tw(s, g);
 #pragma unroll
             for (int j = 0; j < t; ++j) {
                 const int i0 = g * 2 * t + j;
-                gs_bfly(v[i0], v[i0 + t], w, q);
+                const uint32_t x = v[i0], y = v[i0 + t];
+                v[i0] = csub(x + y, q);
+                v[i0 + t] = mul(s, g, x - y + q);
             }
         }
     }
 }
+
+// Multiplier functors.  Table form: one Shoup multiplication by a stored
+// {w, w'} pair.  Split form (the contiguous phase's last / first four stages):
+// w = X[s] * YZ[s][e][g] with X per 256-block and YZ a 240-entry per-modulus
+// table, two chained Shoup multiplications and no per-butterfly table traffic
+// (the on-the-fly idea of reference transform.py:126-169 with a three-way split).
+#define TW_MUL(expr) [&](int s, int gi, uint32_t y) { const uint2 w = (expr); return shoup_mul(y, w.x, w.y, q); }
 
 // ---------------------------------------------------------------------------------
 // N = 2^16, strided phase: 256-point transforms down the columns of the
@@ -139,14 +139,14 @@ ntt16_fwd_strided(const uint32_t* in, uint32_t* out, const int32_t* __restrict__
     for (int k = 0; k < 16; ++k) v[k] = src[(g + 16 * k) * 256];
     __syncthreads();
     // stages 0..3: rows j = g + 16k, group index = k >> (4 - s): uniform twiddles
-    ct16(v, q, [&](int s, int gi) { return s_tw[(1 << s) + gi]; });
+    ct16(v, q, TW_MUL(s_tw[(1 << s) + gi]));
 #pragma unroll
     for (int k = 0; k < 16; ++k) tile[(g + 17 * k) * COLS + c] = v[k];
     __syncthreads();
 #pragma unroll
     for (int k = 0; k < 16; ++k) v[k] = tile[(17 * g + k) * COLS + c];
     // stages 4..7: rows j = 16g + k
-    ct16(v, q, [&](int s, int gi) { return s_tw[(16 << s) + (g << s) + gi]; });
+    ct16(v, q, TW_MUL(s_tw[(16 << s) + (g << s) + gi]));
     uint32_t* dst = out + rm.out_row(blockIdx.y) * kN16 + blockIdx.x * COLS + c;
 #pragma unroll
     for (int k = 0; k < 16; ++k) dst[(16 * g + k) * 256] = csub(v[k], q);
@@ -169,23 +169,14 @@ ntt16_inv_strided(const uint32_t* in, uint32_t* out, const int32_t* __restrict__
     for (int k = 0; k < 16; ++k) v[k] = src[(16 * g + k) * 256];
     __syncthreads();
     // global stages 8..11 = 256-point GS stages 0..3 on rows j = 16g + k
-    gs16(v, q, [&](int s, int gi) { return s_tw[(16 + g) * (8 >> s) + gi]; });
+    gs16(v, q, TW_MUL(s_tw[(16 + g) * (8 >> s) + gi]));
 #pragma unroll
     for (int k = 0; k < 16; ++k) tile[(17 * g + k) * COLS + c] = v[k];
     __syncthreads();
 #pragma unroll
     for (int k = 0; k < 16; ++k) v[k] = tile[(g + 17 * k) * COLS + c];
     // global stages 12..14 on rows j = g + 16k, then the last stage with N^-1
-#pragma unroll
-    for (int s = 0; s < 3; ++s) {
-        const int t = 1 << s;
-#pragma unroll
-        for (int gi = 0; gi < (8 >> s); ++gi) {
-            const uint2 w = s_tw[(8 >> s) + gi];
-#pragma unroll
-            for (int j = 0; j < t; ++j) gs_bfly(v[gi * 2 * t + j], v[gi * 2 * t + j + t], w, q);
-        }
-    }
+    gs16(v, q, TW_MUL(s_tw[(8 >> s) + gi]), 3);
     uint32_t* dst = out + rm.out_row(blockIdx.y) * kN16 + blockIdx.x * COLS + c;
     const uint32_t ninv = m.n_inv, ninv_s = m.n_inv_s, wl = m.w_last, wl_s = m.w_last_s;
 #pragma unroll
@@ -203,11 +194,26 @@ ntt16_inv_strided(const uint32_t* in, uint32_t* out, const int32_t* __restrict__
 // consecutive 1 KiB blocks.  A CTA owns 16 blocks (16 KiB); thread (blk, e)
 // holds 16 elements.  Tile element e of block blk is stored at
 // blk*272 + e + (e >> 4).
+//
+// Twiddles.  The four stages next to the data (forward 12..15, inverse 0..3)
+// use N/2 + N/4 + N/8 + N/16 distinct twiddles per limb -- as many bytes as the
+// limb itself if read from the table.  Their slot index is
+// [1][B:8][e:4][g:s] (block, thread, local group), and psi^bitrev(slot)
+// factors as X_s[B] * YZ_s[g][e]:
+//     X_s[B]     = table[((256 + B) * 16) << s]             (4 per block)
+//     YZ_s[g][e] = psi^(2^(12-s) brev4(e) + 2^(16-s) brev_s(g))   (240 per modulus)
+// so those butterflies do two chained Shoup multiplications and read no
+// per-butterfly table entry.  The other four stages need 15 twiddles per block,
+// staged through shared memory at kernel start.
 // ---------------------------------------------------------------------------------
+__device__ __forceinline__ int yz_index(int s, int gi, int e) { return 16 * ((1 << s) - 1) + gi * 16 + e; }
+
 __global__ void __launch_bounds__(256)
 ntt16_fwd_contig(const uint32_t* in, uint32_t* out, const int32_t* __restrict__ row_slot,
                  const ModSlot* __restrict__ slots, RowMap rm) {
     __shared__ uint32_t tile[16 * 272];
+    __shared__ uint2 s_yz[240];
+    __shared__ uint2 s_blk[16][20];      // per block: 15 twiddles of stages 8..11, then X_0..X_3
     const int tid = threadIdx.x;
     const int e = tid & 15, blk = tid >> 4;
     const ModSlot& m = slots[row_slot[blockIdx.y]];
@@ -215,19 +221,38 @@ ntt16_fwd_contig(const uint32_t* in, uint32_t* out, const int32_t* __restrict__ 
     const uint32_t B = blockIdx.x * 16 + blk;          // 256-element block index within the limb
     const uint32_t* src = in + rm.in_row(blockIdx.y) * kN16 + B * 256;
     const uint2* __restrict__ fwd = m.fwd;
+    if (tid < 240) s_yz[tid] = m.otf_fwd[tid];
+    for (int i = tid; i < 16 * 19; i += 256) {
+        const int b = i / 19, j = i - b * 19;
+        const uint32_t Bb = 256 + blockIdx.x * 16 + b;
+        uint32_t idx;
+        if (j < 15) {
+            const int st = 31 - __clz(j + 1);          // local stage, group = j + 1 - 2^st
+            idx = (Bb << st) + (j + 1 - (1 << st));
+        } else {
+            idx = (Bb * 16) << (j - 15);
+        }
+        s_blk[b][j] = fwd[idx];
+    }
     uint32_t v[16];
 #pragma unroll
     for (int k = 0; k < 16; ++k) v[k] = src[e + 16 * k];
+    __syncthreads();
     // global stages 8..11: elements e + 16k, slot = (256 + B) * 2^s + group
-    ct16(v, q, [&](int s, int gi) { return __ldg(&fwd[((256 + B) << s) + gi]); });
+    ct16(v, q, TW_MUL(s_blk[blk][(1 << s) - 1 + gi]));
 #pragma unroll
     for (int k = 0; k < 16; ++k) tile[blk * 272 + e + 17 * k] = v[k];
     __syncthreads();
 #pragma unroll
     for (int k = 0; k < 16; ++k) v[k] = tile[blk * 272 + 17 * e + k];
-    // global stages 12..15: elements 16e + k, slot = ((256 + B) * 16 + e) * 2^s + group
-    const uint32_t base = (256 + B) * 16 + e;
-    ct16(v, q, [&](int s, int gi) { return __ldg(&fwd[(base << s) + gi]); });
+    // global stages 12..15: elements 16e + k, twiddle = X_s[B] * YZ_s[g][e]
+    uint2 X[4];
+#pragma unroll
+    for (int st = 0; st < 4; ++st) X[st] = s_blk[blk][15 + st];
+    ct16(v, q, [&](int s, int gi, uint32_t y) {
+        const uint2 yz = s_yz[yz_index(s, gi, e)];
+        return shoup_mul(shoup_lazy(y, yz.x, yz.y, q), X[s].x, X[s].y, q);
+    });
     uint4* dst = reinterpret_cast<uint4*>(out + rm.out_row(blockIdx.y) * kN16 + B * 256 + 16 * e);
 #pragma unroll
     for (int k = 0; k < 4; ++k)
@@ -239,6 +264,8 @@ __global__ void __launch_bounds__(256)
 ntt16_inv_contig(const uint32_t* in, uint32_t* out, const int32_t* __restrict__ row_slot,
                  const ModSlot* __restrict__ slots, RowMap rm) {
     __shared__ uint32_t tile[16 * 272];
+    __shared__ uint2 s_yz[240];
+    __shared__ uint2 s_blk[16][20];      // per block: 15 twiddles of stages 4..7, then X_0..X_3
     const int tid = threadIdx.x;
     const int e = tid & 15, blk = tid >> 4;
     const ModSlot& m = slots[row_slot[blockIdx.y]];
@@ -246,22 +273,43 @@ ntt16_inv_contig(const uint32_t* in, uint32_t* out, const int32_t* __restrict__ 
     const uint32_t B = blockIdx.x * 16 + blk;
     const uint4* src = reinterpret_cast<const uint4*>(in + rm.in_row(blockIdx.y) * kN16 + B * 256 + 16 * e);
     const uint2* __restrict__ inv = m.inv;
+    if (tid < 240) s_yz[tid] = m.otf_inv[tid];
+    for (int i = tid; i < 16 * 19; i += 256) {
+        const int b = i / 19, j = i - b * 19;
+        const uint32_t Bb = 256 + blockIdx.x * 16 + b;
+        uint32_t idx;
+        if (j < 15) {
+            // stage s of 4..7 has (8 >> s) groups; entries laid out 8 | 4 | 2 | 1
+            const int st = j < 8 ? 0 : (j < 12 ? 1 : (j < 14 ? 2 : 3));
+            const int off = st == 0 ? 0 : (st == 1 ? 8 : (st == 2 ? 12 : 14));
+            idx = Bb * (8 >> st) + (j - off);
+        } else {
+            idx = (Bb * 16) << (j - 15);
+        }
+        s_blk[b][j] = inv[idx];
+    }
     uint32_t v[16];
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
         const uint4 u = src[k];
         v[4 * k] = u.x; v[4 * k + 1] = u.y; v[4 * k + 2] = u.z; v[4 * k + 3] = u.w;
     }
-    // global stages 0..3 on elements 16e + k: slot = (4096 + 16B + e) * (8 >> s) + group
-    const uint32_t base = 4096 + 16 * B + e;
-    gs16(v, q, [&](int s, int gi) { return __ldg(&inv[base * (8 >> s) + gi]); });
+    __syncthreads();
+    // global stages 0..3 on elements 16e + k: slot = [1][B][e][g] with (3 - s) group bits
+    uint2 X[4];
+#pragma unroll
+    for (int st = 0; st < 4; ++st) X[st] = s_blk[blk][15 + st];
+    gs16(v, q, [&](int s, int gi, uint32_t d) {
+        const uint2 yz = s_yz[yz_index(3 - s, gi, e)];
+        return shoup_mul(shoup_lazy(d, yz.x, yz.y, q), X[3 - s].x, X[3 - s].y, q);
+    });
 #pragma unroll
     for (int k = 0; k < 16; ++k) tile[blk * 272 + 17 * e + k] = v[k];
     __syncthreads();
 #pragma unroll
     for (int k = 0; k < 16; ++k) v[k] = tile[blk * 272 + e + 17 * k];
     // global stages 4..7 on elements e + 16k: slot = (256 + B) * (8 >> s) + group
-    gs16(v, q, [&](int s, int gi) { return __ldg(&inv[(256 + B) * (8 >> s) + gi]); });
+    gs16(v, q, TW_MUL(s_blk[blk][(s == 0 ? 0 : (s == 1 ? 8 : (s == 2 ? 12 : 14))) + gi]));
     uint32_t* dst = out + rm.out_row(blockIdx.y) * kN16 + B * 256;
 #pragma unroll
     for (int k = 0; k < 16; ++k) dst[e + 16 * k] = v[k];
