@@ -123,6 +123,15 @@ int ckks_bconv(ckks_ctx* ctx, int32_t table, const uint32_t* in, uint32_t* out, 
 int ckks_ks_plan_create(ckks_ctx* ctx, uint32_t n, int l, int alpha, const int32_t* q_slot,
                         const int32_t* p_slot, int evk_ext, int evk_p_off, int32_t* plan);
 
+/* ModDown-only plan: the stage-3 machinery for `l` Q limbs and an arbitrary
+ * `alpha`-limb P basis, without raise tables or stage-1/2 workspace.  With
+ * alpha = 1 and P = {q_last} ckks_ks_stage3 on this plan is RNS rescaling
+ * (drop the last limb): (x_i - NTT(INTT(x_last) mod q_i)) * q_last^-1, the
+ * composition of reference primitives recorded as the rescale oracle
+ * (SURVEY 8c).  Not capturable. */
+int ckks_moddown_plan_create(ckks_ctx* ctx, uint32_t n, int l, int alpha, const int32_t* q_slot,
+                             const int32_t* p_slot, int32_t* plan);
+
 /* keyswitch_stage1 (keyswitch.py:297-315): a [l][n] evaluation domain ->
  * raised [beta][l+alpha][n], digit limbs carried through. */
 int ckks_ks_stage1(ckks_ctx* ctx, int32_t plan, const uint32_t* a, uint32_t* raised, void* stream);

@@ -21,7 +21,7 @@ SYMBOLS = (
     "ckks_modulus_register", "ckks_modulus_tables", "ckks_ntt", "ckks_ntt_stages",
     "ckks_elementwise", "ckks_automorphism_eval", "ckks_automorphism_coeff",
     "ckks_bconv_table_create", "ckks_bconv_table_read", "ckks_bconv",
-    "ckks_ks_plan_create", "ckks_ks_stage1", "ckks_ks_stage2", "ckks_ks_stage3", "ckks_keyswitch",
+    "ckks_ks_plan_create", "ckks_moddown_plan_create", "ckks_ks_stage1", "ckks_ks_stage2", "ckks_ks_stage3", "ckks_keyswitch",
 )
 
 
@@ -75,6 +75,7 @@ def load() -> ctypes.CDLL:
     L.ckks_bconv.argtypes = [vp, i32, vp, vp, sz, vp]
     L.ckks_ks_plan_create.argtypes = [vp, u32, ctypes.c_int, ctypes.c_int, vp, vp, ctypes.c_int,
                                       ctypes.c_int, pi32]
+    L.ckks_moddown_plan_create.argtypes = [vp, u32, ctypes.c_int, ctypes.c_int, vp, vp, pi32]
     L.ckks_ks_stage1.argtypes = [vp, i32, vp, vp, vp]
     L.ckks_ks_stage2.argtypes = [vp, i32, vp, vp, ctypes.c_int, ctypes.c_int, vp, vp, vp]
     L.ckks_ks_stage3.argtypes = [vp, i32, vp, vp, vp, vp, vp, vp, vp]

@@ -132,8 +132,11 @@ struct KsPlan {
     int32_t moddown_table = -1;
     int32_t *d_s3_in_row = nullptr, *d_s3_p_slot = nullptr, *d_s3_q_slot = nullptr;
     uint32_t *d_pinv = nullptr, *d_pinv_s = nullptr;
+    // workspace: word offsets into the context's shared arena (bound at call time)
+    size_t off_coeff = 0, off_raised = 0, off_acc = 0, off_conv = 0, off_pc = 0, ws_words = 0;
     uint32_t *ws_coeff = nullptr, *ws_raised = nullptr, *ws_acc = nullptr, *ws_conv = nullptr,
              *ws_pc = nullptr;
+    bool moddown_only = false;
 };
 
 }  // namespace ckks
@@ -149,6 +152,11 @@ struct ckks_ctx {
     std::vector<std::unique_ptr<BconvTable>> tables;
     std::vector<std::unique_ptr<KsPlan>> plans;
     std::vector<void*> owned;
+    // One workspace arena shared by every plan (calls on one stream serialise); it only
+    // grows at plan creation, never in the hot path.  Graphs captured before a later,
+    // larger plan is created must be re-captured.
+    uint32_t* ws = nullptr;
+    size_t ws_words = 0;
 };
 
 static int check_ctx(ckks_ctx* ctx) {
@@ -240,11 +248,11 @@ void ckks_ctx_destroy(ckks_ctx* ctx) {
         for (void* p : {(void*)pl->d_q_slot, (void*)pl->d_p_slot, (void*)pl->d_ext_slot,
                         (void*)pl->d_evk_row, (void*)pl->d_s1_row, (void*)pl->d_s1_slot,
                         (void*)pl->d_s3_in_row, (void*)pl->d_s3_p_slot, (void*)pl->d_s3_q_slot,
-                        (void*)pl->d_pinv, (void*)pl->d_pinv_s, (void*)pl->ws_coeff,
-                        (void*)pl->ws_raised, (void*)pl->ws_acc, (void*)pl->ws_conv, (void*)pl->ws_pc})
+                        (void*)pl->d_pinv, (void*)pl->d_pinv_s})
             cudaFree(p);
         for (int32_t* p : pl->d_raise_out_row) cudaFree(p);
     }
+    cudaFree(ctx->ws);
     cudaFree(ctx->d_slots);
     delete ctx;
 }
@@ -471,8 +479,9 @@ int ckks_bconv(ckks_ctx* ctx, int32_t table, const uint32_t* in, uint32_t* out, 
 
 // ---- key switching --------------------------------------------------------------------
 
-int ckks_ks_plan_create(ckks_ctx* ctx, uint32_t n, int l, int alpha, const int32_t* q_slot,
-                        const int32_t* p_slot, int evk_ext, int evk_p_off, int32_t* plan) {
+static int plan_create(ckks_ctx* ctx, uint32_t n, int l, int alpha, const int32_t* q_slot,
+                       const int32_t* p_slot, int evk_ext, int evk_p_off, bool moddown_only,
+                       int32_t* plan) {
     CKS(check_ctx(ctx));
     if (l < 1 || alpha < 1 || !q_slot || !p_slot || !plan || evk_p_off < l || evk_ext < evk_p_off + alpha) {
         set_last_error("bad key-switch shape l=%d alpha=%d evk_ext=%d evk_p_off=%d", l, alpha, evk_ext, evk_p_off);
@@ -485,7 +494,8 @@ int ckks_ks_plan_create(ckks_ctx* ctx, uint32_t n, int l, int alpha, const int32
     }
     auto pl = std::make_unique<KsPlan>();
     pl->n = n; pl->l = l; pl->alpha = alpha; pl->ext = l + alpha; pl->evk_ext = evk_ext;
-    pl->beta = (l + alpha - 1) / alpha;
+    pl->beta = moddown_only ? 0 : (l + alpha - 1) / alpha;
+    pl->moddown_only = moddown_only;
     const int ext = pl->ext;
     std::vector<int32_t> qv(q_slot, q_slot + l), pv(p_slot, p_slot + alpha), extv, evk_row;
     extv = qv;
@@ -541,13 +551,25 @@ int ckks_ks_plan_create(ckks_ctx* ctx, uint32_t n, int l, int alpha, const int32
     CKS(upload(s3_in_row, &pl->d_s3_in_row));
     CKS(upload(s3_p_slot, &pl->d_s3_p_slot));
     CKS(upload(s3_q_slot, &pl->d_s3_q_slot));
-    // workspace (owned by the plan, sized once; nothing allocates in the hot path)
-    const size_t limb = sizeof(uint32_t) * (size_t)n;
-    CK(cudaMalloc((void**)&pl->ws_coeff, limb * l));
-    CK(cudaMalloc((void**)&pl->ws_raised, limb * pl->beta * ext));
-    CK(cudaMalloc((void**)&pl->ws_acc, limb * 2 * ext));
-    CK(cudaMalloc((void**)&pl->ws_conv, limb * 2 * l));
-    CK(cudaMalloc((void**)&pl->ws_pc, limb * 2 * alpha));
+    // workspace: carve the shared arena (grown here if needed, never in the hot path)
+    {
+        const size_t nn = n;
+        size_t at = 0;
+        pl->off_coeff = at;  at += moddown_only ? 0 : nn * l;
+        pl->off_raised = at; at += moddown_only ? 0 : nn * pl->beta * ext;
+        pl->off_acc = at;    at += moddown_only ? 0 : nn * 2 * ext;
+        pl->off_conv = at;   at += nn * 2 * l;
+        pl->off_pc = at;     at += nn * 2 * alpha;
+        pl->ws_words = at;
+        if (at > ctx->ws_words) {
+            CK(cudaDeviceSynchronize());
+            if (ctx->ws) CK(cudaFree(ctx->ws));
+            ctx->ws = nullptr;
+            ctx->ws_words = 0;
+            CK(cudaMalloc((void**)&ctx->ws, sizeof(uint32_t) * at));
+            ctx->ws_words = at;
+        }
+    }
     *plan = (int32_t)ctx->plans.size();
     ctx->plans.push_back(std::move(pl));
     return CKKS_OK;
@@ -556,7 +578,18 @@ int ckks_ks_plan_create(ckks_ctx* ctx, uint32_t n, int l, int alpha, const int32
 static int get_plan(ckks_ctx* ctx, int32_t id, KsPlan** out) {
     CKS(check_ctx(ctx));
     if (id < 0 || id >= (int32_t)ctx->plans.size()) { set_last_error("key-switch plan %d out of range", id); return CKKS_ERR_ARG; }
-    *out = ctx->plans[id].get();
+    KsPlan* pl = ctx->plans[id].get();
+    pl->ws_coeff = ctx->ws + pl->off_coeff;
+    pl->ws_raised = ctx->ws + pl->off_raised;
+    pl->ws_acc = ctx->ws + pl->off_acc;
+    pl->ws_conv = ctx->ws + pl->off_conv;
+    pl->ws_pc = ctx->ws + pl->off_pc;
+    *out = pl;
+    return CKKS_OK;
+}
+
+static int need_full_plan(KsPlan* pl) {
+    if (pl->moddown_only) { set_last_error("plan was created for ModDown / rescale only"); return CKKS_ERR_STATE; }
     return CKKS_OK;
 }
 
@@ -643,9 +676,20 @@ static InnerProductArgs ip_args(KsPlan* pl, const uint32_t* carry, const uint32_
     return a;
 }
 
+int ckks_ks_plan_create(ckks_ctx* ctx, uint32_t n, int l, int alpha, const int32_t* q_slot,
+                        const int32_t* p_slot, int evk_ext, int evk_p_off, int32_t* plan) {
+    return plan_create(ctx, n, l, alpha, q_slot, p_slot, evk_ext, evk_p_off, false, plan);
+}
+
+int ckks_moddown_plan_create(ckks_ctx* ctx, uint32_t n, int l, int alpha, const int32_t* q_slot,
+                             const int32_t* p_slot, int32_t* plan) {
+    return plan_create(ctx, n, l, alpha, q_slot, p_slot, l + alpha, l, true, plan);
+}
+
 int ckks_ks_stage1(ckks_ctx* ctx, int32_t plan, const uint32_t* a, uint32_t* raised, void* stream) {
     KsPlan* pl;
     CKS(get_plan(ctx, plan, &pl));
+    CKS(need_full_plan(pl));
     return stage1_core(ctx, pl, a, raised, true, (cudaStream_t)stream);
 }
 
@@ -653,6 +697,7 @@ int ckks_ks_stage2(ckks_ctx* ctx, int32_t plan, const uint32_t* raised, const ui
                    int row_lo, int row_hi, uint32_t* acc_a, uint32_t* acc_b, void* stream) {
     KsPlan* pl;
     CKS(get_plan(ctx, plan, &pl));
+    CKS(need_full_plan(pl));
     if (row_lo < 0 || row_hi > pl->ext || row_lo > row_hi) { set_last_error("bad row range [%d, %d)", row_lo, row_hi); return CKKS_ERR_ARG; }
     return inner_product_launch(ip_args(pl, nullptr, raised, evk, row_lo, row_hi, acc_a, acc_b),
                                 ctx->d_slots, (cudaStream_t)stream);
@@ -670,6 +715,7 @@ int ckks_keyswitch(ckks_ctx* ctx, int32_t plan, const uint32_t* ct_a, const uint
                    const uint32_t* evk, uint32_t* out_a, uint32_t* out_b, void* stream) {
     KsPlan* pl;
     CKS(get_plan(ctx, plan, &pl));
+    CKS(need_full_plan(pl));
     cudaStream_t st = (cudaStream_t)stream;
     const size_t n = pl->n;
     CKS(stage1_core(ctx, pl, ct_a, pl->ws_raised, false, st));

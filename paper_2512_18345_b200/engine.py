@@ -155,6 +155,20 @@ class Engine:
             p = self._plans[key] = out.value
         return p
 
+    def moddown_plan(self, n: int, q_basis, p_basis) -> int:
+        """Stage-3-only plan: ModDown from Q||P to Q for an arbitrary P (rescale when
+        P is the single limb being dropped)."""
+        key = ("moddown", n, tuple(m.q for m in q_basis), tuple(m.q for m in p_basis))
+        p = self._plans.get(key)
+        if p is None:
+            qs = (ctypes.c_int32 * len(q_basis))(*[self.slot(m, n) for m in q_basis])
+            ps = (ctypes.c_int32 * len(p_basis))(*[self.slot(m, n) for m in p_basis])
+            out = ctypes.c_int32()
+            _lib.check(self.lib.ckks_moddown_plan_create(self.ctx, n, len(q_basis), len(p_basis),
+                                                         qs, ps, ctypes.byref(out)))
+            p = self._plans[key] = out.value
+        return p
+
     def ks_stage1(self, plan: int, a, beta: int, ext: int):
         raised = self.empty(beta, ext, a.shape[1])
         _lib.check(self.lib.ckks_ks_stage1(self.ctx, plan, a.data_ptr(), raised.data_ptr(),
