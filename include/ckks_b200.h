@@ -98,6 +98,20 @@ int ckks_automorphism_eval(ckks_ctx* ctx, const uint32_t* in, uint32_t* out, int
 int ckks_automorphism_coeff(ckks_ctx* ctx, const uint32_t* in, uint32_t* out,
                             const int32_t* row_slot, int rows, uint32_t n, uint32_t k, void* stream);
 
+/* ---- CKKS additions without a reference counterpart -------------- */
+
+/* Exact centred lift (bootstrapping ModRaise): in [2][n] coefficient-domain
+ * limbs over slots slot0, slot1 -> out [rows][n], out[i] = centred value mod
+ * modulus row_slot[i]. */
+int ckks_lift2_centered(ckks_ctx* ctx, const uint32_t* in, int32_t slot0, int32_t slot1,
+                        uint32_t* out, const int32_t* row_slot, int rows, size_t n, void* stream);
+
+/* acc (+)= x (.) p on both halves of a ciphertext: x, acc [2][rows][cols], p
+ * [rows][cols]; first != 0 overwrites acc (the PMult-accumulate inner loop of
+ * the BSGS linear transforms; each product is poly_elementwise "mul"). */
+int ckks_pmult_accumulate(ckks_ctx* ctx, const uint32_t* x, const uint32_t* p, uint32_t* acc,
+                          const int32_t* row_slot, int rows, size_t cols, int first, void* stream);
+
 /* ---- base conversion: baseconv.py:57-151 ------------------------------------ */
 
 /* build_bconv_table (baseconv.py:57-85) for source slots -> target slots.

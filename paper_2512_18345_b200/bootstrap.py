@@ -1,0 +1,394 @@
+"""CKKS bootstrapping for fully packed ciphertexts (N/2 complex slots):
+ModRaise -> CoeffToSlot -> EvalMod -> SlotToCoeff, every arithmetic step on the
+GPU through the kernels of csrc/ (key switching, automorphism, PMult
+accumulate, rescale), host code only orchestrates.
+
+The reference ships no bootstrapping; this module has no
+reference oracle (parity unpinned) and is checked by decoded-slot
+precision against the input message.
+
+Circuit
+  * ModRaise: exact centred lift of the two bottom limbs to the full basis.
+    The lifted polynomial is t = Delta*m + e + Q0*I with small integer I
+    (sparse secret, h = params.h_sparse).
+  * CoeffToSlot / SlotToCoeff: the special-FFT factorisation of the canonical
+    embedding (the decode map of ckks.Embedding), log2(n) butterfly stages of
+    three diagonals each, merged into a few groups and evaluated with
+    baby-step/giant-step rotations.  The bit reversal is skipped on both sides
+    (EvalMod is slot-wise).  One limb per group (plaintext scale = that limb).
+  * EvalMod: E = exp(2*pi*i*t / (Q0 * 2^r)) by a degree-d Taylor polynomial,
+    r squarings, then (Q0 / (2*pi*Delta)) * sin = Im(E) scaled; real and
+    imaginary coefficient halves are processed as two ciphertexts.  Two limbs
+    per multiplicative level (scale ~ 2^62 on 31-bit limbs).
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import ckks
+from . import keyswitch as ks
+from .params import ParameterSet
+from .rns import EVALUATION, Polynomial, RnsError
+from .transform import ntt_polynomial
+
+
+# ---------------------------------------------------------------------------
+# diagonal algebra on n-slot vectors (host, float)
+# ---------------------------------------------------------------------------
+def _rot(v: np.ndarray, d: int) -> np.ndarray:
+    """Left rotation: out[p] = v[p + d]."""
+    return np.roll(v, -d)
+
+
+def dft_stage(n: int, ell: int, inverse: bool) -> dict[int, np.ndarray]:
+    """Butterfly stage `ell` (block length 2^ell) of the special FFT on n slots,
+    or its inverse, as {rotation offset: diagonal}: out = sum_d diag_d * rot(in, d)."""
+    length = 1 << ell
+    half = length >> 1
+    p = np.arange(n)
+    j = p % length
+    first = j < half
+    jj = np.where(first, j, j - half)
+    pw = np.ones(half, dtype=np.int64)
+    for t in range(1, half):
+        pw[t] = pw[t - 1] * 5 % (4 * length)
+    xi = np.exp(2j * np.pi * pw[jj] / (4 * length))
+    z = np.zeros(n, dtype=np.complex128)
+    if not inverse:
+        d0 = np.where(first, 1.0 + 0j, -xi)
+        dp = np.where(first, xi, z)             # takes in[p + half]
+        dm = np.where(first, z, 1.0 + 0j)       # takes in[p - half]
+    else:
+        d0 = np.where(first, 0.5 + 0j, -0.5 * np.conj(xi))
+        dp = np.where(first, 0.5 + 0j, z)
+        dm = np.where(first, z, 0.5 * np.conj(xi))
+    out = {0: d0}
+    for off, vec in ((half % n, dp), ((-half) % n, dm)):
+        out[off] = out[off] + vec if off in out else vec
+    return out
+
+
+def compose(a: dict, b: dict, n: int) -> dict:
+    """Diagonals of A*B (B applied first)."""
+    out: dict[int, np.ndarray] = {}
+    for d1, va in a.items():
+        for d2, vb in b.items():
+            d = (d1 + d2) % n
+            term = va * _rot(vb, d1)
+            out[d] = out[d] + term if d in out else term
+    return {d: v for d, v in out.items() if np.abs(v).max() > 0}
+
+
+def apply_diagonals(diags: dict, x: np.ndarray) -> np.ndarray:
+    return sum(v * _rot(x, d) for d, v in diags.items())
+
+
+def grouped_dft(n: int, group_sizes: list[int], inverse: bool) -> list[dict]:
+    """The n-slot special FFT without its bit reversal (or the inverse), as
+    merged groups of stages in application order."""
+    lg = n.bit_length() - 1
+    assert sum(group_sizes) == lg
+    stages = list(range(1, lg + 1))
+    groups = []
+    at = 0
+    if not inverse:                      # S_lg ... S_1: stage 1 first
+        for size in group_sizes:
+            acc = None
+            for ell in stages[at:at + size]:
+                st = dft_stage(n, ell, False)
+                acc = st if acc is None else compose(st, acc, n)
+            groups.append(acc)
+            at += size
+    else:                                # S_1^-1 ... S_lg^-1: stage lg first
+        order = stages[::-1]
+        for size in group_sizes:
+            acc = None
+            for ell in order[at:at + size]:
+                st = dft_stage(n, ell, True)
+                acc = st if acc is None else compose(st, acc, n)
+            groups.append(acc)
+            at += size
+    return groups
+
+
+def default_groups(lg: int, count: int = 3) -> list[int]:
+    base, extra = divmod(lg, count)
+    return [base + (1 if i < extra else 0) for i in range(count)]
+
+
+# ---------------------------------------------------------------------------
+# homomorphic linear transform (BSGS)
+# ---------------------------------------------------------------------------
+def ct_tensor(ct):
+    """[2, l, n] device tensor of a ciphertext (a view when a and b are adjacent)."""
+    import torch
+
+    a, b = ct.a.data, ct.b.data
+    if a.data_ptr() + a.numel() * 4 == b.data_ptr() and getattr(a, "_base", None) is not None \
+            and a._base is getattr(b, "_base", None):
+        base = a._base
+        if base.dim() == 3 and base.shape[0] == 2 and base.data_ptr() == a.data_ptr():
+            return base
+    return torch.stack([a, b])
+
+
+def ct_from_tensor(t, basis, scale):
+    return ckks.Ciphertext(a=Polynomial(basis, t[0], EVALUATION), b=Polynomial(basis, t[1], EVALUATION),
+                           scale=scale)
+
+
+class LinearTransform:
+    """y = sum_d diag_d * rot(x, d) with offsets d = g*n1*step + b*step (mod n):
+    inner_g = sum_b rot(diag_d, -g*n1*step) * rot(x, b*step);  y = sum_g rot(inner_g, g*n1*step).
+    Diagonals are encoded once at `level` limbs with scale = the product of the last
+    `limbs` of them, so PMult + rescale by those limbs leaves the ciphertext scale
+    unchanged (two limbs where 2^-31 relative plaintext precision is not enough)."""
+
+    def __init__(self, diags: dict, params: ParameterSet, level: int, n1: int | None = None,
+                 factor: complex = 1.0, limbs: int = 1):
+        n = params.n // 2
+        self.params, self.level, self.n, self.limbs = params, level, n, limbs
+        offs = sorted(diags)
+        signed = [d if d <= n // 2 else d - n for d in offs]
+        nz = [abs(d) for d in signed if d]
+        step = math.gcd(*nz) if nz else 1
+        units = [d // step for d in signed]
+        span = max(units) - min(units) + 1
+        if n1 is None:
+            n1 = 1 << max(0, round(math.log2(math.sqrt(span))))
+        self.step, self.n1 = step, n1
+        self.pt_scale = float(math.prod(m.q for m in params.q_basis[level - limbs:level]))
+        table: dict[int, dict[int, ckks.Plaintext]] = {}
+        for d, u in zip(offs, units):
+            g, b = divmod(u, n1)                      # floor division: b in [0, n1)
+            vec = _rot(diags[d] * factor, -g * n1 * step)
+            table.setdefault(g, {})[b] = ckks.encode(vec, params, level=level, scale=self.pt_scale)
+        self.table = table
+        self.baby = sorted({b for row in table.values() for b in row})
+        self.giants = sorted(table)
+
+    def rotations(self) -> set[int]:
+        out = {(b * self.step) % self.n for b in self.baby if b}
+        out |= {(g * self.n1 * self.step) % self.n for g in self.giants if g}
+        return out
+
+    def apply(self, ct, keys: ckks.EvaluationKeys):
+        from .engine import get_engine
+
+        eng = get_engine()
+        if ckks.level_of(ct) != self.level:
+            raise RnsError(f"linear transform encoded for level {self.level}, ciphertext at {ckks.level_of(ct)}")
+        basis = ct.a.basis
+        slots = eng.row_slots(basis)
+        rotated = {b: ct_tensor(ckks.hrot(ct, b * self.step, keys)) for b in self.baby}
+        total = None
+        for g in self.giants:
+            inner = eng.empty(2, self.level, self.params.n)
+            first = True
+            for b, pt in self.table[g].items():
+                eng.pmult_accumulate(rotated[b], pt.poly.data, inner, slots, first)
+                first = False
+            part = ct_from_tensor(inner, basis, ct.scale * self.pt_scale)
+            if g:
+                part = ckks.hrot(part, g * self.n1 * self.step, keys)
+            total = part if total is None else ckks.add(total, part)
+        out = ckks.rescale(total, self.limbs)
+        return ckks.Ciphertext(a=out.a, b=out.b, scale=ct.scale)
+
+
+# ---------------------------------------------------------------------------
+# bootstrapping
+# ---------------------------------------------------------------------------
+@dataclass
+class BootstrapConfig:
+    squarings: int = 6            # r: exp(i*theta / 2^r) is squared r times
+    degree: int = 15              # Taylor degree of exp on |x| <= 2*pi*K / 2^r
+    k_bound: int = 16             # |I| <= K
+    log_delta_in: int = 52        # input scale 2^log_delta_in at two limbs (Q0 ~ 2^62)
+    groups: int = 3               # stage groups per linear transform
+    n1: int | None = None         # baby-step count (default ~ sqrt of the diagonal span)
+
+
+class Bootstrapper:
+    """Keys, encoded DFT diagonals and constants for one parameter set; bootstrap(ct)
+    refreshes a level-2 ciphertext of scale 2^log_delta_in to `out_level` limbs."""
+
+    def __init__(self, params: ParameterSet, sk: ks.SecretKey, config: BootstrapConfig | None = None,
+                 seed: int = 7000):
+        self.params, self.cfg = params, config or BootstrapConfig()
+        cfg = self.cfg
+        n = params.n // 2
+        lg = n.bit_length() - 1
+        L = params.l
+        self.q0 = params.q_basis[0].q * params.q_basis[1].q
+        self.delta_in = float(1 << cfg.log_delta_in)
+        sizes = default_groups(lg, cfg.groups)
+        # ---- level plan -----------------------------------------------------------
+        self.lvl_cts = L                                   # CoeffToSlot: two limbs per group (its error
+        self.lvl_evalmod = L - 2 * cfg.groups              # is amplified by Q0*2^r/(2*pi*Delta) ~ 2^13)
+        depth = math.ceil(math.log2(cfg.degree + 1))       # Taylor polynomial depth
+        self.lvl_after_evalmod = self.lvl_evalmod - 2 * (depth + cfg.squarings) - 1
+        self.lvl_stc = self.lvl_after_evalmod
+        self.out_level = self.lvl_stc - cfg.groups
+        if self.out_level < 3:
+            raise RnsError(f"parameter set too shallow for bootstrapping: would end at level {self.out_level}")
+        self.eval_scale = float(params.q_basis[self.lvl_evalmod - 1].q) * float(params.q_basis[self.lvl_evalmod - 2].q)
+        self.out_scale = float(params.q_basis[self.out_level - 1].q) * float(params.q_basis[self.out_level - 2].q)
+        # After ModRaise the plaintext polynomial is t; tagging it with scale
+        # Q0 * 2^r / (2*pi) makes CoeffToSlot deliver y = 2*pi*t / (Q0 * 2^r) in the slots.
+        self.raise_scale = self.q0 * float(1 << cfg.squarings) / (2.0 * math.pi)
+        # ---- linear transforms ----------------------------------------------------
+        cts = grouped_dft(n, sizes, inverse=True)
+        stc = grouped_dft(n, sizes, inverse=False)
+        # last CoeffToSlot group also renormalises the scale tag to eval_scale / 2
+        # (the factor 2 is absorbed by W +/- conj(W) below)
+        renorm = (self.eval_scale / 2.0) / self.raise_scale
+        self.cts = [LinearTransform(g, params, self.lvl_cts - 2 * i, cfg.n1,
+                                    factor=renorm if i == len(cts) - 1 else 1.0, limbs=2)
+                    for i, g in enumerate(cts)]
+        self.stc = [LinearTransform(g, params, self.lvl_stc - i, cfg.n1) for i, g in enumerate(stc)]
+        # ---- keys -----------------------------------------------------------------
+        self.keys = ckks.EvaluationKeys(params, relin=ckks.relin_keygen(sk, params, seed=seed))
+        self.keys.add_conjugation(sk, seed=seed + 1)
+        rots = set()
+        for lt in self.cts + self.stc:
+            rots |= lt.rotations()
+        for i, r in enumerate(sorted(rots)):
+            self.keys.add_rotation(sk, r, seed=seed + 2 + i)
+        # Taylor coefficients of exp(i*y) (real-part branch, input y) and exp(x) (input x = i*y)
+        d = cfg.degree
+        self.coef_lo = [(1j ** k) / math.factorial(k) for k in range(d + 1)]
+        self.coef_hi = [1.0 / math.factorial(k) for k in range(d + 1)]
+        self._consts: dict = {}
+
+    def _const(self, value: complex, level: int, scale: float) -> ckks.Plaintext:
+        """Encoded constant, cached: levels and scales are the same on every call."""
+        key = (complex(value), level, float(scale))
+        hit = self._consts.get(key)
+        if hit is None:
+            hit = self._consts[key] = ckks.encode(value, self.params, level=level, scale=scale)
+        return hit
+
+    # -- steps ---------------------------------------------------------------------
+    def mod_raise(self, ct):
+        """Level-2 ciphertext -> full level, plaintext t = Delta*m + e + Q0*I."""
+        from .engine import get_engine
+
+        eng = get_engine()
+        p = self.params
+        if ckks.level_of(ct) != 2:
+            raise RnsError("bootstrap input must live on the two bottom limbs")
+        low = p.q_basis[:2]
+        full = p.q_basis
+        s0, s1 = eng.slot(low[0], p.n), eng.slot(low[1], p.n)
+        slots_full = eng.row_slots(full, p.n)
+        halves = []
+        for poly in (ct.a, ct.b):
+            coeff = ntt_polynomial(poly, "inverse")
+            lifted = eng.lift2_centered(coeff.data, s0, s1, slots_full, len(full))
+            halves.append(eng.ntt(lifted, slots_full, False))
+        return ckks.Ciphertext(a=Polynomial(full, halves[0], EVALUATION),
+                               b=Polynomial(full, halves[1], EVALUATION), scale=self.raise_scale)
+
+    def coeff_to_slot(self, ct):
+        for lt in self.cts:
+            ct = lt.apply(ct, self.keys)
+        # W holds (y_lo + i*y_hi) / 2 in bit-reversed slot order, scale tag eval_scale / 2
+        conj = ckks.conjugate(ct, self.keys)
+        lo = ckks.add(ct, conj)        # y_lo   at tag eval_scale
+        hi = ckks.sub(ct, conj)        # i*y_hi at tag eval_scale
+        lo = ckks.Ciphertext(lo.a, lo.b, self.eval_scale)
+        hi = ckks.Ciphertext(hi.a, hi.b, self.eval_scale)
+        return lo, hi
+
+    def _pair(self, x, c0: complex, c1: complex, target_scale: float, level: int):
+        """c0 + c1*x at `level` limbs and scale `target_scale` (x two limbs above)."""
+        p = self.params
+        lvl = ckks.level_of(x)
+        dropped = math.prod(m.q for m in x.a.basis[lvl - 2:])
+        pt = self._const(c1, lvl, target_scale * dropped / x.scale)
+        t = ckks.rescale(ckks.mul_plain(x, pt), 2)
+        t = ckks.mod_drop(ckks.Ciphertext(t.a, t.b, target_scale), level)
+        return ckks.add_plain(t, self._const(c0, level, target_scale))
+
+    def _mul(self, x, y):
+        lvl = min(ckks.level_of(x), ckks.level_of(y))
+        return ckks.rescale(ckks.hmult(ckks.mod_drop(x, lvl), ckks.mod_drop(y, lvl), self.keys.relin), 2)
+
+    def _exp_taylor(self, x, coef):
+        """sum_k coef[k] x^k by a balanced power tree (depth ceil(log2(degree+1)))."""
+        d = len(coef) - 1
+        depth = math.ceil(math.log2(d + 1))
+        powers = {1: x}
+        for j in range(1, depth):
+            powers[1 << j] = self._mul(powers[1 << (j - 1)], powers[1 << (j - 1)])
+
+        def build(lo: int, span: int):
+            """Polynomial sum_{k<span} coef[lo+k] x^k; returns None when all coefficients vanish."""
+            if lo > d:
+                return None
+            if span == 2:
+                c0 = coef[lo]
+                c1 = coef[lo + 1] if lo + 1 <= d else 0.0
+                return ("pair", c0, c1)
+            half = span // 2
+            return ("node", build(lo, half), build(lo + half, half), half)
+
+        def realise(node, want_scale, want_level):
+            """Materialise a subtree at exactly (want_scale, want_level)."""
+            if node[0] == "pair":
+                return self._pair(x, node[1], node[2], want_scale, want_level)
+            _, left, right, half = node
+            xp = powers[half]
+            if right is None:
+                return realise(left, want_scale, want_level)
+            lvl_in = want_level + 2
+            xp_d = ckks.mod_drop(xp, lvl_in) if ckks.level_of(xp) > lvl_in else xp
+            dropped = math.prod(m.q for m in self.params.q_basis[want_level:lvl_in])
+            r = realise(right, want_scale * dropped / xp_d.scale, lvl_in)
+            prod = self._mul(r, xp_d)
+            prod = ckks.Ciphertext(prod.a, prod.b, want_scale)
+            return ckks.add(prod, realise(left, want_scale, want_level))
+
+        tree = build(0, 1 << depth)
+        out_level = ckks.level_of(x) - 2 * depth
+        return realise(tree, self.eval_scale_at(out_level), out_level)
+
+    def eval_scale_at(self, level: int) -> float:
+        q = self.params.q_basis
+        return float(q[level - 1].q) * float(q[level - 2].q)
+
+    def eval_mod(self, x, coef, kappa: complex):
+        """x: slots y (or i*y) with |y| <= 2*pi*K/2^r.  Returns kappa * (E - conj E), E = exp(i*theta)."""
+        e = self._exp_taylor(x, coef)
+        for _ in range(self.cfg.squarings):
+            e = self._mul(e, e)
+        diff = ckks.sub(e, ckks.conjugate(e, self.keys))
+        lvl = ckks.level_of(diff)
+        pt_scale = float(self.params.q_basis[lvl - 1].q)
+        # message scale folded so the result carries tag out_scale
+        pt = self._const(kappa, lvl, self.out_scale * pt_scale / diff.scale)
+        out = ckks.rescale(ckks.mul_plain(diff, pt), 1)
+        return ckks.Ciphertext(out.a, out.b, self.out_scale)
+
+    def slot_to_coeff(self, ct):
+        for lt in self.stc:
+            ct = lt.apply(ct, self.keys)
+        return ct
+
+    def bootstrap(self, ct):
+        if not ckks._close(ct.scale, self.delta_in):
+            raise RnsError(f"bootstrap expects scale 2^{self.cfg.log_delta_in}, got {ct.scale}")
+        raised = self.mod_raise(ct)
+        lo, hi = self.coeff_to_slot(raised)
+        # (Q0 / (2*pi*Delta)) * sin(theta) = kappa * (E - conj E),  kappa = Q0 / (4*pi*i*Delta)
+        kappa = self.q0 / (4.0 * math.pi * self.delta_in) / 1j
+        m_lo = self.eval_mod(lo, self.coef_lo, kappa)
+        m_hi = self.eval_mod(hi, self.coef_hi, kappa * 1j)
+        w = ckks.add(m_lo, m_hi)                       # m_lo + i*m_hi (bit-reversed slots)
+        w = ckks.mod_drop(w, self.lvl_stc)
+        out = self.slot_to_coeff(w)
+        return ckks.Ciphertext(out.a, out.b, self.out_scale)

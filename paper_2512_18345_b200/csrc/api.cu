@@ -405,6 +405,23 @@ int ckks_automorphism_coeff(ckks_ctx* ctx, const uint32_t* in, uint32_t* out,
                                      (cudaStream_t)stream);
 }
 
+int ckks_lift2_centered(ckks_ctx* ctx, const uint32_t* in, int32_t slot0, int32_t slot1,
+                        uint32_t* out, const int32_t* row_slot, int rows, size_t n, void* stream) {
+    CKS(check_ctx(ctx));
+    CKS(check_slot(ctx, slot0));
+    CKS(check_slot(ctx, slot1));
+    const uint32_t q0 = ctx->h_slots[slot0].q, q1 = ctx->h_slots[slot1].q;
+    if (q0 == q1 || (q0 >> 31) || (q1 >> 31)) { set_last_error("lift needs two distinct moduli below 2^31"); return CKKS_ERR_ARG; }
+    return lift2_centered_launch(in, out, row_slot, ctx->d_slots, slot0, slot1, h_inv(q0 % q1, q1),
+                                 rows, n, (cudaStream_t)stream);
+}
+
+int ckks_pmult_accumulate(ckks_ctx* ctx, const uint32_t* x, const uint32_t* p, uint32_t* acc,
+                          const int32_t* row_slot, int rows, size_t cols, int first, void* stream) {
+    CKS(check_ctx(ctx));
+    return pmult_acc_launch(x, p, acc, row_slot, ctx->d_slots, rows, cols, first, (cudaStream_t)stream);
+}
+
 // ---- base conversion ------------------------------------------------------------------
 
 int ckks_bconv_table_create(ckks_ctx* ctx, const int32_t* in_slot, int l_in, const int32_t* out_slot,

@@ -137,4 +137,84 @@ int automorphism_coeff_launch(const uint32_t* in, uint32_t* out, const int32_t* 
     return CKKS_OK;
 }
 
+// Exact centred lift from two limbs to many (bootstrapping ModRaise): for every
+// column the value v in (-Q0/2, Q0/2], Q0 = q0*q1, is rebuilt from its two
+// residues by Garner's formula and reduced modulo every target modulus.  (The
+// non-centred fast conversion of baseconv.py would add Q0 * (0/1 polynomial) to
+// the mask, which inflates the integer part EvalMod has to remove.)
+__global__ void __launch_bounds__(256)
+lift2_centered_kernel(const uint32_t* __restrict__ in, uint32_t* __restrict__ out,
+                      const int32_t* __restrict__ row_slot, const ModSlot* __restrict__ slots,
+                      int32_t slot0, int32_t slot1, uint32_t q0_inv_mod_q1, int rows, size_t n) {
+    const size_t c = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= n) return;
+    const ModSlot m1 = slots[slot1];
+    const uint64_t q0 = slots[slot0].q, q1 = m1.q;
+    const uint32_t r0 = in[c], r1 = in[n + c];
+    const uint32_t d = (uint32_t)(((uint64_t)r1 + q1 - r0 % q1) % q1);
+    const uint64_t t = (uint64_t)d * q0_inv_mod_q1 % q1;
+    const uint64_t v = r0 + q0 * t;                       // in [0, Q0)
+    const uint64_t big = q0 * q1;
+    const bool neg = v > big / 2;
+    const uint64_t mag = neg ? big - v : v;
+    for (int i = blockIdx.y; i < rows; i += gridDim.y) {
+        const ModSlot& m = slots[row_slot[i]];
+        uint32_t r = reduce64(mag, m);
+        if (neg) r = r ? m.q - r : 0;
+        out[(size_t)i * n + c] = r;
+    }
+}
+
+int lift2_centered_launch(const uint32_t* in, uint32_t* out, const int32_t* row_slot,
+                          const ModSlot* slots, int32_t slot0, int32_t slot1, uint32_t inv,
+                          int rows, size_t n, cudaStream_t st) {
+    if (rows <= 0 || n == 0) return CKKS_OK;
+    ProfScope ps("lift2_centered", st);
+    dim3 grid((unsigned)((n + 255) / 256), rows < 16 ? rows : 16);
+    lift2_centered_kernel<<<grid, 256, 0, st>>>(in, out, row_slot, slots, slot0, slot1, inv, rows, n);
+    CK(cudaGetLastError());
+    return CKKS_OK;
+}
+
+// acc += x (.) p on both halves of a ciphertext in one pass (the inner loop of
+// the BSGS linear transforms): acc, x are [2][rows][n], p is [rows][n].
+__global__ void __launch_bounds__(256)
+pmult_acc_kernel(const uint4* __restrict__ x, const uint4* __restrict__ p, uint4* acc,
+                 const int32_t* __restrict__ row_slot, const ModSlot* __restrict__ slots,
+                 int rows, size_t cols4, int first) {
+    const size_t row = blockIdx.y;
+    const ModSlot m = slots[row_slot[row]];
+    const size_t half = (size_t)rows * cols4;
+    const size_t stride = (size_t)gridDim.x * blockDim.x;
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < cols4; i += stride) {
+        const uint4 pv = p[row * cols4 + i];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const size_t at = h * half + row * cols4 + i;
+            const uint4 xv = x[at];
+            uint4 r;
+            r.x = mul_mod(xv.x, pv.x, m); r.y = mul_mod(xv.y, pv.y, m);
+            r.z = mul_mod(xv.z, pv.z, m); r.w = mul_mod(xv.w, pv.w, m);
+            if (!first) {
+                const uint4 a = acc[at];
+                r.x = add_mod(r.x, a.x, m.q); r.y = add_mod(r.y, a.y, m.q);
+                r.z = add_mod(r.z, a.z, m.q); r.w = add_mod(r.w, a.w, m.q);
+            }
+            acc[at] = r;
+        }
+    }
+}
+
+int pmult_acc_launch(const uint32_t* x, const uint32_t* p, uint32_t* acc, const int32_t* row_slot,
+                     const ModSlot* slots, int rows, size_t cols, int first, cudaStream_t st) {
+    if (rows <= 0 || cols == 0) return CKKS_OK;
+    if (cols % 4 || rows > 65535) { set_last_error("pmult_acc needs cols % 4 == 0 and <= 65535 rows"); return CKKS_ERR_UNSUPPORTED; }
+    ProfScope ps("pmult_acc", st);
+    unsigned gx = (unsigned)((cols / 4 + 255) / 256);
+    pmult_acc_kernel<<<dim3(gx, rows), 256, 0, st>>>((const uint4*)x, (const uint4*)p, (uint4*)acc,
+                                                     row_slot, slots, rows, cols / 4, first);
+    CK(cudaGetLastError());
+    return CKKS_OK;
+}
+
 }  // namespace ckks

@@ -62,6 +62,12 @@ int automorphism_eval_launch(const uint32_t* in, uint32_t* out, int rows, uint32
 int automorphism_coeff_launch(const uint32_t* in, uint32_t* out, const int32_t* row_slot,
                               const ModSlot* slots, int rows, uint32_t n, uint32_t k, cudaStream_t st);
 
+int lift2_centered_launch(const uint32_t* in, uint32_t* out, const int32_t* row_slot,
+                          const ModSlot* slots, int32_t slot0, int32_t slot1, uint32_t inv,
+                          int rows, size_t n, cudaStream_t st);
+int pmult_acc_launch(const uint32_t* x, const uint32_t* p, uint32_t* acc, const int32_t* row_slot,
+                     const ModSlot* slots, int rows, size_t cols, int first, cudaStream_t st);
+
 // bconv.cu
 // Device image of one conversion table (reference baseconv.py:37-54).
 struct BconvDev {

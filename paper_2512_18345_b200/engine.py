@@ -118,6 +118,20 @@ class Engine:
                                             int(inverse), lo, hi, self.stream()))
         return out
 
+    def lift2_centered(self, coeff2, slot0: int, slot1: int, row_slot, rows: int):
+        out = self.empty(rows, coeff2.shape[1])
+        _lib.check(self.lib.ckks_lift2_centered(self.ctx, coeff2.data_ptr(), slot0, slot1,
+                                                out.data_ptr(), row_slot.data_ptr(), rows,
+                                                coeff2.shape[1], self.stream()))
+        return out
+
+    def pmult_accumulate(self, x, p, acc, row_slot, first: bool):
+        """acc (+)= x * p; x, acc are [2, rows, n] ciphertext tensors, p is [rows, n]."""
+        _lib.check(self.lib.ckks_pmult_accumulate(self.ctx, x.data_ptr(), p.data_ptr(),
+                                                  acc.data_ptr(), row_slot.data_ptr(), x.shape[1],
+                                                  x.shape[2], int(first), self.stream()))
+        return acc
+
     def bconv_table(self, q_basis, p_basis) -> int:
         key = (tuple(m.q for m in q_basis), tuple(m.q for m in p_basis))
         t = self._tables.get(key)

@@ -1,0 +1,66 @@
+"""Step-by-step diagnostics of the bootstrapping circuit at a small ring (debug aid)."""
+import math
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+from paper_2512_18345_b200 import ckks, keyswitch as ks
+from paper_2512_18345_b200.bootstrap import BootstrapConfig, Bootstrapper
+from paper_2512_18345_b200.params import ParameterSet, generate_parameter_set
+
+logn = int(sys.argv[1]) if len(sys.argv) > 1 else 11
+N = 1 << logn
+p = generate_parameter_set(n=N, l=36, dnum=3, delta=1 << 40, h_dense=32, h_sparse=32) if logn < 16 \
+    else ParameterSet.builtin("ks48")
+sk = ks.keygen(p, h=32, seed=1)
+t0 = time.time()
+boot = Bootstrapper(p, sk, BootstrapConfig())
+print(f"setup {time.time() - t0:.1f}s  levels: cts {boot.lvl_cts} evalmod {boot.lvl_evalmod} stc {boot.lvl_stc} out {boot.out_level}",
+      "rotation keys", len(boot.keys.galois))
+rng = np.random.default_rng(0)
+n = N // 2
+z = rng.uniform(-1, 1, n) + 1j * rng.uniform(-1, 1, n)
+ct = ckks.encrypt(ckks.encode(z, p, level=2, scale=boot.delta_in), sk, p, seed=5)
+print("fresh err", np.abs(ckks.decrypt_decode(ct, sk, p) - z).max())
+
+raised = boot.mod_raise(ct)
+# decrypt the raised ciphertext: t = Delta*m + e + Q0*I
+d = ckks.decrypt(ckks.mod_drop(raised, 4), sk)
+from paper_2512_18345_b200.transform import ntt_polynomial
+tco = ckks._centered_coeffs(ntt_polynomial(d.poly, "inverse"))
+I = np.rint(tco / boot.q0)
+print("ModRaise: max |I| =", np.abs(I).max(), " residual vs Delta*m:",
+      np.abs((tco - I * boot.q0) / boot.delta_in - ckks.Embedding(N).to_coeffs(z)).max())
+
+lo, hi = boot.coeff_to_slot(raised)
+y_true = 2 * math.pi * tco / (boot.q0 * (1 << boot.cfg.squarings))
+def bitrev_perm(n):
+    lg = n.bit_length() - 1
+    idx = np.arange(n); out = np.zeros(n, dtype=np.int64)
+    for b in range(lg): out |= ((idx >> b) & 1) << (lg - 1 - b)
+    return out
+R = bitrev_perm(n)
+got_lo = ckks.decrypt_decode(lo, sk, p)
+got_hi = ckks.decrypt_decode(hi, sk, p)
+print("CtS: err lo", np.abs(got_lo - y_true[:n][R]).max(), " err hi", np.abs(got_hi - 1j * y_true[n:][R]).max(),
+      " max|y|", np.abs(y_true).max(), "level", ckks.level_of(lo))
+
+kappa = boot.q0 / (4.0 * math.pi * boot.delta_in) / 1j
+e = boot._exp_taylor(lo, boot.coef_lo)
+print("Taylor: err", np.abs(ckks.decrypt_decode(e, sk, p) - np.exp(1j * y_true[:n][R])).max(), "level", ckks.level_of(e))
+m_lo = boot.eval_mod(lo, boot.coef_lo, kappa)
+m_true = ckks.Embedding(N).to_coeffs(z)
+print("EvalMod lo: err", np.abs(ckks.decrypt_decode(m_lo, sk, p) - m_true[:n][R]).max(), "level", ckks.level_of(m_lo))
+m_hi = boot.eval_mod(hi, boot.coef_hi, kappa * 1j)
+print("EvalMod hi: err", np.abs(ckks.decrypt_decode(m_hi, sk, p) - 1j * m_true[n:][R]).max())
+out = boot.slot_to_coeff(ckks.add(m_lo, m_hi))
+out = ckks.Ciphertext(out.a, out.b, boot.out_scale)
+err = np.abs(ckks.decrypt_decode(out, sk, p) - z).max()
+print(f"bootstrap: level {ckks.level_of(out)}  max err {err:.3e} = 2^{math.log2(err):.2f}")
+import torch
+torch.cuda.synchronize(); t0 = time.time()
+out2 = boot.bootstrap(ct); torch.cuda.synchronize()
+print(f"bootstrap wall (eager, python-driven): {(time.time() - t0) * 1e3:.1f} ms")
