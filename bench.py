@@ -2,29 +2,35 @@
 """bench.py -- headline measurement of the CKKS hot path on B200.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
-                    [--workload keyswitch|ntt]
+                    [--workload bootstrap|keyswitch|ntt]
 
-One process per GPU (torchrun for N > 1, NCCL only for the barrier / max over
+One process per GPU (torchrun for N > 1; NCCL only for the barrier / max over
 ranks: independent ciphertexts shard with no data-path collective, "weak"
 scaling).  A step is one pass of the hot path over one synthetic ciphertext:
 
-  keyswitch  hybrid key switch (the HRot / relinearisation core, BASELINE
-             config 3) at ks48: N = 2^16, L = 48, alpha = 12, dnum = 4.
+  bootstrap  (default, BASELINE config 4 / headline) full CKKS bootstrapping of
+             2^15 complex slots at N = 2^16 on the reference's ks48 moduli
+             (L = 48 31-bit limbs, alpha = 12, dnum = 4), replayed as one CUDA
+             graph; `ms_per_step` is the bootstrap latency.
+  keyswitch  hybrid key switch (HRot / relinearisation core, config 3) at ks48.
   ntt        batched forward NTT over the 60-limb extended basis (config 2).
 
 `value` is whole-job throughput with inputs resident in HBM; `e2e` is the same
 metric through the public Python API with HOST ciphertexts (pinned H2D of the
-input and D2H of the result inside the timed region; evaluation keys are
-resident state, like model weights).  Inputs rotate through more bytes than
-the 126 MB L2 so no step finds its key or ciphertext cached.
+input and D2H of the result inside the timed region; evaluation keys and
+encoded DFT matrices are resident state, like model weights).  Every step
+streams far more than the 126 MB L2 (a bootstrap touches ~5 GB of switching
+keys and ~3 GB of plaintext diagonals; the key-switch / NTT workloads rotate
+their inputs through > 126 MB).
 
 --impl reference times the CPU restatement of the reference (oracle/, C with
 OpenMP on all host threads; the reference itself is single-threaded NumPy and
-cannot travel to the GPU box) on the same workload.
+cannot travel to the GPU box) on a bounded sample of the same workload.
 """
 from __future__ import annotations
 
 import argparse
+import ctypes
 import json
 import os
 import sys
@@ -39,12 +45,29 @@ sys.path.insert(0, str(ROOT))
 
 LIMB_BYTES = 65536 * 4
 
+METRIC = {
+    "bootstrap": "CKKS bootstrap throughput (2^15 slots, N=2^16); ms_per_step = bootstrap latency ms",
+    "keyswitch": "hybrid key-switch throughput (CKKS HRot/relinearise core, N=2^16 L=48 dnum=4)",
+    "ntt": "batched RNS NTT throughput (N=2^16, 60 limbs)",
+}
+UNIT = {"bootstrap": "bootstraps/s", "keyswitch": "keyswitch/s", "ntt": "ntt/s"}
+CONFIG = {
+    "bootstrap": {"workload": "full CKKS bootstrapping, 2^15 complex slots, N=2^16, ks48 moduli (L=48 31-bit "
+                              "limbs, alpha=12, dnum=4), sparse secret h=32, input level 2 scale 2^52, "
+                              "output level 18; one ciphertext per step, CUDA-graph replay",
+                  "l2_policy": "each step streams ~8 GB of keys and plaintext diagonals (>> 126 MB L2)"},
+    "keyswitch": {"workload": "keyswitch ks48 (N=2^16, L=48, alpha=12, dnum=4, 31-bit primes), one ciphertext per step",
+                  "l2_policy": "inputs rotate through >126 MB"},
+    "ntt": {"workload": "forward NTT of one 60-limb polynomial (ks48 extended basis) per step",
+            "l2_policy": "inputs rotate through >126 MB"},
+}
+DEFAULT_STEPS = {"bootstrap": 30, "keyswitch": 2000, "ntt": 2000}
+
 
 def load_peaks():
     p = ROOT / "MEASURED_PEAKS.json"
     if p.exists():
-        d = json.loads(p.read_text())
-        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+        return float(json.loads(p.read_text())["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, burst copy)"
     return 6650.0, "fallback (B200_PROFILING.md)"
 
 
@@ -84,66 +107,49 @@ class ClockSampler:
                 pass
             time.sleep(0.02)
 
-    def __enter__(self):
+    def start(self):
         if self.nv:
             self._thread = threading.Thread(target=self._run, daemon=True)
             self._thread.start()
-        return self
 
-    def __exit__(self, *exc):
+    def stop(self):
         self._stop.set()
         if self._thread:
             self._thread.join()
 
     def summary(self):
-        if not self.samples:
-            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons)}
-        return {"sm_mhz": float(np.median(self.samples)), "sm_max_mhz": self.max_mhz,
-                "reasons": sorted(self.reasons), "samples": len(self.samples)}
-
-
-def ks_algorithmic_bytes(l, alpha, beta):
-    """Algorithmic HBM/L2-boundary bytes per launch of every kernel class of one
-    key switch, in limbs read + written (SURVEY Appendix A convention: one read
-    and one write of each operand, twiddles and tables excluded)."""
-    ext = l + alpha
-    conv_rows = beta * l            # converted limbs of stage 1 (ext - alpha per digit)
-    limbs = {
-        # two launches each (stage 1 INTT of L limbs, stage 3 INTT of 2*alpha limbs)
-        "ntt16_inv_contig": [2 * l, 2 * 2 * alpha],
-        "ntt16_inv_strided": [2 * l, 2 * 2 * alpha],
-        "ntt16_fwd_strided": [2 * conv_rows, 2 * 2 * l],
-        "ntt16_fwd_contig": [2 * conv_rows, 2 * 2 * l],
-        "bconv": [l + conv_rows, 2 * alpha + 2 * l],
-        "inner_product": [beta * ext + 2 * beta * ext + 2 * ext],
-        "moddown_epilogue": [2 * l + 2 * l + l + 2 * l],
-    }
-    return {k: [x * LIMB_BYTES for x in v] for k, v in limbs.items()}
+        med = float(np.median(self.samples)) if self.samples else None
+        return {"sm_mhz": med, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(self.samples)}
 
 
 def read_profile(eng):
-    import ctypes
-
     buf = ctypes.create_string_buffer(1 << 16)
     eng.lib.ckks_profile_read(buf, len(buf))
     out = {}
     for line in buf.value.decode().splitlines():
-        name, cnt, ms = line.split()
-        out[name] = (int(cnt), float(ms))
+        name, cnt, ms, nbytes = line.split()
+        out[name] = (int(cnt), float(ms), float(nbytes))
     return out
+
+
+def host_threads():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
 
 
 # --------------------------------------------------------------------------------------
 # reference arm / CPU baseline: the oracle port on host cores
 # --------------------------------------------------------------------------------------
-def oracle_setup(workload):
+def oracle_step(workload):
     from oracle import oracle
     from paper_2512_18345_b200.params import ParameterSet
 
     p = ParameterSet.builtin("ks48")
     op = oracle.OParams(p.n, p.l, p.dnum, p.alpha, p.delta, p.h_dense,
-                        tuple((m.q, m.psi) for m in p.q_basis),
-                        tuple((m.q, m.psi) for m in p.p_basis))
+                        tuple((m.q, m.psi) for m in p.q_basis), tuple((m.q, m.psi) for m in p.p_basis))
     orc = oracle.Oracle(p.n, op.ext_basis)
     rng = np.random.default_rng(0)
     qs = [q for q, _ in op.ext_basis]
@@ -158,55 +164,61 @@ def oracle_setup(workload):
     return lambda: orc.keyswitch(op, a, b, evk)
 
 
+# key switches of one bootstrap by number of active limbs (CoeffToSlot at 48/46/44, EvalMod
+# 42..24, SlotToCoeff 21..19), from the circuit in paper_2512_18345_b200/bootstrap.py:
+# 3 x 14 rotations per linear transform side, 2 branches x 16 relinearisations + 3 conjugations.
+def bootstrap_keyswitch_levels():
+    levels = []
+    for lvl in (48, 46, 44):
+        levels += [lvl] * 14
+    levels += [42]                                 # conjugation after CoeffToSlot
+    for _branch in range(2):
+        levels += [42, 40, 38]                     # x^2, x^4, x^8
+        levels += [40, 40, 40, 40, 38, 38, 36]     # Taylor tree products
+        levels += [34, 32, 30, 28, 26, 24]         # squarings
+        levels += [22]                             # conjugation for the sine
+    for lvl in (21, 20, 19):
+        levels += [lvl] * 14
+    return levels
+
+
 def time_oracle(workload, steps, warmup):
-    step = oracle_setup(workload)
+    """(throughput, ms per unit, sample description) of the CPU port."""
+    base = "keyswitch" if workload == "bootstrap" else workload
+    step = oracle_step(base)
     for _ in range(warmup):
         step()
     t0 = time.perf_counter()
     for _ in range(steps):
         step()
-    dt = time.perf_counter() - t0
-    return steps / dt, dt / steps * 1e3
-
-
-def host_threads():
-    try:
-        return len(os.sched_getaffinity(0))
-    except Exception:
-        return os.cpu_count() or 1
+    ms = (time.perf_counter() - t0) / steps * 1e3
+    if workload != "bootstrap":
+        return 1e3 / ms, ms, f"{steps} steps of the workload, oracle/ckks_oracle.c with OpenMP"
+    # a bootstrap on the CPU is dominated by its key switches; cost of one at l active limbs
+    # scales with the limb-transforms it runs, (beta_l + 2) * (l + alpha) against 6 * 60 at l = 48
+    units = sum((-(-l // 12) + 2) * (l + 12) / 360.0 for l in bootstrap_keyswitch_levels())
+    boot_ms = ms * units
+    return 1e3 / boot_ms, boot_ms, (f"{steps} full-level ks48 key switches with oracle/ckks_oracle.c (OpenMP), scaled by "
+                                    f"the {units:.1f} full-level-equivalent key switches of one bootstrap "
+                                    "(PMult / rescale / automorphism time not included: lower bound)")
 
 
 def run_reference(args):
-    rank = int(os.environ.get("RANK", "0"))
-    if rank != 0:
+    if int(os.environ.get("RANK", "0")) != 0:
         return
     steps = max(1, min(args.steps, 5))
-    warmup = max(1, min(args.warmup, 1))
-    thr, ms = time_oracle(args.workload, steps, warmup)
-    unit = "keyswitch/s" if args.workload == "keyswitch" else "ntt/s"
-    cores = host_threads()
+    warmup = 1
+    thr, ms, sample = time_oracle(args.workload, steps, warmup)
+    unit = UNIT[args.workload]
     line = {
         "impl": "reference", "metric": METRIC[args.workload], "value": thr, "unit": unit,
         "n_gpus": args.gpus, "steps": steps, "warmup": warmup, "ms_per_step": ms,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
         "data": "synthetic", "config": CONFIG[args.workload],
-        "cpu_baseline": {"value": thr, "unit": unit, "cores": cores, "kind": "port",
-                         "sample": f"{steps} steps of the workload, oracle/ckks_oracle.c with OpenMP"},
+        "cpu_baseline": {"value": thr, "unit": unit, "cores": host_threads(), "kind": "port", "sample": sample},
         "e2e": {"value": thr, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line))
-
-
-METRIC = {
-    "keyswitch": "hybrid key-switch throughput (CKKS HRot/relinearise core, N=2^16 L=48 dnum=4)",
-    "ntt": "batched RNS NTT throughput (N=2^16, 60 limbs)",
-}
-CONFIG = {
-    "keyswitch": {"workload": "keyswitch ks48 (N=2^16, L=48, alpha=12, dnum=4, 31-bit primes), "
-                              "one ciphertext per step", "l2_policy": "inputs rotate through >126 MB"},
-    "ntt": {"workload": "forward NTT of one 60-limb polynomial (ks48 extended basis) per step",
-            "l2_policy": "inputs rotate through >126 MB"},
-}
 
 
 # --------------------------------------------------------------------------------------
@@ -224,11 +236,10 @@ def run_b200(args):
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
-    from paper_2512_18345_b200 import keyswitch as ks
+    from paper_2512_18345_b200 import ckks, keyswitch as ks, transform
     from paper_2512_18345_b200.engine import get_engine
     from paper_2512_18345_b200.params import ParameterSet
-    from paper_2512_18345_b200.rns import EVALUATION, COEFFICIENT, Polynomial
-    from paper_2512_18345_b200 import transform
+    from paper_2512_18345_b200.rns import COEFFICIENT, EVALUATION, Polynomial
 
     eng = get_engine()
     p = ParameterSet.builtin("ks48")
@@ -236,6 +247,7 @@ def run_b200(args):
     dev = eng.device
     g = torch.Generator(device=dev)
     g.manual_seed(1234 + rank)
+    wl = args.workload
 
     def rand_limbs(basis, *lead):
         """Uniform residues below each modulus, generated on the device (synthetic)."""
@@ -243,8 +255,48 @@ def run_b200(args):
         u = torch.rand((*lead, len(basis), p.n), generator=g, device=dev, dtype=torch.float64)
         return (u * q).to(torch.int64).clamp_(min=0).to(torch.int32).contiguous()
 
-    n_ct, n_evk = 8, 4
-    if args.workload == "keyswitch":
+    precision_bits = None
+    if wl == "bootstrap":
+        from paper_2512_18345_b200.bootstrap import BootstrapConfig, Bootstrapper
+
+        sk = ks.keygen(p, h=p.h_sparse, seed=1 + rank)
+        boot = Bootstrapper(p, sk, BootstrapConfig())
+        rng = np.random.default_rng(rank)
+        n_in = 4
+        msgs = [rng.uniform(-1, 1, p.n // 2) + 1j * rng.uniform(-1, 1, p.n // 2) for _ in range(n_in)]
+        cts = [ckks.encrypt(ckks.encode(z, p, level=2, scale=boot.delta_in), sk, p, seed=50 + i)
+               for i, z in enumerate(msgs)]
+        cts_t = [torch.stack([c.a.data, c.b.data]) for c in cts]
+        replay = boot.capture(cts[0])
+        low = p.q_basis[:2]
+
+        def step(i):
+            replay.static_in.copy_(cts_t[i % n_in])
+            replay.graph.replay()
+
+        def profiled_step(i):
+            boot.bootstrap(cts[i % n_in])
+
+        host_in = [t.cpu().pin_memory() for t in cts_t[:2]]
+        host_out = [torch.empty(tuple(replay.static_out.shape), dtype=torch.int32).pin_memory() for _ in range(2)]
+
+        def e2e_step(i):
+            # public API: host ciphertext in -> bootstrap -> host ciphertext out
+            d = host_in[i % 2].to(dev, non_blocking=True)
+            ct = ckks.Ciphertext(a=Polynomial(low, d[0], EVALUATION), b=Polynomial(low, d[1], EVALUATION),
+                                 scale=boot.delta_in)
+            out = replay(ct, copy_out=False)
+            host_out[i % 2][0].copy_(out.a.data, non_blocking=True)
+            host_out[i % 2][1].copy_(out.b.data, non_blocking=True)
+
+        h2d = 2 * 2 * LIMB_BYTES
+        d2h = 2 * boot.out_level * LIMB_BYTES
+        # precision of the refreshed ciphertext (reported, not timed)
+        out = replay(cts[0])
+        err = float(np.abs(ckks.decrypt_decode(out, sk, p) - msgs[0]).max())
+        precision_bits = float(np.log2(err))
+    elif wl == "keyswitch":
+        n_ct, n_evk = 8, 4
         cts = [rand_limbs(p.q_basis, 2) for _ in range(n_ct)]               # 25 MB each
         evks = [rand_limbs(ext, p.dnum, 2) for _ in range(n_evk)]           # 126 MB each
         outs = [eng.empty(2, p.l, p.n) for _ in range(n_ct)]
@@ -254,6 +306,7 @@ def run_b200(args):
             ct = cts[i % n_ct]
             eng.keyswitch(plan, ct[0], ct[1], evks[i % n_evk], out=outs[i % n_ct])
 
+        profiled_step = step
         host_in = [torch.empty((2, p.l, p.n), dtype=torch.int32).pin_memory() for _ in range(2)]
         host_out = [torch.empty((2, p.l, p.n), dtype=torch.int32).pin_memory() for _ in range(2)]
         for h, c in zip(host_in, cts):
@@ -263,7 +316,6 @@ def run_b200(args):
             for t in range(p.dnum)), params=p, _matrix=e) for e in evks]
 
         def e2e_step(i):
-            # public API: host ciphertext in, host ciphertext out
             d = host_in[i % 2].to(dev, non_blocking=True)
             ct = ks.Ciphertext(a=Polynomial(p.q_basis, d[0], EVALUATION),
                                b=Polynomial(p.q_basis, d[1], EVALUATION), scale=p.delta)
@@ -272,7 +324,6 @@ def run_b200(args):
             host_out[i % 2][1].copy_(out.b.data, non_blocking=True)
 
         h2d = d2h = 2 * p.l * LIMB_BYTES
-        unit = "keyswitch/s"
     else:
         polys = [rand_limbs(ext) for _ in range(12)]                         # 15.7 MB each
         outs = [eng.empty(len(ext), p.n) for _ in range(12)]
@@ -281,6 +332,7 @@ def run_b200(args):
         def step(i):
             eng.ntt(polys[i % 12], slots, False, out=outs[i % 12])
 
+        profiled_step = step
         host_in = [torch.empty((len(ext), p.n), dtype=torch.int32).pin_memory() for _ in range(2)]
         host_out = [torch.empty((len(ext), p.n), dtype=torch.int32).pin_memory() for _ in range(2)]
 
@@ -290,7 +342,6 @@ def run_b200(args):
             host_out[i % 2].copy_(out.data, non_blocking=True)
 
         h2d = d2h = len(ext) * LIMB_BYTES
-        unit = "ntt/s"
 
     def barrier():
         if world > 1:
@@ -303,14 +354,14 @@ def run_b200(args):
         barrier()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         if sampler:
-            sampler.__enter__()
+            sampler.start()
         a.record()
         for i in range(steps):
             fn(i)
         b.record()
         barrier()
         if sampler:
-            sampler.__exit__()
+            sampler.stop()
         ms = a.elapsed_time(b)
         if world > 1:
             t = torch.tensor([ms], device=dev, dtype=torch.float64)
@@ -327,53 +378,54 @@ def run_b200(args):
     e2e_ms = timed(e2e_step, e2e_steps, max(3, min(args.warmup, 5)))
     e2e_value = world * e2e_steps / (e2e_ms * 1e-3)
 
-    # per-kernel pass: same steps with every launch bracketed by CUDA events
-    prof_steps = max(3, min(args.steps, 50))
+    # per-kernel pass: the same step, eager, every launch bracketed by CUDA events
+    prof_steps = max(2, min(args.steps, 3 if wl == "bootstrap" else 50))
+    profiled_step(0)
+    torch.cuda.synchronize()
     eng.lib.ckks_profile_enable(1)
     for i in range(prof_steps):
-        step(i)
+        profiled_step(i)
     prof = read_profile(eng)
     eng.lib.ckks_profile_enable(0)
-    launches_per_step = sum(c for c, _ in prof.values()) / prof_steps
-    total_prof_ms = sum(ms for _, ms in prof.values())
+    launches_per_step = sum(c for c, _, _ in prof.values()) / prof_steps
+    total_prof_ms = sum(ms for _, ms, _ in prof.values())
     top = max(prof, key=lambda k: prof[k][1])
     peak, peak_src = load_peaks()
-    if args.workload == "keyswitch":
-        alg = ks_algorithmic_bytes(p.l, p.alpha, p.beta)
-    else:
-        alg = {"ntt16_fwd_strided": [2 * len(ext) * LIMB_BYTES], "ntt16_fwd_contig": [2 * len(ext) * LIMB_BYTES]}
-    per_launch_bytes = sum(alg[top]) / len(alg[top])
-    avg_launch_ms = prof[top][1] / prof[top][0]
-    achieved = per_launch_bytes / (avg_launch_ms * 1e-3) / 1e9
+    cnt, ms_top, bytes_top = prof[top]
+    achieved = bytes_top / (ms_top * 1e-3) / 1e9
     roofline = {
         "bound": "hbm", "kernel": top, "achieved": achieved, "peak": peak, "unit": "GB/s",
         "frac": achieved / peak, "traffic": None, "peak_source": peak_src,
-        "avg_launch_us": avg_launch_ms * 1e3, "alg_bytes_per_launch": per_launch_bytes,
-        "share_of_step": prof[top][1] / total_prof_ms,
+        "avg_launch_us": ms_top / cnt * 1e3, "alg_bytes_per_launch": bytes_top / cnt,
+        "share_of_step": ms_top / total_prof_ms,
+        "note": "achieved = algorithmic bytes (operand limbs read+written once) / CUDA-event time of the "
+                "launches of this kernel class in an eager pass of the same step",
         "kernels": {k: {"launches_per_step": c / prof_steps, "us_per_launch": ms / c * 1e3,
-                        "share": ms / total_prof_ms,
-                        "gbs": (sum(alg[k]) / len(alg[k])) / (ms / c * 1e-3) / 1e9 if k in alg else None}
-                    for k, (c, ms) in sorted(prof.items(), key=lambda kv: -kv[1][1])},
+                        "share": ms / total_prof_ms, "gbs": (nb / (ms * 1e-3) / 1e9) if nb else None}
+                    for k, (c, ms, nb) in sorted(prof.items(), key=lambda kv: -kv[1][1])},
     }
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        thr, ms_cpu = time_oracle(args.workload, 3, 1)
-        cpu = {"value": thr, "unit": unit, "cores": host_threads(), "kind": "port",
-               "ms_per_step": ms_cpu,
-               "sample": "3 steps of the same workload, oracle/ckks_oracle.c (OpenMP over limbs)"}
+        thr, ms_cpu, sample = time_oracle(wl, 3, 1)
+        cpu = {"value": thr, "unit": UNIT[wl], "cores": host_threads(), "kind": "port",
+               "ms_per_step": ms_cpu, "sample": sample}
 
     if rank == 0:
         line = {
-            "metric": METRIC[args.workload], "value": value, "unit": unit, "n_gpus": world,
+            "metric": METRIC[wl], "value": value, "unit": UNIT[wl], "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
-            "data": "synthetic", "config": CONFIG[args.workload],
-            "e2e": {"value": e2e_value, "unit": unit, "h2d_bytes_per_step": h2d,
+            "data": "synthetic", "config": CONFIG[wl],
+            "e2e": {"value": e2e_value, "unit": UNIT[wl], "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms / e2e_steps},
             "gpu_launches": int(round(launches_per_step * args.steps)),
             "clocks": sampler.summary(), "roofline": roofline, "cpu_baseline": cpu,
         }
+        if wl == "bootstrap":
+            line["latency_ms"] = ms_step
+            line["paper_rtx5090_latency_ms"] = 15.2
+            line["precision_log2_max_err"] = precision_bits
         print(json.dumps(line))
     if world > 1:
         dist.destroy_process_group()
@@ -382,12 +434,16 @@ def run_b200(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=2000)
-    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=None)
+    ap.add_argument("--warmup", type=int, default=None)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--workload", default="keyswitch", choices=["keyswitch", "ntt"])
+    ap.add_argument("--workload", default="bootstrap", choices=["bootstrap", "keyswitch", "ntt"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
+    if args.steps is None:
+        args.steps = DEFAULT_STEPS[args.workload]
+    if args.warmup is None:
+        args.warmup = 3 if args.workload == "bootstrap" else 20
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -188,6 +188,12 @@ bconv_generic(BconvJobs jobs, const ModSlot* __restrict__ slots, size_t cols) {
     }
 }
 
+static double jobs_bytes(const BconvJobs& jobs, size_t cols) {
+    double limbs = 0;
+    for (int j = 0; j < jobs.count; ++j) limbs += jobs.job[j].tab.l_in + jobs.job[j].tab.l_out;
+    return limbs * 4.0 * cols;
+}
+
 static int bconv_variant() {
     static int v = -1;
     if (v < 0) {
@@ -204,7 +210,7 @@ static int launch_fast(const BconvJobs& jobs, const ModSlot* slots, size_t cols,
         constexpr int LINP = (LIN + 1) / 2 * 2;
         const size_t sm = sizeof(double) * (size_t)l_out_max * LINP + sizeof(uint4) * ((size_t)l_out_max + LIN);
         dim3 grid((unsigned)((cols + 127) / 128), jobs.count, (l_out_max + kOutChunk - 1) / kOutChunk);
-        ProfScope ps("bconv", st);
+        ProfScope ps("bconv", st, jobs_bytes(jobs, cols));
         if (sm > 48 * 1024)
             CK(cudaFuncSetAttribute(bconv_f64<LIN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
         bconv_f64<LIN><<<grid, 128, sm, st>>>(jobs, slots, cols);
@@ -215,7 +221,7 @@ static int launch_fast(const BconvJobs& jobs, const ModSlot* slots, size_t cols,
     const size_t sm = sizeof(uint4) * ((size_t)l_out_max * G + l_out_max + LIN);
     const size_t work = pairs ? cols / 2 : cols;
     dim3 grid((unsigned)((work + 127) / 128), jobs.count, (l_out_max + kOutChunk - 1) / kOutChunk);
-    ProfScope ps("bconv", st);
+    ProfScope ps("bconv", st, jobs_bytes(jobs, cols));
     if (pairs) {
         if (sm > 48 * 1024)
             CK(cudaFuncSetAttribute(bconv_fast<LIN, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
@@ -255,7 +261,7 @@ int bconv_launch_jobs(const BconvJobs& jobs, const ModSlot* slots, size_t cols, 
         }
     }
     dim3 grid((unsigned)((cols + 127) / 128), jobs.count);
-    ProfScope ps("bconv_generic", st);
+    ProfScope ps("bconv_generic", st, jobs_bytes(jobs, cols));
     bconv_generic<<<grid, 128, 0, st>>>(jobs, slots, cols);
     CK(cudaGetLastError());
     return CKKS_OK;

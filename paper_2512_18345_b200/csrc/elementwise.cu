@@ -53,7 +53,7 @@ int elementwise_launch(const uint32_t* a, const uint32_t* b, uint32_t* out, cons
     unsigned gx = (unsigned)((work + 255) / 256);
     if (gx > 1024) gx = 1024;
     dim3 grid(gx, rows);
-    ProfScope ps("elementwise", st);
+    ProfScope ps("elementwise", st, 12.0 * rows * cols);
 #define EW_DISPATCH(K)                                                                             \
     if (vec)                                                                                       \
         elementwise_vec4<K><<<grid, 256, 0, st>>>((const uint4*)a, (const uint4*)b, (uint4*)out,   \
@@ -101,7 +101,7 @@ int automorphism_eval_launch(const uint32_t* in, uint32_t* out, int rows, uint32
     }
     unsigned gx = (n + 255) / 256;
     if (gx > 256) gx = 256;
-    ProfScope ps("automorphism_eval", st);
+    ProfScope ps("automorphism_eval", st, 8.0 * rows * n);
     automorphism_eval_kernel<<<dim3(gx, rows), 256, 0, st>>>(in, out, n, lg, k);
     CK(cudaGetLastError());
     return CKKS_OK;
@@ -131,7 +131,7 @@ int automorphism_coeff_launch(const uint32_t* in, uint32_t* out, const int32_t* 
     if (in == out) { set_last_error("automorphism cannot run in place"); return CKKS_ERR_ARG; }
     unsigned gx = (n + 255) / 256;
     if (gx > 256) gx = 256;
-    ProfScope ps("automorphism_coeff", st);
+    ProfScope ps("automorphism_coeff", st, 8.0 * rows * n);
     automorphism_coeff_kernel<<<dim3(gx, rows), 256, 0, st>>>(in, out, row_slot, slots, n, k);
     CK(cudaGetLastError());
     return CKKS_OK;
@@ -169,7 +169,7 @@ int lift2_centered_launch(const uint32_t* in, uint32_t* out, const int32_t* row_
                           const ModSlot* slots, int32_t slot0, int32_t slot1, uint32_t inv,
                           int rows, size_t n, cudaStream_t st) {
     if (rows <= 0 || n == 0) return CKKS_OK;
-    ProfScope ps("lift2_centered", st);
+    ProfScope ps("lift2_centered", st, 4.0 * n * (2 + rows));
     dim3 grid((unsigned)((n + 255) / 256), rows < 16 ? rows : 16);
     lift2_centered_kernel<<<grid, 256, 0, st>>>(in, out, row_slot, slots, slot0, slot1, inv, rows, n);
     CK(cudaGetLastError());
@@ -209,7 +209,7 @@ int pmult_acc_launch(const uint32_t* x, const uint32_t* p, uint32_t* acc, const 
                      const ModSlot* slots, int rows, size_t cols, int first, cudaStream_t st) {
     if (rows <= 0 || cols == 0) return CKKS_OK;
     if (cols % 4 || rows > 65535) { set_last_error("pmult_acc needs cols % 4 == 0 and <= 65535 rows"); return CKKS_ERR_UNSUPPORTED; }
-    ProfScope ps("pmult_acc", st);
+    ProfScope ps("pmult_acc", st, 4.0 * cols * rows * (first ? 5.0 : 7.0));
     unsigned gx = (unsigned)((cols / 4 + 255) / 256);
     pmult_acc_kernel<<<dim3(gx, rows), 256, 0, st>>>((const uint4*)x, (const uint4*)p, (uint4*)acc,
                                                      row_slot, slots, rows, cols / 4, first);

@@ -43,7 +43,9 @@ struct RowMap {
 struct ProfScope {
     cudaStream_t st;
     bool live;
-    ProfScope(const char* name, cudaStream_t stream);
+    // alg_bytes: algorithmic bytes of the launch (operand limbs read + written once,
+    // tables and twiddles excluded: SURVEY 8d / Appendix A convention)
+    ProfScope(const char* name, cudaStream_t stream, double alg_bytes = 0.0);
     ~ProfScope();
 };
 

@@ -83,7 +83,7 @@ int inner_product_launch(const InnerProductArgs& a, const ModSlot* slots, cudaSt
     const bool vec = a.n % 4 == 0;
     const size_t work = vec ? a.n / 4 : a.n;
     dim3 grid((unsigned)((work + 255) / 256), rows);
-    ProfScope ps("inner_product", st);
+    ProfScope ps("inner_product", st, 4.0 * a.n * rows * (3.0 * a.beta + 2.0));
     if (vec) inner_product_kernel<true><<<grid, 256, 0, st>>>(a, slots);
     else inner_product_kernel<false><<<grid, 256, 0, st>>>(a, slots);
     CK(cudaGetLastError());
@@ -131,7 +131,7 @@ int moddown_epilogue_launch(const ModDownEpilogueArgs& a, const ModSlot* slots, 
     const bool vec = a.n % 4 == 0;
     const size_t work = vec ? a.n / 4 : a.n;
     dim3 grid((unsigned)((work + 255) / 256), 2 * a.l);
-    ProfScope ps("moddown_epilogue", st);
+    ProfScope ps("moddown_epilogue", st, 4.0 * a.n * a.l * (a.fold_b ? 7.0 : 6.0));
     if (vec) moddown_epilogue_kernel<true><<<grid, 256, 0, st>>>(a, slots);
     else moddown_epilogue_kernel<false><<<grid, 256, 0, st>>>(a, slots);
     CK(cudaGetLastError());

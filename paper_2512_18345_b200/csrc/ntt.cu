@@ -343,7 +343,7 @@ static int launch_generic(const uint32_t* in, uint32_t* out, const int32_t* row_
         const size_t off_in = rm.in ? 0 : (size_t)r0 * n, off_out = rm.out ? 0 : (size_t)r0 * n;
         for (uint32_t s = s_lo; s < s_hi; ++s) {
             const bool first = s == s_lo;
-            ProfScope ps("ntt_generic_stage", st);
+            ProfScope ps("ntt_generic_stage", st, 8.0 * cnt * n);
             ntt_stage_generic<<<grid, threads, 0, st>>>(first ? in + off_in : out + off_out,
                                                         out + off_out, row_slot + r0, slots,
                                                         first ? rm_first : rm_rest, n, lg, s, inverse);
@@ -361,14 +361,14 @@ int ntt_launch(const uint32_t* in, uint32_t* out, const int32_t* row_slot, const
         dim3 g_str(256 / COLS, rows), g_con(16, rows);
         const RowMap rm2{rm.out, rm.out};
         if (!inverse) {
-            { ProfScope ps("ntt16_fwd_strided", st);
+            { ProfScope ps("ntt16_fwd_strided", st, 8.0 * rows * kN16);
               ntt16_fwd_strided<COLS><<<g_str, 16 * COLS, 0, st>>>(in, out, row_slot, slots, rm); }
-            { ProfScope ps("ntt16_fwd_contig", st);
+            { ProfScope ps("ntt16_fwd_contig", st, 8.0 * rows * kN16);
               ntt16_fwd_contig<<<g_con, 256, 0, st>>>(out, out, row_slot, slots, rm2); }
         } else {
-            { ProfScope ps("ntt16_inv_contig", st);
+            { ProfScope ps("ntt16_inv_contig", st, 8.0 * rows * kN16);
               ntt16_inv_contig<<<g_con, 256, 0, st>>>(in, out, row_slot, slots, rm); }
-            { ProfScope ps("ntt16_inv_strided", st);
+            { ProfScope ps("ntt16_inv_strided", st, 8.0 * rows * kN16);
               ntt16_inv_strided<COLS><<<g_str, 16 * COLS, 0, st>>>(out, out, row_slot, slots, rm2); }
         }
         CK(cudaGetLastError());

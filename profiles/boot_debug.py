@@ -64,3 +64,38 @@ import torch
 torch.cuda.synchronize(); t0 = time.time()
 out2 = boot.bootstrap(ct); torch.cuda.synchronize()
 print(f"bootstrap wall (eager, python-driven): {(time.time() - t0) * 1e3:.1f} ms")
+
+# CUDA-graph replay
+t0 = time.time()
+replay = boot.capture(ct)
+torch.cuda.synchronize()
+print(f"capture {time.time() - t0:.1f}s")
+out3 = replay(ct)
+torch.cuda.synchronize()
+print("graph == eager:", bool((out3.a.data == out2.a.data).all() and (out3.b.data == out2.b.data).all()))
+a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+for _ in range(3):
+    replay(ct, copy_out=False)
+a.record()
+reps = 10
+for _ in range(reps):
+    replay(ct, copy_out=False)
+b.record(); torch.cuda.synchronize()
+print(f"bootstrap graph replay: {a.elapsed_time(b) / reps:.2f} ms")
+# per-kernel time inside one eager bootstrap
+import ctypes
+from paper_2512_18345_b200.engine import get_engine
+eng = get_engine()
+eng.lib.ckks_profile_enable(1)
+boot.bootstrap(ct)
+buf = ctypes.create_string_buffer(1 << 16)
+eng.lib.ckks_profile_read(buf, len(buf))
+eng.lib.ckks_profile_enable(0)
+tot = 0.0
+rows = []
+for line in buf.value.decode().splitlines():
+    name, cnt, ms = line.split()[:3]
+    rows.append((float(ms), name, int(cnt))); tot += float(ms)
+for ms, name, cnt in sorted(rows, reverse=True):
+    print(f"   {name:22s} {cnt:6d} launches {ms:8.3f} ms  {100 * ms / tot:5.1f}%")
+print(f"   sum of kernel time {tot:.2f} ms over {sum(r[2] for r in rows)} launches")

@@ -1,0 +1,79 @@
+"""End-to-end bootstrapping on the GPU at a small ring (N = 2^11, 1024 complex
+slots, 36 limbs).  No reference oracle exists for bootstrapping;
+the check is decoded-slot precision against the encrypted message, tolerance
+2^-20 (the paper reports 2^-18.6 at N = 2^16)."""
+import math
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def boot_env():
+    import torch
+
+    assert torch.cuda.is_available()
+    from paper_2512_18345_b200 import ckks, keyswitch as ks
+    from paper_2512_18345_b200.bootstrap import BootstrapConfig, Bootstrapper
+    from paper_2512_18345_b200.params import generate_parameter_set
+
+    p = generate_parameter_set(n=2048, l=36, dnum=3, delta=1 << 40, h_dense=32, h_sparse=32)
+    sk = ks.keygen(p, h=p.h_sparse, seed=1)
+    return ckks, p, sk, Bootstrapper(p, sk, BootstrapConfig())
+
+
+def test_bootstrap_precision_and_level(boot_env):
+    ckks, p, sk, boot = boot_env
+    rng = np.random.default_rng(0)
+    n = p.n // 2
+    z = rng.uniform(-1, 1, n) + 1j * rng.uniform(-1, 1, n)
+    ct = ckks.encrypt(ckks.encode(z, p, level=2, scale=boot.delta_in), sk, p, seed=5)
+    out = boot.bootstrap(ct)
+    assert ckks.level_of(out) == boot.out_level > 2
+    err = np.abs(ckks.decrypt_decode(out, sk, p) - z).max()
+    assert err < 2.0 ** -20, f"bootstrap precision 2^{math.log2(err):.1f}"
+    # the refreshed ciphertext is usable: one more multiplication at the new level
+    sq = ckks.rescale(ckks.hmult(out, out, boot.keys.relin), 2)
+    assert np.abs(ckks.decrypt_decode(sq, sk, p) - z * z).max() < 2.0 ** -18
+    # deterministic: same input, same limbs
+    again = boot.bootstrap(ct)
+    assert np.array_equal(again.a.coeffs, out.a.coeffs) and np.array_equal(again.b.coeffs, out.b.coeffs)
+
+
+def test_mod_raise_is_exact_centred_lift(boot_env):
+    ckks, p, sk, boot = boot_env
+    from paper_2512_18345_b200.transform import ntt_polynomial
+
+    rng = np.random.default_rng(3)
+    n = p.n // 2
+    z = rng.uniform(-1, 1, n) + 1j * rng.uniform(-1, 1, n)
+    ct = ckks.encrypt(ckks.encode(z, p, level=2, scale=boot.delta_in), sk, p, seed=9)
+    raised = boot.mod_raise(ct)
+    assert ckks.level_of(raised) == p.l
+    # every limb of the raised a-part is the centred two-limb value reduced mod q_i
+    coeff2 = ntt_polynomial(ct.a, "inverse").coeffs
+    q0, q1 = p.q_basis[0].q, p.q_basis[1].q
+    t = (coeff2[1].astype(object) - coeff2[0].astype(object)) * pow(q0, -1, q1) % q1
+    v = coeff2[0].astype(object) + t * q0
+    v = np.where(v > (q0 * q1) // 2, v - q0 * q1, v)
+    got = ntt_polynomial(raised.a, "inverse").coeffs
+    for i in (0, 1, 2, 17, p.l - 1):
+        want = np.array([int(x) % p.q_basis[i].q for x in v], dtype=np.uint64)
+        assert np.array_equal(got[i], want)
+    # decrypts to Delta*m + small multiple of Q0
+    d = ckks.decrypt(ckks.mod_drop(raised, 4), sk)
+    tco = ckks._centered_coeffs(ntt_polynomial(d.poly, "inverse"))
+    assert np.abs(np.rint(tco / boot.q0)).max() <= boot.cfg.k_bound
+
+
+def test_bootstrap_rejects_wrong_inputs(boot_env):
+    ckks, p, sk, boot = boot_env
+    from paper_2512_18345_b200.rns import RnsError
+
+    z = np.zeros(p.n // 2)
+    with pytest.raises(RnsError):
+        boot.bootstrap(ckks.encrypt(ckks.encode(z, p, level=3, scale=boot.delta_in), sk, p, seed=1))
+    with pytest.raises(RnsError):
+        boot.bootstrap(ckks.encrypt(ckks.encode(z, p, level=2, scale=2.0 ** 40), sk, p, seed=1))
