@@ -60,6 +60,15 @@ int ckks_profile_read(char* buf, size_t cap);
 int ckks_ctx_create(int device, ckks_ctx** out);
 void ckks_ctx_destroy(ckks_ctx* ctx);
 
+/* Workspace lanes.  Key-switch plans work out of one device arena; with
+ * `lanes` > 1 the arena is replicated so that calls issued on different
+ * streams (independent rotations, the two EvalMod branches of a bootstrap) can
+ * run concurrently: select a lane, then enqueue on that lane's stream.
+ * ckks_set_lanes reallocates (not capturable); ckks_select_lane is host state
+ * only. */
+int ckks_set_lanes(ckks_ctx* ctx, int lanes);
+int ckks_select_lane(ckks_ctx* ctx, int lane);
+
 /* Register modulus q for ring degree n with psi a primitive 2n-th root of
  * unity mod q (already squared down to order 2n, transform.py:88-96) and build
  * its device twiddle tables: fwd[t] = psi^bitrev(t), inv[t] = psi^-bitrev(t),
@@ -112,6 +121,19 @@ int ckks_lift2_centered(ckks_ctx* ctx, const uint32_t* in, int32_t slot0, int32_
  * the BSGS linear transforms; each product is poly_elementwise "mul"). */
 int ckks_pmult_accumulate(ckks_ctx* ctx, const uint32_t* x, const uint32_t* p, uint32_t* acc,
                           const int32_t* row_slot, int rows, size_t cols, int first, void* stream);
+
+/* out = sum_t x[t] (.) p[t] over `count` <= 16 (ciphertext, plaintext) pairs in one
+ * pass; x[t] are DEVICE pointers to [2][rows][cols] ciphertexts, p[t] to
+ * [rows][cols] plaintexts or NULL (term = x[t]); the pointer arrays themselves
+ * are HOST arrays.  The inner sum of a BSGS linear transform (each product is
+ * poly_elementwise "mul", each sum "add", rns.py:243-258). */
+int ckks_fused_terms(ckks_ctx* ctx, int count, const uint32_t* const* x, const uint32_t* const* p,
+                     uint32_t* out, const int32_t* row_slot, int rows, size_t cols, void* stream);
+
+/* Tensor product (front of HMult): x, y [2][rows][cols] -> out [3][rows][cols] =
+ * (b1*b2, a1*b2 + a2*b1, a1*a2). */
+int ckks_tensor(ckks_ctx* ctx, const uint32_t* x, const uint32_t* y, uint32_t* out,
+                const int32_t* row_slot, int rows, size_t cols, void* stream);
 
 /* ---- base conversion: baseconv.py:57-151 ------------------------------------ */
 

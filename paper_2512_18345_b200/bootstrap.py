@@ -122,22 +122,8 @@ def default_groups(lg: int, count: int = 3) -> list[int]:
 # ---------------------------------------------------------------------------
 # homomorphic linear transform (BSGS)
 # ---------------------------------------------------------------------------
-def ct_tensor(ct):
-    """[2, l, n] device tensor of a ciphertext (a view when a and b are adjacent)."""
-    import torch
-
-    a, b = ct.a.data, ct.b.data
-    if a.data_ptr() + a.numel() * 4 == b.data_ptr() and getattr(a, "_base", None) is not None \
-            and a._base is getattr(b, "_base", None):
-        base = a._base
-        if base.dim() == 3 and base.shape[0] == 2 and base.data_ptr() == a.data_ptr():
-            return base
-    return torch.stack([a, b])
-
-
-def ct_from_tensor(t, basis, scale):
-    return ckks.Ciphertext(a=Polynomial(basis, t[0], EVALUATION), b=Polynomial(basis, t[1], EVALUATION),
-                           scale=scale)
+ct_tensor = ckks.ct_tensor
+ct_from_tensor = ckks.ct_from_tensor
 
 
 class LinearTransform:
@@ -183,18 +169,22 @@ class LinearTransform:
             raise RnsError(f"linear transform encoded for level {self.level}, ciphertext at {ckks.level_of(ct)}")
         basis = ct.a.basis
         slots = eng.row_slots(basis)
-        rotated = {b: ct_tensor(ckks.hrot(ct, b * self.step, keys)) for b in self.baby}
-        total = None
-        for g in self.giants:
-            inner = eng.empty(2, self.level, self.params.n)
-            first = True
-            for b, pt in self.table[g].items():
-                eng.pmult_accumulate(rotated[b], pt.poly.data, inner, slots, first)
-                first = False
+        # baby steps: independent rotations of the same input, spread over the lanes
+        rot = eng.fork([(lambda b=b: ct_tensor(ckks.hrot(ct, b * self.step, keys))) for b in self.baby])
+        rotated = dict(zip(self.baby, rot))
+
+        def giant(g):
+            row = self.table[g]
+            inner = eng.fused_terms([rotated[b] for b in row], [pt.poly.data for pt in row.values()], slots)
             part = ct_from_tensor(inner, basis, ct.scale * self.pt_scale)
-            if g:
-                part = ckks.hrot(part, g * self.n1 * self.step, keys)
-            total = part if total is None else ckks.add(total, part)
+            return ckks.hrot(part, g * self.n1 * self.step, keys) if g else part
+
+        parts = eng.fork([(lambda g=g: giant(g)) for g in self.giants])
+        if len(parts) > 1:
+            summed = eng.fused_terms([ct_tensor(x) for x in parts], [None] * len(parts), slots)
+            total = ct_from_tensor(summed, basis, parts[0].scale)
+        else:
+            total = parts[0]
         out = ckks.rescale(total, self.limbs)
         return ckks.Ciphertext(a=out.a, b=out.b, scale=ct.scale)
 
@@ -424,8 +414,10 @@ class Bootstrapper:
         lo, hi = self.coeff_to_slot(raised)
         # (Q0 / (2*pi*Delta)) * sin(theta) = kappa * (E - conj E),  kappa = Q0 / (4*pi*i*Delta)
         kappa = self.q0 / (4.0 * math.pi * self.delta_in) / 1j
-        m_lo = self.eval_mod(lo, self.coef_lo, kappa)
-        m_hi = self.eval_mod(hi, self.coef_hi, kappa * 1j)
+        from .engine import get_engine
+
+        m_lo, m_hi = get_engine().fork([lambda: self.eval_mod(lo, self.coef_lo, kappa),
+                                        lambda: self.eval_mod(hi, self.coef_hi, kappa * 1j)])
         w = ckks.add(m_lo, m_hi)                       # m_lo + i*m_hi (bit-reversed slots)
         w = ckks.mod_drop(w, self.lvl_stc)
         out = self.slot_to_coeff(w)

@@ -309,13 +309,37 @@ def mul_plain(ct: Ciphertext, pt: Plaintext) -> Ciphertext:
                       scale=ct.scale * pt.scale)
 
 
+def ct_tensor(ct: Ciphertext):
+    """[2, l, n] device tensor of a ciphertext (a view when a and b are adjacent halves
+    of one allocation, as every kernel-produced ciphertext is; a copy otherwise)."""
+    import torch
+
+    a, b = ct.a.data, ct.b.data
+    base = getattr(a, "_base", None)
+    if base is not None and base is getattr(b, "_base", None) and base.dim() == 3 and base.shape[0] == 2 \
+            and base.data_ptr() == a.data_ptr() and a.data_ptr() + a.numel() * 4 == b.data_ptr():
+        return base
+    return torch.stack([a, b])
+
+
+def ct_from_tensor(t, basis, scale) -> Ciphertext:
+    return Ciphertext(a=Polynomial(basis, t[0], EVALUATION), b=Polynomial(basis, t[1], EVALUATION), scale=scale)
+
+
 def tensor(x: Ciphertext, y: Ciphertext):
-    """(d0, d1, d2) with d0 + d1*s + d2*s^2 = (b1 + a1 s)(b2 + a2 s)."""
+    """(d0, d1, d2) with d0 + d1*s + d2*s^2 = (b1 + a1 s)(b2 + a2 s): d0 = b1*b2,
+    d1 = a1*b2 + a2*b1, d2 = a1*a2 (each a poly_elementwise product), one fused kernel."""
     _same_level(x.a, y.a)
-    d0 = poly_elementwise(x.b, y.b, "mul")
-    d1 = poly_elementwise(poly_elementwise(x.a, y.b, "mul"), poly_elementwise(y.a, x.b, "mul"), "add")
-    d2 = poly_elementwise(x.a, y.a, "mul")
-    return d0, d1, d2
+    from .engine import get_engine
+
+    eng = get_engine()
+    basis = x.a.basis
+    if x.a.n % 4:
+        d0 = poly_elementwise(x.b, y.b, "mul")
+        d1 = poly_elementwise(poly_elementwise(x.a, y.b, "mul"), poly_elementwise(y.a, x.b, "mul"), "add")
+        return d0, d1, poly_elementwise(x.a, y.a, "mul")
+    d = eng.tensor(ct_tensor(x), ct_tensor(y), eng.row_slots(basis))
+    return tuple(Polynomial(basis, d[i], EVALUATION) for i in range(3))
 
 
 def keyswitch_level(ct: Ciphertext, evk: ks.SwitchingKey) -> Ciphertext:

@@ -156,7 +156,11 @@ struct ckks_ctx {
     // grows at plan creation, never in the hot path.  Graphs captured before a later,
     // larger plan is created must be re-captured.
     uint32_t* ws = nullptr;
-    size_t ws_words = 0;
+    size_t ws_words = 0;          // words per lane
+    // Lanes: independent copies of the arena so that key switches issued on different
+    // streams (independent rotations, the two EvalMod branches) can overlap.
+    int lanes = 1;
+    int lane = 0;
 };
 
 static int check_ctx(ckks_ctx* ctx) {
@@ -206,6 +210,26 @@ int ckks_profile_read(char* buf, size_t cap) {
         if (w < 0 || (size_t)w >= cap - at) break;
         at += (size_t)w;
     }
+    return CKKS_OK;
+}
+
+int ckks_set_lanes(ckks_ctx* ctx, int lanes) {
+    CKS(check_ctx(ctx));
+    if (lanes < 1 || lanes > 16) { set_last_error("lane count %d out of range [1, 16]", lanes); return CKKS_ERR_ARG; }
+    if (lanes != ctx->lanes) {
+        CK(cudaDeviceSynchronize());
+        if (ctx->ws) CK(cudaFree(ctx->ws));
+        ctx->ws = nullptr;
+        ctx->lanes = lanes;
+        ctx->lane = 0;
+        if (ctx->ws_words) CK(cudaMalloc((void**)&ctx->ws, sizeof(uint32_t) * ctx->ws_words * lanes));
+    }
+    return CKKS_OK;
+}
+
+int ckks_select_lane(ckks_ctx* ctx, int lane) {
+    if (!ctx || lane < 0 || lane >= ctx->lanes) { set_last_error("lane %d out of range", lane); return CKKS_ERR_ARG; }
+    ctx->lane = lane;
     return CKKS_OK;
 }
 
@@ -424,6 +448,22 @@ int ckks_pmult_accumulate(ckks_ctx* ctx, const uint32_t* x, const uint32_t* p, u
     return pmult_acc_launch(x, p, acc, row_slot, ctx->d_slots, rows, cols, first, (cudaStream_t)stream);
 }
 
+int ckks_fused_terms(ckks_ctx* ctx, int count, const uint32_t* const* x, const uint32_t* const* p,
+                     uint32_t* out, const int32_t* row_slot, int rows, size_t cols, void* stream) {
+    CKS(check_ctx(ctx));
+    if (count < 1 || count > kMaxTerms || !x || !p) { set_last_error("term count %d out of range [1, %d]", count, kMaxTerms); return CKKS_ERR_ARG; }
+    FusedTerms t{};
+    t.count = count;
+    for (int i = 0; i < count; ++i) { t.x[i] = x[i]; t.p[i] = p[i]; }
+    return fused_terms_launch(t, out, row_slot, ctx->d_slots, rows, cols, (cudaStream_t)stream);
+}
+
+int ckks_tensor(ckks_ctx* ctx, const uint32_t* x, const uint32_t* y, uint32_t* out,
+                const int32_t* row_slot, int rows, size_t cols, void* stream) {
+    CKS(check_ctx(ctx));
+    return tensor_launch(x, y, out, row_slot, ctx->d_slots, rows, cols, (cudaStream_t)stream);
+}
+
 // ---- base conversion ------------------------------------------------------------------
 
 int ckks_bconv_table_create(ckks_ctx* ctx, const int32_t* in_slot, int l_in, const int32_t* out_slot,
@@ -585,7 +625,7 @@ static int plan_create(ckks_ctx* ctx, uint32_t n, int l, int alpha, const int32_
             if (ctx->ws) CK(cudaFree(ctx->ws));
             ctx->ws = nullptr;
             ctx->ws_words = 0;
-            CK(cudaMalloc((void**)&ctx->ws, sizeof(uint32_t) * at));
+            CK(cudaMalloc((void**)&ctx->ws, sizeof(uint32_t) * at * ctx->lanes));
             ctx->ws_words = at;
         }
     }
@@ -598,11 +638,12 @@ static int get_plan(ckks_ctx* ctx, int32_t id, KsPlan** out) {
     CKS(check_ctx(ctx));
     if (id < 0 || id >= (int32_t)ctx->plans.size()) { set_last_error("key-switch plan %d out of range", id); return CKKS_ERR_ARG; }
     KsPlan* pl = ctx->plans[id].get();
-    pl->ws_coeff = ctx->ws + pl->off_coeff;
-    pl->ws_raised = ctx->ws + pl->off_raised;
-    pl->ws_acc = ctx->ws + pl->off_acc;
-    pl->ws_conv = ctx->ws + pl->off_conv;
-    pl->ws_pc = ctx->ws + pl->off_pc;
+    uint32_t* base = ctx->ws + (size_t)ctx->lane * ctx->ws_words;
+    pl->ws_coeff = base + pl->off_coeff;
+    pl->ws_raised = base + pl->off_raised;
+    pl->ws_acc = base + pl->off_acc;
+    pl->ws_conv = base + pl->off_conv;
+    pl->ws_pc = base + pl->off_pc;
     *out = pl;
     return CKKS_OK;
 }

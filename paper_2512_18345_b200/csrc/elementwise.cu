@@ -217,4 +217,104 @@ int pmult_acc_launch(const uint32_t* x, const uint32_t* p, uint32_t* acc, const 
     return CKKS_OK;
 }
 
+// Fused inner sum of a BSGS linear transform: out = sum_t x_t (.) p_t over up to
+// kMaxTerms (rotated ciphertext, plaintext diagonal) pairs in one pass -- every operand
+// is read once and the accumulator never leaves registers (products are summed in 64
+// bits, four at a time, then reduced).  With p_t == null the term is x_t itself (plain
+// sum of ciphertexts, the giant-step accumulation).
+__global__ void __launch_bounds__(256)
+fused_terms_kernel(FusedTerms terms, uint4* out, const int32_t* __restrict__ row_slot,
+                   const ModSlot* __restrict__ slots, int rows, size_t cols4) {
+    const size_t row = blockIdx.y;
+    const ModSlot m = slots[row_slot[row]];
+    const size_t half = (size_t)rows * cols4;
+    const size_t stride = (size_t)gridDim.x * blockDim.x;
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < cols4; i += stride) {
+        const size_t at = row * cols4 + i;
+        uint64_t sa[4] = {0, 0, 0, 0}, sb[4] = {0, 0, 0, 0};
+        uint32_t ra[4] = {0, 0, 0, 0}, rb[4] = {0, 0, 0, 0};
+        int pending = 0;
+        for (int t = 0; t < terms.count; ++t) {
+            const uint4* x = reinterpret_cast<const uint4*>(terms.x[t]);
+            const uint4 xa = x[at], xb = x[half + at];
+            if (terms.p[t]) {
+                const uint4 pv = reinterpret_cast<const uint4*>(terms.p[t])[at];
+                sa[0] += (uint64_t)xa.x * pv.x; sa[1] += (uint64_t)xa.y * pv.y;
+                sa[2] += (uint64_t)xa.z * pv.z; sa[3] += (uint64_t)xa.w * pv.w;
+                sb[0] += (uint64_t)xb.x * pv.x; sb[1] += (uint64_t)xb.y * pv.y;
+                sb[2] += (uint64_t)xb.z * pv.z; sb[3] += (uint64_t)xb.w * pv.w;
+            } else {
+                sa[0] += xa.x; sa[1] += xa.y; sa[2] += xa.z; sa[3] += xa.w;
+                sb[0] += xb.x; sb[1] += xb.y; sb[2] += xb.z; sb[3] += xb.w;
+            }
+            if (++pending == 4 || t == terms.count - 1) {
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    ra[k] = add_mod(ra[k], reduce64(sa[k], m), m.q);
+                    rb[k] = add_mod(rb[k], reduce64(sb[k], m), m.q);
+                    sa[k] = sb[k] = 0;
+                }
+                pending = 0;
+            }
+        }
+        out[at] = make_uint4(ra[0], ra[1], ra[2], ra[3]);
+        out[half + at] = make_uint4(rb[0], rb[1], rb[2], rb[3]);
+    }
+}
+
+int fused_terms_launch(const FusedTerms& terms, uint32_t* out, const int32_t* row_slot,
+                       const ModSlot* slots, int rows, size_t cols, cudaStream_t st) {
+    if (rows <= 0 || cols == 0 || terms.count <= 0) return CKKS_OK;
+    if (cols % 4 || rows > 65535 || terms.count > kMaxTerms) {
+        set_last_error("fused_terms needs cols %% 4 == 0, <= 65535 rows, <= %d terms", kMaxTerms);
+        return CKKS_ERR_UNSUPPORTED;
+    }
+    ProfScope ps("fused_terms", st, 4.0 * cols * rows * (3.0 * terms.count + 2.0));
+    unsigned gx = (unsigned)((cols / 4 + 255) / 256);
+    fused_terms_kernel<<<dim3(gx, rows), 256, 0, st>>>(terms, (uint4*)out, row_slot, slots, rows, cols / 4);
+    CK(cudaGetLastError());
+    return CKKS_OK;
+}
+
+// Tensor product of two ciphertexts in one pass (the front of HMult):
+// d0 = b1*b2, d1 = a1*b2 + a2*b1, d2 = a1*a2; x, y are [2][rows][n] (a then b),
+// out is [3][rows][n] (d0, d1, d2).
+__global__ void __launch_bounds__(256)
+tensor_kernel(const uint4* __restrict__ x, const uint4* __restrict__ y, uint4* out,
+              const int32_t* __restrict__ row_slot, const ModSlot* __restrict__ slots, int rows,
+              size_t cols4) {
+    const size_t row = blockIdx.y;
+    const ModSlot m = slots[row_slot[row]];
+    const size_t half = (size_t)rows * cols4;
+    const size_t stride = (size_t)gridDim.x * blockDim.x;
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < cols4; i += stride) {
+        const size_t at = row * cols4 + i;
+        const uint4 a1 = x[at], b1 = x[half + at], a2 = y[at], b2 = y[half + at];
+        const uint32_t A1[4] = {a1.x, a1.y, a1.z, a1.w}, B1[4] = {b1.x, b1.y, b1.z, b1.w};
+        const uint32_t A2[4] = {a2.x, a2.y, a2.z, a2.w}, B2[4] = {b2.x, b2.y, b2.z, b2.w};
+        uint32_t d0[4], d1[4], d2[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            d0[k] = mul_mod(B1[k], B2[k], m);
+            d2[k] = mul_mod(A1[k], A2[k], m);
+            d1[k] = reduce64((uint64_t)A1[k] * B2[k] + (uint64_t)A2[k] * B1[k], m);
+        }
+        out[at] = make_uint4(d0[0], d0[1], d0[2], d0[3]);
+        out[half + at] = make_uint4(d1[0], d1[1], d1[2], d1[3]);
+        out[2 * half + at] = make_uint4(d2[0], d2[1], d2[2], d2[3]);
+    }
+}
+
+int tensor_launch(const uint32_t* x, const uint32_t* y, uint32_t* out, const int32_t* row_slot,
+                  const ModSlot* slots, int rows, size_t cols, cudaStream_t st) {
+    if (rows <= 0 || cols == 0) return CKKS_OK;
+    if (cols % 4 || rows > 65535) { set_last_error("tensor needs cols %% 4 == 0 and <= 65535 rows"); return CKKS_ERR_UNSUPPORTED; }
+    ProfScope ps("tensor", st, 4.0 * cols * rows * 7.0);
+    unsigned gx = (unsigned)((cols / 4 + 255) / 256);
+    tensor_kernel<<<dim3(gx, rows), 256, 0, st>>>((const uint4*)x, (const uint4*)y, (uint4*)out, row_slot,
+                                                  slots, rows, cols / 4);
+    CK(cudaGetLastError());
+    return CKKS_OK;
+}
+
 }  // namespace ckks

@@ -70,6 +70,17 @@ int lift2_centered_launch(const uint32_t* in, uint32_t* out, const int32_t* row_
 int pmult_acc_launch(const uint32_t* x, const uint32_t* p, uint32_t* acc, const int32_t* row_slot,
                      const ModSlot* slots, int rows, size_t cols, int first, cudaStream_t st);
 
+constexpr int kMaxTerms = 16;
+struct FusedTerms {
+    int count;
+    const uint32_t* x[kMaxTerms];   // ciphertexts [2][rows][n]
+    const uint32_t* p[kMaxTerms];   // plaintexts [rows][n] or null
+};
+int fused_terms_launch(const FusedTerms& terms, uint32_t* out, const int32_t* row_slot,
+                       const ModSlot* slots, int rows, size_t cols, cudaStream_t st);
+int tensor_launch(const uint32_t* x, const uint32_t* y, uint32_t* out, const int32_t* row_slot,
+                  const ModSlot* slots, int rows, size_t cols, cudaStream_t st);
+
 // bconv.cu
 // Device image of one conversion table (reference baseconv.py:37-54).
 struct BconvDev {

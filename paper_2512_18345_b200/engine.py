@@ -45,6 +45,44 @@ class Engine:
     def empty(self, *shape):
         return self.torch.empty(shape, dtype=self.torch.int32, device=self.device)
 
+    # ---- lanes: concurrent key switches on side streams ---------------------
+    def set_lanes(self, count: int) -> None:
+        """Replicate the key-switch workspace `count` times and create one side
+        stream per extra lane (lane 0 runs on the caller's stream)."""
+        _lib.check(self.lib.ckks_set_lanes(self.ctx, count))
+        self.lanes = count
+        self.lane_streams = [None] + [self.torch.cuda.Stream(device=self.device) for _ in range(count - 1)]
+
+    def fork(self, jobs):
+        """Run the callables in `jobs` round-robin over the lanes (each on its lane's
+        stream and workspace), joined back into the current stream.  Results in order."""
+        torch = self.torch
+        lanes = getattr(self, "lanes", 1)
+        if lanes == 1 or len(jobs) < 2:
+            return [job() for job in jobs]
+        main = torch.cuda.current_stream(self.device)
+        start = torch.cuda.Event()
+        start.record(main)
+        used = set()
+        out = []
+        for i, job in enumerate(jobs):
+            lane = i % lanes
+            if lane == 0:
+                _lib.check(self.lib.ckks_select_lane(self.ctx, 0))
+                out.append(job())
+                continue
+            side = self.lane_streams[lane]
+            if lane not in used:
+                side.wait_event(start)
+                used.add(lane)
+            _lib.check(self.lib.ckks_select_lane(self.ctx, lane))
+            with torch.cuda.stream(side):
+                out.append(job())
+        _lib.check(self.lib.ckks_select_lane(self.ctx, 0))
+        for lane in used:
+            main.wait_stream(self.lane_streams[lane])
+        return out
+
     # ---- modulus slots ----------------------------------------------------
     def slot(self, m, n: int) -> int:
         """Context slot of Modulus ``m`` with transform tables for degree n
@@ -131,6 +169,23 @@ class Engine:
                                                   acc.data_ptr(), row_slot.data_ptr(), x.shape[1],
                                                   x.shape[2], int(first), self.stream()))
         return acc
+
+    def fused_terms(self, xs, ps, row_slot, out=None):
+        """out = sum_t xs[t] * ps[t] (ps[t] None: plain term); xs are [2, rows, n] tensors."""
+        count = len(xs)
+        out = self.torch.empty_like(xs[0]) if out is None else out
+        xp = (ctypes.c_void_p * count)(*[x.data_ptr() for x in xs])
+        pp = (ctypes.c_void_p * count)(*[None if p is None else p.data_ptr() for p in ps])
+        _lib.check(self.lib.ckks_fused_terms(self.ctx, count, xp, pp, out.data_ptr(), row_slot.data_ptr(),
+                                             xs[0].shape[1], xs[0].shape[2], self.stream()))
+        return out
+
+    def tensor(self, x, y, row_slot):
+        """(d0, d1, d2) of two [2, rows, n] ciphertext tensors as one [3, rows, n] tensor."""
+        out = self.empty(3, x.shape[1], x.shape[2])
+        _lib.check(self.lib.ckks_tensor(self.ctx, x.data_ptr(), y.data_ptr(), out.data_ptr(),
+                                        row_slot.data_ptr(), x.shape[1], x.shape[2], self.stream()))
+        return out
 
     def bconv_table(self, q_basis, p_basis) -> int:
         key = (tuple(m.q for m in q_basis), tuple(m.q for m in p_basis))

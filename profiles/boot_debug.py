@@ -16,6 +16,10 @@ N = 1 << logn
 p = generate_parameter_set(n=N, l=36, dnum=3, delta=1 << 40, h_dense=32, h_sparse=32) if logn < 16 \
     else ParameterSet.builtin("ks48")
 sk = ks.keygen(p, h=32, seed=1)
+lanes = int(sys.argv[2]) if len(sys.argv) > 2 else 1
+from paper_2512_18345_b200.engine import get_engine
+get_engine().set_lanes(lanes)
+print('lanes', lanes)
 t0 = time.time()
 boot = Bootstrapper(p, sk, BootstrapConfig())
 print(f"setup {time.time() - t0:.1f}s  levels: cts {boot.lvl_cts} evalmod {boot.lvl_evalmod} stc {boot.lvl_stc} out {boot.out_level}",
