@@ -188,6 +188,18 @@ int ckks_ks_stage3(ckks_ctx* ctx, int32_t plan, const uint32_t* q_a, const uint3
 int ckks_keyswitch(ckks_ctx* ctx, int32_t plan, const uint32_t* ct_a, const uint32_t* ct_b,
                    const uint32_t* evk, uint32_t* out_a, uint32_t* out_b, void* stream);
 
+/* Hoisted rotation: with `raised` = ckks_ks_stage1(ct_a) computed once, returns the key
+ * switch of the rotated ciphertext (sigma_k(ct_a), sigma_k(ct_b)) for the Galois key
+ * `evk` of X -> X^k: the raised digits and ct_b are read through the automorphism
+ * inside the inner-product and ModDown kernels, so each further rotation of the same
+ * ciphertext skips the whole of stage 1.  sigma_k commutes with ModUp only up to a
+ * multiple of the digit modulus, so the limbs differ from
+ * ckks_keyswitch(automorphism(ct)) by key-switch noise, not bit for bit (the reference
+ * has no hoisting, PAPER.md:616 notes Cheddar does). */
+int ckks_ks_hoisted(ckks_ctx* ctx, int32_t plan, const uint32_t* raised, uint32_t k,
+                    const uint32_t* evk, const uint32_t* ct_b, uint32_t* out_a, uint32_t* out_b,
+                    void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -170,8 +170,8 @@ class LinearTransform:
         basis = ct.a.basis
         slots = eng.row_slots(basis)
         # baby steps: independent rotations of the same input, spread over the lanes
-        rot = eng.fork([(lambda b=b: ct_tensor(ckks.hrot(ct, b * self.step, keys))) for b in self.baby])
-        rotated = dict(zip(self.baby, rot))
+        hoisted = ckks.hrot_hoisted(ct, [b * self.step for b in self.baby], keys)
+        rotated = {b: hoisted[b * self.step] for b in self.baby}
 
         def giant(g):
             row = self.table[g]

@@ -408,6 +408,38 @@ def hrot(ct: Ciphertext, r: int, keys: EvaluationKeys) -> Ciphertext:
     return apply_galois(ct, k, keys.galois[k])
 
 
+def hrot_hoisted(ct: Ciphertext, rotations, keys: EvaluationKeys) -> dict:
+    """Several rotations of one ciphertext sharing a single ModUp (hoisting): returns
+    {r: [2, l, n] ciphertext tensor}.  Independent rotations run on the engine's lanes."""
+    from .engine import get_engine
+
+    eng = get_engine()
+    params = keys.params
+    level = level_of(ct)
+    n = ct.a.n
+    basis = ct.a.basis
+    out = {}
+    todo = []
+    for r in rotations:
+        if r % (n // 2) == 0:
+            out[r] = ct_tensor(ct)
+        else:
+            k = galois_element(r, n)
+            if k not in keys.galois:
+                raise RnsError(f"no Galois key for rotation {r}")
+            todo.append((r, k))
+    if todo:
+        plan = eng.ks_plan(n, basis, params.p_basis, params.alpha, params.l + params.alpha, params.l)
+        beta = -(-level // params.alpha)
+        raised = eng.ks_stage1(plan, ct.a.data, beta, level + params.alpha)
+        b = ct.b.data
+        res = eng.fork([(lambda k=k: eng.ks_hoisted(plan, raised, k, keys.galois[k].matrix(), b))
+                        for _, k in todo])
+        for (r, _), t in zip(todo, res):
+            out[r] = t
+    return out
+
+
 def conjugate(ct: Ciphertext, keys: EvaluationKeys) -> Ciphertext:
     k = conjugation_element(ct.a.n)
     if k not in keys.galois:

@@ -690,9 +690,15 @@ static int stage1_core(ckks_ctx* ctx, KsPlan* pl, const uint32_t* a, uint32_t* r
     return CKKS_OK;
 }
 
+static uint32_t log2u(uint32_t n) {
+    uint32_t lg = 0;
+    while ((1u << lg) < n) ++lg;
+    return lg;
+}
+
 static int stage3_core(ckks_ctx* ctx, KsPlan* pl, const uint32_t* q_a, const uint32_t* q_b,
                        const uint32_t* p_a, const uint32_t* p_b, const uint32_t* fold_b,
-                       uint32_t* out_a, uint32_t* out_b, cudaStream_t st) {
+                       uint32_t* out_a, uint32_t* out_b, cudaStream_t st, uint32_t galois = 0) {
     const size_t n = pl->n;
     const RowMap id{nullptr, nullptr};
     if (p_a == pl->ws_acc + (size_t)pl->l * n && p_b == p_a + (size_t)pl->ext * n) {
@@ -722,6 +728,7 @@ static int stage3_core(ckks_ctx* ctx, KsPlan* pl, const uint32_t* q_a, const uin
     e.out_a = out_a; e.out_b = out_b;
     e.q_slot = pl->d_q_slot; e.pinv = pl->d_pinv; e.pinv_s = pl->d_pinv_s;
     e.l = pl->l; e.n = pl->n;
+    e.galois = galois; e.lg = log2u(pl->n);
     return moddown_epilogue_launch(e, ctx->d_slots, st);
 }
 
@@ -733,6 +740,7 @@ static InnerProductArgs ip_args(KsPlan* pl, const uint32_t* carry, const uint32_
     a.ext_slot = pl->d_ext_slot; a.evk_row = pl->d_evk_row;
     a.l = pl->l; a.alpha = pl->alpha; a.beta = pl->beta; a.ext = pl->ext; a.evk_ext = pl->evk_ext;
     a.row_lo = row_lo; a.row_hi = row_hi; a.n = pl->n;
+    a.galois = 0; a.lg = log2u(pl->n);
     return a;
 }
 
@@ -785,6 +793,24 @@ int ckks_keyswitch(ckks_ctx* ctx, int32_t plan, const uint32_t* ct_a, const uint
                              ctx->d_slots, st));
     return stage3_core(ctx, pl, acc_a, acc_b, acc_a + (size_t)pl->l * n, acc_b + (size_t)pl->l * n,
                        ct_b, out_a, out_b, st);
+}
+
+int ckks_ks_hoisted(ckks_ctx* ctx, int32_t plan, const uint32_t* raised, uint32_t k,
+                    const uint32_t* evk, const uint32_t* ct_b, uint32_t* out_a, uint32_t* out_b,
+                    void* stream) {
+    KsPlan* pl;
+    CKS(get_plan(ctx, plan, &pl));
+    CKS(need_full_plan(pl));
+    if (!(k & 1)) { set_last_error("automorphism index must be odd"); return CKKS_ERR_ARG; }
+    cudaStream_t st = (cudaStream_t)stream;
+    const size_t n = pl->n;
+    uint32_t* acc_a = pl->ws_acc;
+    uint32_t* acc_b = pl->ws_acc + (size_t)pl->ext * n;
+    InnerProductArgs ip = ip_args(pl, nullptr, raised, evk, 0, pl->ext, acc_a, acc_b);
+    ip.galois = k & (2 * pl->n - 1);
+    CKS(inner_product_launch(ip, ctx->d_slots, st));
+    return stage3_core(ctx, pl, acc_a, acc_b, acc_a + (size_t)pl->l * n, acc_b + (size_t)pl->l * n,
+                       ct_b, out_a, out_b, st, ip.galois);
 }
 
 }  // extern "C"

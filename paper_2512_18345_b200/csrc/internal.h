@@ -125,6 +125,7 @@ struct InnerProductArgs {
     int l, alpha, beta, ext, evk_ext;
     int row_lo, row_hi;
     uint32_t n;
+    uint32_t galois, lg;        // galois != 0: read digit columns through X -> X^galois (hoisting)
 };
 int inner_product_launch(const InnerProductArgs& a, const ModSlot* slots, cudaStream_t st);
 
@@ -140,6 +141,7 @@ struct ModDownEpilogueArgs {
     const uint32_t* pinv_s;     // [l]  Shoup companions
     int l;
     uint32_t n;
+    uint32_t galois, lg;        // galois != 0: fold_b is read through X -> X^galois
 };
 int moddown_epilogue_launch(const ModDownEpilogueArgs& a, const ModSlot* slots, cudaStream_t st);
 

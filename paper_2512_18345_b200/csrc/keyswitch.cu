@@ -17,6 +17,14 @@ __device__ __forceinline__ uint64_t mad64(uint32_t a, uint32_t b, uint64_t c) {
     return (uint64_t)a * b + c;
 }
 
+// Source column of output column t under the evaluation-domain automorphism X -> X^k
+// (same closed form as automorphism_eval_kernel).
+__device__ __forceinline__ uint32_t galois_src(uint32_t t, uint32_t k, uint32_t n, uint32_t lg) {
+    const uint32_t u = __brev(t) >> (32 - lg);
+    const uint32_t e = ((2 * u + 1) * k) & (2 * n - 1);
+    return __brev((e - 1) >> 1) >> (32 - lg);
+}
+
 template <bool VEC>
 __global__ void __launch_bounds__(256)
 inner_product_kernel(InnerProductArgs p, const ModSlot* __restrict__ slots) {
@@ -39,7 +47,16 @@ inner_product_kernel(InnerProductArgs p, const ModSlot* __restrict__ slots) {
         const uint32_t* ka = p.evk + (((size_t)t * 2 + 0) * p.evk_ext + erow) * n;
         const uint32_t* kb = p.evk + (((size_t)t * 2 + 1) * p.evk_ext + erow) * n;
         uint32_t d[W], xa[W], xb[W];
-        if (VEC) {
+        if (VEC && p.galois) {
+            // hoisted rotation: the raised digit is read through the automorphism
+            // (sigma_k commutes with ModUp up to a multiple of the digit modulus)
+#pragma unroll
+            for (int w = 0; w < W; ++w) d[w] = dsrc[galois_src((uint32_t)i + w, p.galois, p.n, p.lg)];
+            const uint4 av = ld_stream(reinterpret_cast<const uint4*>(ka + i));
+            const uint4 bv = ld_stream(reinterpret_cast<const uint4*>(kb + i));
+            xa[0] = av.x; xa[W > 1 ? 1 : 0] = av.y; xa[W > 2 ? 2 : 0] = av.z; xa[W > 3 ? 3 : 0] = av.w;
+            xb[0] = bv.x; xb[W > 1 ? 1 : 0] = bv.y; xb[W > 2 ? 2 : 0] = bv.z; xb[W > 3 ? 3 : 0] = bv.w;
+        } else if (VEC) {
             const uint4 dv = *reinterpret_cast<const uint4*>(dsrc + i);
             const uint4 av = ld_stream(reinterpret_cast<const uint4*>(ka + i));
             const uint4 bv = ld_stream(reinterpret_cast<const uint4*>(kb + i));
@@ -47,7 +64,8 @@ inner_product_kernel(InnerProductArgs p, const ModSlot* __restrict__ slots) {
             xa[0] = av.x; xa[W > 1 ? 1 : 0] = av.y; xa[W > 2 ? 2 : 0] = av.z; xa[W > 3 ? 3 : 0] = av.w;
             xb[0] = bv.x; xb[W > 1 ? 1 : 0] = bv.y; xb[W > 2 ? 2 : 0] = bv.z; xb[W > 3 ? 3 : 0] = bv.w;
         } else {
-            d[0] = dsrc[i]; xa[0] = ka[i]; xb[0] = kb[i];
+            d[0] = p.galois ? dsrc[galois_src((uint32_t)i, p.galois, p.n, p.lg)] : dsrc[i];
+            xa[0] = ka[i]; xb[0] = kb[i];
         }
 #pragma unroll
         for (int w = 0; w < W; ++w) {
@@ -103,7 +121,7 @@ moddown_epilogue_kernel(ModDownEpilogueArgs p, const ModSlot* __restrict__ slots
     if (i >= n) return;
     const uint32_t* x = (half ? p.xq_b : p.xq_a) + (size_t)row * n + i;
     const uint32_t* c = p.conv + ((size_t)half * p.l + row) * n + i;
-    const uint32_t* f = (half && p.fold_b) ? p.fold_b + (size_t)row * n + i : nullptr;
+    const uint32_t* f = (half && p.fold_b) ? p.fold_b + (size_t)row * n + (p.galois ? 0 : i) : nullptr;
     uint32_t* o = (half ? p.out_b : p.out_a) + (size_t)row * n + i;
     if (VEC) {
         const uint4 xv = *reinterpret_cast<const uint4*>(x);
@@ -113,7 +131,12 @@ moddown_epilogue_kernel(ModDownEpilogueArgs p, const ModSlot* __restrict__ slots
         r.y = shoup_mul(xv.y - cv.y + q, pinv, pinv_s, q);
         r.z = shoup_mul(xv.z - cv.z + q, pinv, pinv_s, q);
         r.w = shoup_mul(xv.w - cv.w + q, pinv, pinv_s, q);
-        if (f) {
+        if (f && p.galois) {
+            r.x = add_mod(r.x, f[galois_src((uint32_t)i, p.galois, p.n, p.lg)], q);
+            r.y = add_mod(r.y, f[galois_src((uint32_t)i + 1, p.galois, p.n, p.lg)], q);
+            r.z = add_mod(r.z, f[galois_src((uint32_t)i + 2, p.galois, p.n, p.lg)], q);
+            r.w = add_mod(r.w, f[galois_src((uint32_t)i + 3, p.galois, p.n, p.lg)], q);
+        } else if (f) {
             const uint4 fv = *reinterpret_cast<const uint4*>(f);
             r.x = add_mod(r.x, fv.x, q); r.y = add_mod(r.y, fv.y, q);
             r.z = add_mod(r.z, fv.z, q); r.w = add_mod(r.w, fv.w, q);
@@ -121,7 +144,7 @@ moddown_epilogue_kernel(ModDownEpilogueArgs p, const ModSlot* __restrict__ slots
         *reinterpret_cast<uint4*>(o) = r;
     } else {
         uint32_t r = shoup_mul(x[0] - c[0] + q, pinv, pinv_s, q);
-        if (f) r = add_mod(r, f[0], q);
+        if (f) r = add_mod(r, p.galois ? f[galois_src((uint32_t)i, p.galois, p.n, p.lg)] : f[0], q);
         o[0] = r;
     }
 }

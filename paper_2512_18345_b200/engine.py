@@ -259,6 +259,14 @@ class Engine:
                                            out[1].data_ptr(), self.stream()))
         return out
 
+    def ks_hoisted(self, plan: int, raised, k: int, evk, ct_b):
+        """Key switch of the ciphertext rotated by X -> X^k from pre-raised digits."""
+        out = self.empty(2, ct_b.shape[0], ct_b.shape[1])
+        _lib.check(self.lib.ckks_ks_hoisted(self.ctx, plan, raised.data_ptr(), k, evk.data_ptr(),
+                                            ct_b.data_ptr(), out[0].data_ptr(), out[1].data_ptr(),
+                                            self.stream()))
+        return out
+
     def keyswitch(self, plan: int, ct_a, ct_b, evk, out=None):
         out = self.empty(2, ct_a.shape[0], ct_a.shape[1]) if out is None else out
         _lib.check(self.lib.ckks_keyswitch(self.ctx, plan, ct_a.data_ptr(),

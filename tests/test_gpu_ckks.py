@@ -131,6 +131,11 @@ def test_slotwise_semantics_rotation_conjugation_mult(env):
     assert np.abs(got - np.roll(z1, -5)).max() < tol
     sq = ck.rescale(ck.hmult(low, ck.mod_drop(ct2, 7), keys.relin), 2)
     assert np.abs(ck.decrypt_decode(sq, sk, p) - z1 * z2).max() < tol
+    # hoisted rotations (one ModUp shared) decode to the same slots as plain HRot
+    hoisted = ck.hrot_hoisted(low, [0, 1, 5], keys)
+    for r in (0, 1, 5):
+        got = ck.decrypt_decode(ck.ct_from_tensor(hoisted[r], low.a.basis, low.scale), sk, p)
+        assert np.abs(got - np.roll(z1, -r)).max() < tol
     # PMult by an encoded vector and by a constant
     w = rng.uniform(-1, 1, n2)
     pm = ck.rescale(ck.mul_plain(ct1, ck.encode(w, p, scale=scale)), 2)
