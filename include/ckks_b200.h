@@ -200,6 +200,18 @@ int ckks_ks_hoisted(ckks_ctx* ctx, int32_t plan, const uint32_t* raised, uint32_
                     const uint32_t* evk, const uint32_t* ct_b, uint32_t* out_a, uint32_t* out_b,
                     void* stream);
 
+/* Key switches whose results are summed (giant steps of a BSGS linear transform) can
+ * share one ModDown: ckks_ks_accumulate runs stages 1-2 of keyswitch.py:444-453 for
+ * (ct_a, evk) and adds the Q||P accumulator into the current lane's workspace (first !=
+ * 0 overwrites); ckks_ks_finish sums the accumulators of lanes [0, lanes_used), runs
+ * stage 3 once on lane 0 and adds fold_a / fold_b (may be NULL) to the two halves.
+ * ModDown is linear up to its rounding, so this equals the sum of separate key switches
+ * up to key-switch noise. */
+int ckks_ks_accumulate(ckks_ctx* ctx, int32_t plan, const uint32_t* ct_a, const uint32_t* evk,
+                       int first, void* stream);
+int ckks_ks_finish(ckks_ctx* ctx, int32_t plan, int lanes_used, const uint32_t* fold_a,
+                   const uint32_t* fold_b, uint32_t* out_a, uint32_t* out_b, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -173,18 +173,38 @@ class LinearTransform:
         hoisted = ckks.hrot_hoisted(ct, [b * self.step for b in self.baby], keys)
         rotated = {b: hoisted[b * self.step] for b in self.baby}
 
-        def giant(g):
+        def inner_sum(g):
             row = self.table[g]
-            inner = eng.fused_terms([rotated[b] for b in row], [pt.poly.data for pt in row.values()], slots)
-            part = ct_from_tensor(inner, basis, ct.scale * self.pt_scale)
-            return ckks.hrot(part, g * self.n1 * self.step, keys) if g else part
+            return eng.fused_terms([rotated[b] for b in row], [pt.poly.data for pt in row.values()], slots)
 
-        parts = eng.fork([(lambda g=g: giant(g)) for g in self.giants])
-        if len(parts) > 1:
-            summed = eng.fused_terms([ct_tensor(x) for x in parts], [None] * len(parts), slots)
-            total = ct_from_tensor(summed, basis, parts[0].scale)
+        inners = dict(zip(self.giants, eng.fork([(lambda g=g: inner_sum(g)) for g in self.giants])))
+        base = inners.get(0)
+        moving = [g for g in self.giants if g]
+        scale = ct.scale * self.pt_scale
+        if not moving:
+            total = ct_from_tensor(base, basis, scale)
         else:
-            total = parts[0]
+            # giant steps: rotate each inner sum, run stages 1-2 of its key switch into the
+            # lane's Q||P accumulator, and scale everything down with ONE ModDown at the end
+            p = self.params
+            n_ring = p.n
+            plan = eng.ks_plan(n_ring, basis, p.p_basis, p.alpha, p.l + p.alpha, p.l)
+
+            def giant(lane, nth, g):
+                k = ckks.galois_element(g * self.n1 * self.step, n_ring)
+                if k not in keys.galois:
+                    raise RnsError(f"no Galois key for rotation {g * self.n1 * self.step}")
+                rot = eng.automorphism_eval(inners[g].view(2 * self.level, n_ring), k).view(2, self.level, n_ring)
+                eng.ks_accumulate(plan, rot[0], keys.galois[k].matrix(), first=(nth == 0))
+                return rot
+
+            rots = eng.fork([(lambda lane, nth, g=g: giant(lane, nth, g)) for g in moving], with_lane=True)
+            lanes_used = min(getattr(eng, "lanes", 1), len(moving))
+            terms = list(rots) + ([base] if base is not None else [])
+            b_sum = eng.fused_terms(terms, [None] * len(terms), slots) if len(terms) > 1 else terms[0]
+            out_t = eng.ks_finish(plan, lanes_used, None if base is None else base[0], b_sum[1],
+                                  self.level, n_ring)
+            total = ct_from_tensor(out_t, basis, scale)
         out = ckks.rescale(total, self.limbs)
         return ckks.Ciphertext(a=out.a, b=out.b, scale=ct.scale)
 

@@ -372,23 +372,26 @@ def hmult(x: Ciphertext, y: Ciphertext, rlk: ks.SwitchingKey) -> Ciphertext:
 
 
 def rescale(ct: Ciphertext, k: int = 1) -> Ciphertext:
-    """Drop the last k limbs, dividing message and scale by their product."""
+    """Drop the last k limbs, dividing message and scale by their product P: one ModDown
+    pass with P = the dropped limbs, (x_rest - NTT(BConv_{P -> rest}(INTT(x_P)))) * P^-1.
+    For k = 1 this is the single-limb RNS rescale of the reference composition
+    (bit-exact); for k > 1 it divides by the product in one pass instead of
+    k successive single-limb passes (same value up to the rounding of the floor)."""
     from .engine import get_engine
 
+    if k < 1:
+        return ct
     eng = get_engine()
-    for _ in range(k):
-        level = level_of(ct)
-        if level < 2:
-            raise RnsError("no limb left to rescale by")
-        basis = ct.a.basis
-        rest, last = basis[:-1], basis[-1]
-        n = ct.a.n
-        plan = eng.moddown_plan(n, rest, (last,))
-        a, b = ct.a.data, ct.b.data
-        out = eng.ks_stage3(plan, a[:level - 1], b[:level - 1], a[level - 1:], b[level - 1:])
-        ct = Ciphertext(a=Polynomial(rest, out[0], EVALUATION), b=Polynomial(rest, out[1], EVALUATION),
-                        scale=ct.scale / last.q)
-    return ct
+    level = level_of(ct)
+    if level <= k:
+        raise RnsError("no limb left to rescale by")
+    basis = ct.a.basis
+    rest, dropped = basis[:level - k], basis[level - k:]
+    plan = eng.moddown_plan(ct.a.n, rest, dropped)
+    a, b = ct.a.data, ct.b.data
+    out = eng.ks_stage3(plan, a[:level - k], b[:level - k], a[level - k:], b[level - k:])
+    return Ciphertext(a=Polynomial(rest, out[0], EVALUATION), b=Polynomial(rest, out[1], EVALUATION),
+                      scale=ct.scale / math.prod(m.q for m in dropped))
 
 
 def apply_galois(ct: Ciphertext, k: int, evk: ks.SwitchingKey) -> Ciphertext:

@@ -698,7 +698,8 @@ static uint32_t log2u(uint32_t n) {
 
 static int stage3_core(ckks_ctx* ctx, KsPlan* pl, const uint32_t* q_a, const uint32_t* q_b,
                        const uint32_t* p_a, const uint32_t* p_b, const uint32_t* fold_b,
-                       uint32_t* out_a, uint32_t* out_b, cudaStream_t st, uint32_t galois = 0) {
+                       uint32_t* out_a, uint32_t* out_b, cudaStream_t st, uint32_t galois = 0,
+                       const uint32_t* fold_a = nullptr) {
     const size_t n = pl->n;
     const RowMap id{nullptr, nullptr};
     if (p_a == pl->ws_acc + (size_t)pl->l * n && p_b == p_a + (size_t)pl->ext * n) {
@@ -724,7 +725,7 @@ static int stage3_core(ckks_ctx* ctx, KsPlan* pl, const uint32_t* q_a, const uin
     CKS(bconv_launch_jobs(jobs, ctx->d_slots, n, st));
     CKS(ntt_launch(pl->ws_conv, pl->ws_conv, pl->d_s3_q_slot, ctx->d_slots, id, 2 * pl->l, pl->n, 0, st));
     ModDownEpilogueArgs e{};
-    e.xq_a = q_a; e.xq_b = q_b; e.conv = pl->ws_conv; e.fold_b = fold_b;
+    e.xq_a = q_a; e.xq_b = q_b; e.conv = pl->ws_conv; e.fold_a = fold_a; e.fold_b = fold_b;
     e.out_a = out_a; e.out_b = out_b;
     e.q_slot = pl->d_q_slot; e.pinv = pl->d_pinv; e.pinv_s = pl->d_pinv_s;
     e.l = pl->l; e.n = pl->n;
@@ -740,7 +741,7 @@ static InnerProductArgs ip_args(KsPlan* pl, const uint32_t* carry, const uint32_
     a.ext_slot = pl->d_ext_slot; a.evk_row = pl->d_evk_row;
     a.l = pl->l; a.alpha = pl->alpha; a.beta = pl->beta; a.ext = pl->ext; a.evk_ext = pl->evk_ext;
     a.row_lo = row_lo; a.row_hi = row_hi; a.n = pl->n;
-    a.galois = 0; a.lg = log2u(pl->n);
+    a.galois = 0; a.lg = log2u(pl->n); a.accumulate = 0;
     return a;
 }
 
@@ -811,6 +812,44 @@ int ckks_ks_hoisted(ckks_ctx* ctx, int32_t plan, const uint32_t* raised, uint32_
     CKS(inner_product_launch(ip, ctx->d_slots, st));
     return stage3_core(ctx, pl, acc_a, acc_b, acc_a + (size_t)pl->l * n, acc_b + (size_t)pl->l * n,
                        ct_b, out_a, out_b, st, ip.galois);
+}
+
+// ---- giant steps sharing one ModDown ---------------------------------------------------
+// ModDown is linear up to its rounding, so the key switches of several independent
+// ciphertexts that are summed afterwards (the giant steps of a BSGS linear transform)
+// can add their stage-2 accumulators over Q||P and be scaled down once.
+
+int ckks_ks_accumulate(ckks_ctx* ctx, int32_t plan, const uint32_t* ct_a, const uint32_t* evk,
+                       int first, void* stream) {
+    KsPlan* pl;
+    CKS(get_plan(ctx, plan, &pl));
+    CKS(need_full_plan(pl));
+    cudaStream_t st = (cudaStream_t)stream;
+    const size_t n = pl->n;
+    CKS(stage1_core(ctx, pl, ct_a, pl->ws_raised, false, st));
+    InnerProductArgs ip = ip_args(pl, ct_a, pl->ws_raised, evk, 0, pl->ext, pl->ws_acc,
+                                  pl->ws_acc + (size_t)pl->ext * n);
+    ip.accumulate = first ? 0 : 1;
+    return inner_product_launch(ip, ctx->d_slots, st);
+}
+
+int ckks_ks_finish(ckks_ctx* ctx, int32_t plan, int lanes_used, const uint32_t* fold_a,
+                   const uint32_t* fold_b, uint32_t* out_a, uint32_t* out_b, void* stream) {
+    if (!ctx || lanes_used < 1 || lanes_used > ctx->lanes) { set_last_error("bad lane count %d", lanes_used); return CKKS_ERR_ARG; }
+    const int keep = ctx->lane;
+    ctx->lane = 0;
+    KsPlan* pl;
+    int rc = get_plan(ctx, plan, &pl);
+    ctx->lane = keep;
+    CKS(rc);
+    CKS(need_full_plan(pl));
+    cudaStream_t st = (cudaStream_t)stream;
+    const size_t n = pl->n;
+    CKS(lane_reduce_launch(pl->ws_acc, ctx->ws_words, lanes_used, pl->d_ext_slot, ctx->d_slots, pl->ext, n, st));
+    uint32_t* acc_a = pl->ws_acc;
+    uint32_t* acc_b = pl->ws_acc + (size_t)pl->ext * n;
+    return stage3_core(ctx, pl, acc_a, acc_b, acc_a + (size_t)pl->l * n, acc_b + (size_t)pl->l * n,
+                       fold_b, out_a, out_b, st, 0, fold_a);
 }
 
 }  // extern "C"

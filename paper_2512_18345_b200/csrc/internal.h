@@ -126,6 +126,7 @@ struct InnerProductArgs {
     int row_lo, row_hi;
     uint32_t n;
     uint32_t galois, lg;        // galois != 0: read digit columns through X -> X^galois (hoisting)
+    int accumulate;             // add into acc instead of overwriting it
 };
 int inner_product_launch(const InnerProductArgs& a, const ModSlot* slots, cudaStream_t st);
 
@@ -133,6 +134,7 @@ struct ModDownEpilogueArgs {
     const uint32_t* xq_a;       // [l][n] accumulator Q part (a half)
     const uint32_t* xq_b;
     const uint32_t* conv;       // [2][l][n]  NTT(BConv_{P->Q}(INTT(x_P)))
+    const uint32_t* fold_a;     // polynomial to add into the a half (null: none)
     const uint32_t* fold_b;     // ct.b to add into the b half (null: none)
     uint32_t* out_a;
     uint32_t* out_b;
@@ -144,5 +146,7 @@ struct ModDownEpilogueArgs {
     uint32_t galois, lg;        // galois != 0: fold_b is read through X -> X^galois
 };
 int moddown_epilogue_launch(const ModDownEpilogueArgs& a, const ModSlot* slots, cudaStream_t st);
+int lane_reduce_launch(uint32_t* acc0, size_t lane_stride_words, int lanes, const int32_t* ext_slot,
+                       const ModSlot* slots, int ext, size_t n, cudaStream_t st);
 
 }  // namespace ckks

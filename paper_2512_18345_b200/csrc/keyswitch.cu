@@ -86,6 +86,13 @@ inner_product_kernel(InnerProductArgs p, const ModSlot* __restrict__ slots) {
     }
     uint32_t* oa = p.acc_a + (size_t)(row - p.row_lo) * n + i;
     uint32_t* ob = p.acc_b + (size_t)(row - p.row_lo) * n + i;
+    if (p.accumulate) {
+#pragma unroll
+        for (int w = 0; w < W; ++w) {
+            ra[w] = add_mod(ra[w], oa[w], m.q);
+            rb[w] = add_mod(rb[w], ob[w], m.q);
+        }
+    }
     if (VEC) {
         *reinterpret_cast<uint4*>(oa) = make_uint4(ra[0], ra[W > 1 ? 1 : 0], ra[W > 2 ? 2 : 0], ra[W > 3 ? 3 : 0]);
         *reinterpret_cast<uint4*>(ob) = make_uint4(rb[0], rb[W > 1 ? 1 : 0], rb[W > 2 ? 2 : 0], rb[W > 3 ? 3 : 0]);
@@ -121,7 +128,8 @@ moddown_epilogue_kernel(ModDownEpilogueArgs p, const ModSlot* __restrict__ slots
     if (i >= n) return;
     const uint32_t* x = (half ? p.xq_b : p.xq_a) + (size_t)row * n + i;
     const uint32_t* c = p.conv + ((size_t)half * p.l + row) * n + i;
-    const uint32_t* f = (half && p.fold_b) ? p.fold_b + (size_t)row * n + (p.galois ? 0 : i) : nullptr;
+    const uint32_t* fsrc = half ? p.fold_b : p.fold_a;
+    const uint32_t* f = fsrc ? fsrc + (size_t)row * n + (p.galois ? 0 : i) : nullptr;
     uint32_t* o = (half ? p.out_b : p.out_a) + (size_t)row * n + i;
     if (VEC) {
         const uint4 xv = *reinterpret_cast<const uint4*>(x);
@@ -157,6 +165,38 @@ int moddown_epilogue_launch(const ModDownEpilogueArgs& a, const ModSlot* slots, 
     ProfScope ps("moddown_epilogue", st, 4.0 * a.n * a.l * (a.fold_b ? 7.0 : 6.0));
     if (vec) moddown_epilogue_kernel<true><<<grid, 256, 0, st>>>(a, slots);
     else moddown_epilogue_kernel<false><<<grid, 256, 0, st>>>(a, slots);
+    CK(cudaGetLastError());
+    return CKKS_OK;
+}
+
+// acc0 += acc1 + ... over the [2][ext][n] accumulators of several workspace lanes
+// (giant steps of a linear transform accumulate their inner products per lane).
+__global__ void __launch_bounds__(256)
+lane_reduce_kernel(uint4* acc0, size_t lane_stride4, int lanes, const int32_t* __restrict__ ext_slot,
+                   const ModSlot* __restrict__ slots, int ext, size_t cols4) {
+    const int row = blockIdx.y % ext;
+    const uint32_t q = slots[ext_slot[row]].q;
+    const size_t stride = (size_t)gridDim.x * blockDim.x;
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < cols4; i += stride) {
+        const size_t at = (size_t)blockIdx.y * cols4 + i;
+        uint4 r = acc0[at];
+        for (int l = 1; l < lanes; ++l) {
+            const uint4 v = acc0[at + (size_t)l * lane_stride4];
+            r.x = add_mod(r.x, v.x, q); r.y = add_mod(r.y, v.y, q);
+            r.z = add_mod(r.z, v.z, q); r.w = add_mod(r.w, v.w, q);
+        }
+        acc0[at] = r;
+    }
+}
+
+int lane_reduce_launch(uint32_t* acc0, size_t lane_stride_words, int lanes, const int32_t* ext_slot,
+                       const ModSlot* slots, int ext, size_t n, cudaStream_t st) {
+    if (lanes < 2) return CKKS_OK;
+    if (n % 4 || lane_stride_words % 4) { set_last_error("lane reduction needs n %% 4 == 0"); return CKKS_ERR_UNSUPPORTED; }
+    ProfScope ps("lane_reduce", st, 4.0 * n * 2 * ext * (lanes + 1));
+    unsigned gx = (unsigned)((n / 4 + 255) / 256);
+    lane_reduce_kernel<<<dim3(gx, 2 * ext), 256, 0, st>>>((uint4*)acc0, lane_stride_words / 4, lanes, ext_slot,
+                                                          slots, ext, n / 4);
     CK(cudaGetLastError());
     return CKKS_OK;
 }

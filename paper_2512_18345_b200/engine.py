@@ -53,13 +53,13 @@ class Engine:
         self.lanes = count
         self.lane_streams = [None] + [self.torch.cuda.Stream(device=self.device) for _ in range(count - 1)]
 
-    def fork(self, jobs):
+    def fork(self, jobs, with_lane: bool = False):
         """Run the callables in `jobs` round-robin over the lanes (each on its lane's
         stream and workspace), joined back into the current stream.  Results in order."""
         torch = self.torch
         lanes = getattr(self, "lanes", 1)
         if lanes == 1 or len(jobs) < 2:
-            return [job() for job in jobs]
+            return [job(0, i) if with_lane else job() for i, job in enumerate(jobs)]
         main = torch.cuda.current_stream(self.device)
         start = torch.cuda.Event()
         start.record(main)
@@ -69,7 +69,7 @@ class Engine:
             lane = i % lanes
             if lane == 0:
                 _lib.check(self.lib.ckks_select_lane(self.ctx, 0))
-                out.append(job())
+                out.append(job(0, i // lanes) if with_lane else job())
                 continue
             side = self.lane_streams[lane]
             if lane not in used:
@@ -77,7 +77,7 @@ class Engine:
                 used.add(lane)
             _lib.check(self.lib.ckks_select_lane(self.ctx, lane))
             with torch.cuda.stream(side):
-                out.append(job())
+                out.append(job(lane, i // lanes) if with_lane else job())
         _lib.check(self.lib.ckks_select_lane(self.ctx, 0))
         for lane in used:
             main.wait_stream(self.lane_streams[lane])
@@ -265,6 +265,18 @@ class Engine:
         _lib.check(self.lib.ckks_ks_hoisted(self.ctx, plan, raised.data_ptr(), k, evk.data_ptr(),
                                             ct_b.data_ptr(), out[0].data_ptr(), out[1].data_ptr(),
                                             self.stream()))
+        return out
+
+    def ks_accumulate(self, plan: int, ct_a, evk, first: bool):
+        _lib.check(self.lib.ckks_ks_accumulate(self.ctx, plan, ct_a.data_ptr(), evk.data_ptr(),
+                                               int(first), self.stream()))
+
+    def ks_finish(self, plan: int, lanes_used: int, fold_a, fold_b, rows: int, n: int):
+        out = self.empty(2, rows, n)
+        _lib.check(self.lib.ckks_ks_finish(self.ctx, plan, lanes_used,
+                                           None if fold_a is None else fold_a.data_ptr(),
+                                           None if fold_b is None else fold_b.data_ptr(),
+                                           out[0].data_ptr(), out[1].data_ptr(), self.stream()))
         return out
 
     def keyswitch(self, plan: int, ct_a, ct_b, evk, out=None):

@@ -103,3 +103,26 @@ for line in buf.value.decode().splitlines():
 for ms, name, cnt in sorted(rows, reverse=True):
     print(f"   {name:22s} {cnt:6d} launches {ms:8.3f} ms  {100 * ms / tot:5.1f}%")
 print(f"   sum of kernel time {tot:.2f} ms over {sum(r[2] for r in rows)} launches")
+
+# phase timing (eager, with lanes): CUDA events around each stage
+def timed(fn):
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(); r = fn(); b.record(); torch.cuda.synchronize()
+    return r, a.elapsed_time(b)
+for _ in range(2):
+    raised, t_raise = timed(lambda: boot.mod_raise(ct))
+    (lo, hi), t_cts = timed(lambda: boot.coeff_to_slot(raised))
+    (m_lo, m_hi), t_em = timed(lambda: eng.fork([lambda: boot.eval_mod(lo, boot.coef_lo, kappa),
+                                                 lambda: boot.eval_mod(hi, boot.coef_hi, kappa * 1j)]))
+    w = ckks.add(m_lo, m_hi)
+    out, t_stc = timed(lambda: boot.slot_to_coeff(w))
+print(f"phases (eager): mod_raise {t_raise:.2f}  coeff_to_slot {t_cts:.2f}  eval_mod {t_em:.2f}  slot_to_coeff {t_stc:.2f} ms")
+for i, lt in enumerate(boot.cts + boot.stc):
+    x = raised if i < 3 else w
+    if ckks.level_of(x) != lt.level:
+        x = ckks.mod_drop(x, lt.level) if ckks.level_of(x) > lt.level else None
+    if x is None:
+        continue
+    _, t = timed(lambda: lt.apply(x, boot.keys))
+    print(f"   LT {i}: level {lt.level} diags {sum(len(r) for r in lt.table.values())} baby {len(lt.baby)} giants {len(lt.giants)} step {lt.step}: {t:.2f} ms")
