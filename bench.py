@@ -54,7 +54,7 @@ UNIT = {"bootstrap": "bootstraps/s", "keyswitch": "keyswitch/s", "ntt": "ntt/s"}
 CONFIG = {
     "bootstrap": {"workload": "full CKKS bootstrapping, 2^15 complex slots, N=2^16, ks48 moduli (L=48 31-bit "
                               "limbs, alpha=12, dnum=4), sparse secret h=32, input level 2 scale 2^52, "
-                              "output level 18; one ciphertext per step, CUDA-graph replay",
+                              "output level 18; one ciphertext per step, CUDA-graph replay with 4 stream lanes",
                   "l2_policy": "each step streams ~8 GB of keys and plaintext diagonals (>> 126 MB L2)"},
     "keyswitch": {"workload": "keyswitch ks48 (N=2^16, L=48, alpha=12, dnum=4, 31-bit primes), one ciphertext per step",
                   "l2_policy": "inputs rotate through >126 MB"},
@@ -259,6 +259,7 @@ def run_b200(args):
     if wl == "bootstrap":
         from paper_2512_18345_b200.bootstrap import BootstrapConfig, Bootstrapper
 
+        eng.set_lanes(args.lanes)           # concurrent rotations / EvalMod branches inside the graph
         sk = ks.keygen(p, h=p.h_sparse, seed=1 + rank)
         boot = Bootstrapper(p, sk, BootstrapConfig())
         rng = np.random.default_rng(rank)
@@ -439,6 +440,7 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--workload", default="bootstrap", choices=["bootstrap", "keyswitch", "ntt"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--lanes", type=int, default=4, help="workspace lanes / side streams of the bootstrap graph")
     args = ap.parse_args()
     if args.steps is None:
         args.steps = DEFAULT_STEPS[args.workload]

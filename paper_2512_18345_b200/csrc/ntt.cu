@@ -72,14 +72,12 @@ template <class MUL>
 __device__ __forceinline__ void ct16(uint32_t (&v)[16], uint32_t q, MUL mul) {
 #pragma unroll
     for (int s = 0; s < 4; ++s) {
-        const int half = 8 >> s;
 #pragma unroll
-        for (int g = 0; g < (1 << s); ++g) {
-#pragma unroll
-            for (int j = 0; j < half; ++j) {
-                const int i0 = g * 2 * half + j;
-                ct_bfly(v[i0], v[i0 + half], mul(s, g, v[i0 + half]), q);
-            }
+        for (int b = 0; b < 8; ++b) {              // fixed trip count: always fully unrolled
+            const int half = 8 >> s;
+            const int g = b >> (3 - s), j = b & (half - 1);
+            const int i0 = g * 2 * half + j;
+            ct_bfly(v[i0], v[i0 + half], mul(s, g, v[i0 + half]), q);
         }
     }
 }
@@ -87,21 +85,18 @@ __device__ __forceinline__ void ct16(uint32_t (&v)[16], uint32_t q, MUL mul) {
 // Four Gentleman-Sande stages on 16 registers, canonical in and out.
 // MUL(s, g, d): d * w mod q in [0, q) for local stage s (pair distance 2^s),
 // local group g (0 .. (8 >> s) - 1); d may be any 32-bit value.
-template <class MUL>
-__device__ __forceinline__ void gs16(uint32_t (&v)[16], uint32_t q, MUL mul, int stages = 4) {
+template <int STAGES = 4, class MUL>
+__device__ __forceinline__ void gs16(uint32_t (&v)[16], uint32_t q, MUL mul) {
 #pragma unroll
-    for (int s = 0; s < 4; ++s) {
-        if (s >= stages) break;
-        const int t = 1 << s;
+    for (int s = 0; s < STAGES; ++s) {
 #pragma unroll
-        for (int g = 0; g < (8 >> s); ++g) {
-#pragma unroll
-            for (int j = 0; j < t; ++j) {
-                const int i0 = g * 2 * t + j;
-                const uint32_t x = v[i0], y = v[i0 + t];
-                v[i0] = csub(x + y, q);
-                v[i0 + t] = mul(s, g, x - y + q);
-            }
+        for (int b = 0; b < 8; ++b) {
+            const int t = 1 << s;
+            const int g = b >> s, j = b & (t - 1);
+            const int i0 = g * 2 * t + j;
+            const uint32_t x = v[i0], y = v[i0 + t];
+            v[i0] = csub(x + y, q);
+            v[i0 + t] = mul(s, g, x - y + q);
         }
     }
 }
@@ -176,7 +171,7 @@ ntt16_inv_strided(const uint32_t* in, uint32_t* out, const int32_t* __restrict__
 #pragma unroll
     for (int k = 0; k < 16; ++k) v[k] = tile[(g + 17 * k) * COLS + c];
     // global stages 12..14 on rows j = g + 16k, then the last stage with N^-1
-    gs16(v, q, TW_MUL(s_tw[(8 >> s) + gi]), 3);
+    gs16<3>(v, q, TW_MUL(s_tw[(8 >> s) + gi]));
     uint32_t* dst = out + rm.out_row(blockIdx.y) * kN16 + blockIdx.x * COLS + c;
     const uint32_t ninv = m.n_inv, ninv_s = m.n_inv_s, wl = m.w_last, wl_s = m.w_last_s;
 #pragma unroll
@@ -212,7 +207,6 @@ __global__ void __launch_bounds__(256)
 ntt16_fwd_contig(const uint32_t* in, uint32_t* out, const int32_t* __restrict__ row_slot,
                  const ModSlot* __restrict__ slots, RowMap rm) {
     __shared__ uint32_t tile[16 * 272];
-    __shared__ uint2 s_yz[240];
     __shared__ uint2 s_blk[16][20];      // per block: 15 twiddles of stages 8..11, then X_0..X_3
     const int tid = threadIdx.x;
     const int e = tid & 15, blk = tid >> 4;
@@ -221,10 +215,11 @@ ntt16_fwd_contig(const uint32_t* in, uint32_t* out, const int32_t* __restrict__ 
     const uint32_t B = blockIdx.x * 16 + blk;          // 256-element block index within the limb
     const uint32_t* src = in + rm.in_row(blockIdx.y) * kN16 + B * 256;
     const uint2* __restrict__ fwd = m.fwd;
-    if (tid < 240) s_yz[tid] = m.otf_fwd[tid];
-    for (int i = tid; i < 16 * 19; i += 256) {
-        const int b = i / 19, j = i - b * 19;
-        const uint32_t Bb = 256 + blockIdx.x * 16 + b;
+    const uint2* __restrict__ yz = m.otf_fwd;
+    // the 16 threads of a 256-block stage that block's 19 table entries themselves: the whole
+    // kernel then only needs warp-level synchronisation (a block's exchange is half a warp)
+    for (int j = e; j < 19; j += 16) {
+        const uint32_t Bb = 256 + B;
         uint32_t idx;
         if (j < 15) {
             const int st = 31 - __clz(j + 1);          // local stage, group = j + 1 - 2^st
@@ -232,17 +227,17 @@ ntt16_fwd_contig(const uint32_t* in, uint32_t* out, const int32_t* __restrict__ 
         } else {
             idx = (Bb * 16) << (j - 15);
         }
-        s_blk[b][j] = fwd[idx];
+        s_blk[blk][j] = fwd[idx];
     }
     uint32_t v[16];
 #pragma unroll
     for (int k = 0; k < 16; ++k) v[k] = src[e + 16 * k];
-    __syncthreads();
+    __syncwarp();
     // global stages 8..11: elements e + 16k, slot = (256 + B) * 2^s + group
     ct16(v, q, TW_MUL(s_blk[blk][(1 << s) - 1 + gi]));
 #pragma unroll
     for (int k = 0; k < 16; ++k) tile[blk * 272 + e + 17 * k] = v[k];
-    __syncthreads();
+    __syncwarp();
 #pragma unroll
     for (int k = 0; k < 16; ++k) v[k] = tile[blk * 272 + 17 * e + k];
     // global stages 12..15: elements 16e + k, twiddle = X_s[B] * YZ_s[g][e]
@@ -250,8 +245,8 @@ ntt16_fwd_contig(const uint32_t* in, uint32_t* out, const int32_t* __restrict__ 
 #pragma unroll
     for (int st = 0; st < 4; ++st) X[st] = s_blk[blk][15 + st];
     ct16(v, q, [&](int s, int gi, uint32_t y) {
-        const uint2 yz = s_yz[yz_index(s, gi, e)];
-        return shoup_mul(shoup_lazy(y, yz.x, yz.y, q), X[s].x, X[s].y, q);
+        const uint2 yzv = __ldg(&yz[yz_index(s, gi, e)]);
+        return shoup_mul(shoup_lazy(y, yzv.x, yzv.y, q), X[s].x, X[s].y, q);
     });
     uint4* dst = reinterpret_cast<uint4*>(out + rm.out_row(blockIdx.y) * kN16 + B * 256 + 16 * e);
 #pragma unroll
@@ -264,7 +259,6 @@ __global__ void __launch_bounds__(256)
 ntt16_inv_contig(const uint32_t* in, uint32_t* out, const int32_t* __restrict__ row_slot,
                  const ModSlot* __restrict__ slots, RowMap rm) {
     __shared__ uint32_t tile[16 * 272];
-    __shared__ uint2 s_yz[240];
     __shared__ uint2 s_blk[16][20];      // per block: 15 twiddles of stages 4..7, then X_0..X_3
     const int tid = threadIdx.x;
     const int e = tid & 15, blk = tid >> 4;
@@ -273,10 +267,9 @@ ntt16_inv_contig(const uint32_t* in, uint32_t* out, const int32_t* __restrict__ 
     const uint32_t B = blockIdx.x * 16 + blk;
     const uint4* src = reinterpret_cast<const uint4*>(in + rm.in_row(blockIdx.y) * kN16 + B * 256 + 16 * e);
     const uint2* __restrict__ inv = m.inv;
-    if (tid < 240) s_yz[tid] = m.otf_inv[tid];
-    for (int i = tid; i < 16 * 19; i += 256) {
-        const int b = i / 19, j = i - b * 19;
-        const uint32_t Bb = 256 + blockIdx.x * 16 + b;
+    const uint2* __restrict__ yz = m.otf_inv;
+    for (int j = e; j < 19; j += 16) {
+        const uint32_t Bb = 256 + B;
         uint32_t idx;
         if (j < 15) {
             // stage s of 4..7 has (8 >> s) groups; entries laid out 8 | 4 | 2 | 1
@@ -286,7 +279,7 @@ ntt16_inv_contig(const uint32_t* in, uint32_t* out, const int32_t* __restrict__ 
         } else {
             idx = (Bb * 16) << (j - 15);
         }
-        s_blk[b][j] = inv[idx];
+        s_blk[blk][j] = inv[idx];
     }
     uint32_t v[16];
 #pragma unroll
@@ -294,18 +287,18 @@ ntt16_inv_contig(const uint32_t* in, uint32_t* out, const int32_t* __restrict__ 
         const uint4 u = src[k];
         v[4 * k] = u.x; v[4 * k + 1] = u.y; v[4 * k + 2] = u.z; v[4 * k + 3] = u.w;
     }
-    __syncthreads();
+    __syncwarp();
     // global stages 0..3 on elements 16e + k: slot = [1][B][e][g] with (3 - s) group bits
     uint2 X[4];
 #pragma unroll
     for (int st = 0; st < 4; ++st) X[st] = s_blk[blk][15 + st];
     gs16(v, q, [&](int s, int gi, uint32_t d) {
-        const uint2 yz = s_yz[yz_index(3 - s, gi, e)];
-        return shoup_mul(shoup_lazy(d, yz.x, yz.y, q), X[3 - s].x, X[3 - s].y, q);
+        const uint2 yzv = __ldg(&yz[yz_index(3 - s, gi, e)]);
+        return shoup_mul(shoup_lazy(d, yzv.x, yzv.y, q), X[3 - s].x, X[3 - s].y, q);
     });
 #pragma unroll
     for (int k = 0; k < 16; ++k) tile[blk * 272 + 17 * e + k] = v[k];
-    __syncthreads();
+    __syncwarp();
 #pragma unroll
     for (int k = 0; k < 16; ++k) v[k] = tile[blk * 272 + e + 17 * k];
     // global stages 4..7 on elements e + 16k: slot = (256 + B) * (8 >> s) + group
