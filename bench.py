@@ -356,11 +356,16 @@ def run_b200(args):
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         if sampler:
             sampler.start()
+        ranged = sampler is not None and os.environ.get("BENCH_PROFILER_RANGE")
+        if ranged:                      # ncu --profile-from-start off: only the timed region is profiled
+            torch.cuda.profiler.start()
         a.record()
         for i in range(steps):
             fn(i)
         b.record()
         barrier()
+        if ranged:
+            torch.cuda.profiler.stop()
         if sampler:
             sampler.stop()
         ms = a.elapsed_time(b)
@@ -381,6 +386,8 @@ def run_b200(args):
 
     # per-kernel pass: the same step, eager, every launch bracketed by CUDA events
     prof_steps = max(2, min(args.steps, 3 if wl == "bootstrap" else 50))
+    lanes_saved = getattr(eng, "lanes", 1)
+    eng.lanes = 1                      # one stream: per-kernel durations without overlap from other lanes
     profiled_step(0)
     torch.cuda.synchronize()
     eng.lib.ckks_profile_enable(1)
@@ -388,6 +395,7 @@ def run_b200(args):
         profiled_step(i)
     prof = read_profile(eng)
     eng.lib.ckks_profile_enable(0)
+    eng.lanes = lanes_saved
     launches_per_step = sum(c for c, _, _ in prof.values()) / prof_steps
     total_prof_ms = sum(ms for _, ms, _ in prof.values())
     top = max(prof, key=lambda k: prof[k][1])

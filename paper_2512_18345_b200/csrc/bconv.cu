@@ -148,23 +148,34 @@ bconv_f64(BconvJobs jobs, const ModSlot* __restrict__ slots, size_t cols) {
     }
     const double seed = 4503599627370496.0;     // 2^52
     const int i_lo = blockIdx.z * kOutChunk, i_hi = min(l_out, i_lo + kOutChunk);
-#pragma unroll 2
-    for (int i = i_lo; i < i_hi; ++i) {
-        const uint4 om = s_om[i];
-        const double2* trow = reinterpret_cast<const double2*>(s_t + (size_t)i * LINP);
-        double a0 = seed, a1 = seed;
+    constexpr int U = 4;                        // outputs in flight: 2*U independent DFMA chains
+    for (int i0 = i_lo; i0 < i_hi; i0 += U) {
+        double a0[U], a1[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) a0[u] = a1[u] = seed;
 #pragma unroll
         for (int k = 0; k < LINP; k += 2) {
-            const double2 t = trow[k / 2];
-            a0 = fma(t.x, y0[k], a0);
-            a1 = fma(t.x, y1[k], a1);
-            a0 = fma(t.y, y0[k + 1], a0);
-            a1 = fma(t.y, y1[k + 1], a1);
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int i = min(i0 + u, i_hi - 1);
+                const double2 t = reinterpret_cast<const double2*>(s_t + (size_t)i * LINP)[k / 2];
+                a0[u] = fma(t.x, y0[k], a0[u]);
+                a1[u] = fma(t.x, y1[k], a1[u]);
+                a0[u] = fma(t.y, y0[k + 1], a0[u]);
+                a1[u] = fma(t.y, y1[k + 1], a1[u]);
+            }
         }
-        const uint64_t b0 = (uint64_t)__double_as_longlong(a0) & 0xFFFFFFFFFFFFFull;
-        const uint64_t b1 = (uint64_t)__double_as_longlong(a1) & 0xFFFFFFFFFFFFFull;
-        const uint64_t v = (uint64_t)(uint32_t)(b1 >> 32) * om.w + ((b1 & 0xFFFFFFFFull) << 16) + b0;
-        job.out[(size_t)om.z * job.out_stride + c] = redc((uint32_t)v, (uint32_t)(v >> 32), om.x, om.y);
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int i = i0 + u;
+            if (i < i_hi) {
+                const uint4 om = s_om[i];
+                const uint64_t b0 = (uint64_t)__double_as_longlong(a0[u]) & 0xFFFFFFFFFFFFFull;
+                const uint64_t b1 = (uint64_t)__double_as_longlong(a1[u]) & 0xFFFFFFFFFFFFFull;
+                const uint64_t v = (uint64_t)(uint32_t)(b1 >> 32) * om.w + ((b1 & 0xFFFFFFFFull) << 16) + b0;
+                job.out[(size_t)om.z * job.out_stride + c] = redc((uint32_t)v, (uint32_t)(v >> 32), om.x, om.y);
+            }
+        }
     }
 }
 

@@ -126,3 +126,39 @@ for i, lt in enumerate(boot.cts + boot.stc):
         continue
     _, t = timed(lambda: lt.apply(x, boot.keys))
     print(f"   LT {i}: level {lt.level} diags {sum(len(r) for r in lt.table.values())} baby {len(lt.baby)} giants {len(lt.giants)} step {lt.step}: {t:.2f} ms")
+
+# phase timing under CUDA-graph replay
+def graph_time(fn, reps=10):
+    fn(); torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(side):
+        fn(); torch.cuda.synchronize()
+        with torch.cuda.graph(g, stream=side):
+            keep = fn()
+    torch.cuda.current_stream().wait_stream(side)
+    for _ in range(3):
+        g.replay()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(reps):
+        g.replay()
+    b.record(); torch.cuda.synchronize()
+    return a.elapsed_time(b) / reps
+raised = boot.mod_raise(ct)
+lo, hi = boot.coeff_to_slot(raised)
+t_cts = graph_time(lambda: boot.coeff_to_slot(raised))
+t_em = graph_time(lambda: eng.fork([lambda: boot.eval_mod(lo, boot.coef_lo, kappa), lambda: boot.eval_mod(hi, boot.coef_hi, kappa * 1j)]))
+m_lo, m_hi = eng.fork([lambda: boot.eval_mod(lo, boot.coef_lo, kappa), lambda: boot.eval_mod(hi, boot.coef_hi, kappa * 1j)])
+w = ckks.add(m_lo, m_hi)
+t_stc = graph_time(lambda: boot.slot_to_coeff(w))
+t_one = graph_time(lambda: boot.eval_mod(lo, boot.coef_lo, kappa))
+print(f"graph phases: coeff_to_slot {t_cts:.2f}  eval_mod(both) {t_em:.2f}  eval_mod(one branch) {t_one:.2f}  slot_to_coeff {t_stc:.2f} ms")
+for i, lt in enumerate(boot.cts[:1] + boot.stc[:1]):
+    x = raised if i == 0 else w
+    print(f"   graph LT level {lt.level}: {graph_time(lambda: lt.apply(x, boot.keys)):.2f} ms")
+sq_in = lo
+print(f"   graph hmult+rescale at level {ckks.level_of(sq_in)}: {graph_time(lambda: boot._mul(sq_in, sq_in)):.3f} ms")
+low = ckks.mod_drop(lo, 24)
+print(f"   graph hmult+rescale at level 24: {graph_time(lambda: boot._mul(low, low)):.3f} ms")
