@@ -200,6 +200,16 @@ int ckks_ks_hoisted(ckks_ctx* ctx, int32_t plan, const uint32_t* raised, uint32_
                     const uint32_t* evk, const uint32_t* ct_b, uint32_t* out_a, uint32_t* out_b,
                     void* stream);
 
+/* Double hoisting: like ckks_ks_hoisted but WITHOUT the ModDown -- writes the Q||P
+ * accumulator of the rotated ciphertext, out_qp [2][l+alpha][n], with (P mod q_i) *
+ * sigma_k(ct_b) already folded into the Q rows of its b half, so that
+ * ModDown(out_qp) = hrot(ct).  Sums of plaintext products of several such accumulators
+ * (the inner sums of a BSGS linear transform, plaintexts encoded over Q||P) then need one
+ * ModDown per sum (ckks_ks_stage3 on the pieces of the buffer) instead of one per
+ * rotation.  k = 0 applies no automorphism. */
+int ckks_ks_hoisted_raw(ckks_ctx* ctx, int32_t plan, const uint32_t* raised, uint32_t k,
+                        const uint32_t* evk, const uint32_t* ct_b, uint32_t* out_qp, void* stream);
+
 /* Key switches whose results are summed (giant steps of a BSGS linear transform) can
  * share one ModDown: ckks_ks_accumulate runs stages 1-2 of keyswitch.py:444-453 for
  * (ct_a, evk) and adds the Q||P accumulator into the current lane's workspace (first !=

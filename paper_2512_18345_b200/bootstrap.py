@@ -134,9 +134,10 @@ class LinearTransform:
     unchanged (two limbs where 2^-31 relative plaintext precision is not enough)."""
 
     def __init__(self, diags: dict, params: ParameterSet, level: int, n1: int | None = None,
-                 factor: complex = 1.0, limbs: int = 1):
+                 factor: complex = 1.0, limbs: int = 1, double_hoist: bool = True):
         n = params.n // 2
         self.params, self.level, self.n, self.limbs = params, level, n, limbs
+        self.double_hoist = double_hoist
         offs = sorted(diags)
         signed = [d if d <= n // 2 else d - n for d in offs]
         nz = [abs(d) for d in signed if d]
@@ -145,16 +146,63 @@ class LinearTransform:
         span = max(units) - min(units) + 1
         if n1 is None:
             n1 = 1 << max(0, round(math.log2(math.sqrt(span))))
+            if double_hoist:
+                # baby steps cost one inner product each (no ModUp, no ModDown), giant steps a
+                # ModUp + inner product + a ModDown of their inner sum: favour more baby steps
+                n1 = min(2 * n1, 16)
         self.step, self.n1 = step, n1
         self.pt_scale = float(math.prod(m.q for m in params.q_basis[level - limbs:level]))
+        ext_basis = params.q_basis[:level] + params.p_basis
+        p_prod = math.prod(m.q for m in params.p_basis)
+        lift = [p_prod % m.q for m in params.q_basis[:level]] + [0] * len(params.p_basis)
         table: dict[int, dict[int, ckks.Plaintext]] = {}
         for d, u in zip(offs, units):
             g, b = divmod(u, n1)                      # floor division: b in [0, n1)
             vec = _rot(diags[d] * factor, -g * n1 * step)
-            table.setdefault(g, {})[b] = ckks.encode(vec, params, level=level, scale=self.pt_scale)
+            if double_hoist:
+                # plaintexts over Q_l || P; the unrotated term multiplies the ciphertext lifted to
+                # Q||P, i.e. times P on the Q limbs and zero on the P limbs: fold that into it
+                pt = ckks.encode(vec, params, scale=self.pt_scale, basis=ext_basis,
+                                 row_factors=lift if b == 0 else None)
+            else:
+                pt = ckks.encode(vec, params, level=level, scale=self.pt_scale)
+            table.setdefault(g, {})[b] = pt
         self.table = table
         self.baby = sorted({b for row in table.values() for b in row})
         self.giants = sorted(table)
+
+    def _double_hoisted_inner(self, ct, keys, eng):
+        """Baby steps as raw Q||P accumulators sharing one ModUp; returns inner_sum(g) that
+        forms sum_b pt_{g,b} * u_b over Q||P in one fused pass and scales it down once."""
+        import torch
+
+        p = self.params
+        n_ring, level, alpha = p.n, self.level, p.alpha
+        ext = level + alpha
+        basis = ct.a.basis
+        plan = eng.ks_plan(n_ring, basis, p.p_basis, alpha, p.l + alpha, p.l)
+        ext_slots = eng.row_slots(basis + p.p_basis)
+        raised = eng.ks_stage1(plan, ct.a.data, -(-level // alpha), ext)
+        b_half = ct.b.data
+        moving = [b for b in self.baby if b]
+
+        def raw(b):
+            k = ckks.galois_element(b * self.step, n_ring)
+            if k not in keys.galois:
+                raise RnsError(f"no Galois key for rotation {b * self.step}")
+            return eng.ks_hoisted_raw(plan, raised, k, keys.galois[k].matrix(), b_half, ext)
+
+        acc = dict(zip(moving, eng.fork([(lambda b=b: raw(b)) for b in moving])))
+        if 0 in self.baby:
+            x = ckks.ct_tensor(ct)
+            acc[0] = torch.cat([x, torch.zeros((2, alpha, n_ring), dtype=x.dtype, device=x.device)], dim=1)
+
+        def inner_sum(g):
+            row = self.table[g]
+            qp = eng.fused_terms([acc[b] for b in row], [pt.poly.data for pt in row.values()], ext_slots)
+            return eng.ks_stage3(plan, qp[0, :level], qp[1, :level], qp[0, level:], qp[1, level:])
+
+        return inner_sum
 
     def rotations(self) -> set[int]:
         out = {(b * self.step) % self.n for b in self.baby if b}
@@ -169,13 +217,16 @@ class LinearTransform:
             raise RnsError(f"linear transform encoded for level {self.level}, ciphertext at {ckks.level_of(ct)}")
         basis = ct.a.basis
         slots = eng.row_slots(basis)
-        # baby steps: independent rotations of the same input, spread over the lanes
-        hoisted = ckks.hrot_hoisted(ct, [b * self.step for b in self.baby], keys)
-        rotated = {b: hoisted[b * self.step] for b in self.baby}
+        if self.double_hoist:
+            inner_sum = self._double_hoisted_inner(ct, keys, eng)
+        else:
+            # baby steps: rotations of the same input sharing one ModUp, spread over the lanes
+            hoisted = ckks.hrot_hoisted(ct, [b * self.step for b in self.baby], keys)
+            rotated = {b: hoisted[b * self.step] for b in self.baby}
 
-        def inner_sum(g):
-            row = self.table[g]
-            return eng.fused_terms([rotated[b] for b in row], [pt.poly.data for pt in row.values()], slots)
+            def inner_sum(g):
+                row = self.table[g]
+                return eng.fused_terms([rotated[b] for b in row], [pt.poly.data for pt in row.values()], slots)
 
         inners = dict(zip(self.giants, eng.fork([(lambda g=g: inner_sum(g)) for g in self.giants])))
         base = inners.get(0)

@@ -131,9 +131,12 @@ def _round_to_residues(vals: np.ndarray, basis) -> np.ndarray:
     return np.stack(rows)
 
 
-def encode(values, params: ParameterSet, level: int | None = None, scale: float | None = None) -> Plaintext:
+def encode(values, params: ParameterSet, level: int | None = None, scale: float | None = None,
+           basis=None, row_factors=None) -> Plaintext:
     """Complex (or real) slot vector of length N/2 (a scalar broadcasts) ->
-    evaluation-domain plaintext at `level` limbs, coefficients round(scale * m)."""
+    evaluation-domain plaintext at `level` limbs, coefficients round(scale * m).
+    `basis` overrides the limb set (e.g. Q_l || P for double-hoisted linear transforms);
+    `row_factors[i]` multiplies limb i by a constant (e.g. P mod q_i)."""
     level = params.l if level is None else level
     scale = float(params.delta) if scale is None else float(scale)
     n = params.n
@@ -141,8 +144,11 @@ def encode(values, params: ParameterSet, level: int | None = None, scale: float 
     if z.ndim == 0:
         z = np.full(n // 2, z)
     coeffs = Embedding(n).to_coeffs(z)
-    basis = params.q_basis[:level]
+    basis = params.q_basis[:level] if basis is None else tuple(basis)
     rows = _round_to_residues(coeffs.astype(np.longdouble) * np.longdouble(scale), basis)
+    if row_factors is not None:
+        for i, (m, f) in enumerate(zip(basis, row_factors)):
+            rows[i] = rows[i] * np.uint64(f % m.q) % np.uint64(m.q)
     return Plaintext(ntt_polynomial(Polynomial(basis, rows, COEFFICIENT)), scale)
 
 

@@ -132,6 +132,7 @@ struct KsPlan {
     int32_t moddown_table = -1;
     int32_t *d_s3_in_row = nullptr, *d_s3_p_slot = nullptr, *d_s3_q_slot = nullptr;
     uint32_t *d_pinv = nullptr, *d_pinv_s = nullptr;
+    uint32_t *d_pmod = nullptr, *d_pmod_s = nullptr;   // P mod q_i (and Shoup companion)
     // workspace: word offsets into the context's shared arena (bound at call time)
     size_t off_coeff = 0, off_raised = 0, off_acc = 0, off_conv = 0, off_pc = 0, ws_words = 0;
     uint32_t *ws_coeff = nullptr, *ws_raised = nullptr, *ws_acc = nullptr, *ws_conv = nullptr,
@@ -274,7 +275,7 @@ void ckks_ctx_destroy(ckks_ctx* ctx) {
         for (void* p : {(void*)pl->d_q_slot, (void*)pl->d_p_slot, (void*)pl->d_ext_slot,
                         (void*)pl->d_evk_row, (void*)pl->d_s1_row, (void*)pl->d_s1_slot,
                         (void*)pl->d_s3_in_row, (void*)pl->d_s3_p_slot, (void*)pl->d_s3_q_slot,
-                        (void*)pl->d_pinv, (void*)pl->d_pinv_s})
+                        (void*)pl->d_pinv, (void*)pl->d_pinv_s, (void*)pl->d_pmod, (void*)pl->d_pmod_s})
             cudaFree(p);
         for (int32_t* p : pl->d_raise_out_row) cudaFree(p);
     }
@@ -591,7 +592,7 @@ static int plan_create(ckks_ctx* ctx, uint32_t n, int l, int alpha, const int32_
     CKS(upload(s1_slot, &pl->d_s1_slot));
     // stage 3: P -> Q table, P^-1 mod q_i (keyswitch.py:203-208)
     CKS(ckks_bconv_table_create(ctx, pv.data(), alpha, qv.data(), l, &pl->moddown_table));
-    std::vector<uint32_t> pinv(l), pinv_s(l);
+    std::vector<uint32_t> pinv(l), pinv_s(l), pmod(l), pmod_s(l);
     for (int i = 0; i < l; ++i) {
         const uint32_t q = ctx->h_slots[qv[i]].q;
         uint64_t prod = 1 % q;
@@ -599,7 +600,11 @@ static int plan_create(ckks_ctx* ctx, uint32_t n, int l, int alpha, const int32_
         if (prod == 0) { set_last_error("P and Q bases share a modulus"); return CKKS_ERR_ARG; }
         pinv[i] = h_inv((uint32_t)prod, q);
         pinv_s[i] = h_shoup(pinv[i], q);
+        pmod[i] = (uint32_t)prod;
+        pmod_s[i] = h_shoup(pmod[i], q);
     }
+    CKS(upload(pmod, &pl->d_pmod));
+    CKS(upload(pmod_s, &pl->d_pmod_s));
     CKS(upload(pinv, &pl->d_pinv));
     CKS(upload(pinv_s, &pl->d_pinv_s));
     std::vector<int32_t> s3_in_row, s3_p_slot, s3_q_slot;
@@ -702,9 +707,9 @@ static int stage3_core(ckks_ctx* ctx, KsPlan* pl, const uint32_t* q_a, const uin
                        const uint32_t* fold_a = nullptr) {
     const size_t n = pl->n;
     const RowMap id{nullptr, nullptr};
-    if (p_a == pl->ws_acc + (size_t)pl->l * n && p_b == p_a + (size_t)pl->ext * n) {
-        // accumulator laid out [2][ext][n]: both P parts in one launch
-        CKS(ntt_launch(pl->ws_acc, pl->ws_pc, pl->d_s3_p_slot, ctx->d_slots,
+    if (p_b == p_a + (size_t)pl->ext * n) {
+        // accumulator laid out [2][ext][n]: both P parts in one launch through the row map
+        CKS(ntt_launch(p_a - (size_t)pl->l * n, pl->ws_pc, pl->d_s3_p_slot, ctx->d_slots,
                        RowMap{pl->d_s3_in_row, nullptr}, 2 * pl->alpha, pl->n, 1, st));
     } else {
         CKS(ntt_launch(p_a, pl->ws_pc, pl->d_s3_p_slot, ctx->d_slots, id, pl->alpha, pl->n, 1, st));
@@ -742,6 +747,7 @@ static InnerProductArgs ip_args(KsPlan* pl, const uint32_t* carry, const uint32_
     a.l = pl->l; a.alpha = pl->alpha; a.beta = pl->beta; a.ext = pl->ext; a.evk_ext = pl->evk_ext;
     a.row_lo = row_lo; a.row_hi = row_hi; a.n = pl->n;
     a.galois = 0; a.lg = log2u(pl->n); a.accumulate = 0;
+    a.lift_b = nullptr; a.pmod = nullptr; a.pmod_s = nullptr;
     return a;
 }
 
@@ -812,6 +818,21 @@ int ckks_ks_hoisted(ckks_ctx* ctx, int32_t plan, const uint32_t* raised, uint32_
     CKS(inner_product_launch(ip, ctx->d_slots, st));
     return stage3_core(ctx, pl, acc_a, acc_b, acc_a + (size_t)pl->l * n, acc_b + (size_t)pl->l * n,
                        ct_b, out_a, out_b, st, ip.galois);
+}
+
+int ckks_ks_hoisted_raw(ckks_ctx* ctx, int32_t plan, const uint32_t* raised, uint32_t k,
+                        const uint32_t* evk, const uint32_t* ct_b, uint32_t* out_qp, void* stream) {
+    KsPlan* pl;
+    CKS(get_plan(ctx, plan, &pl));
+    CKS(need_full_plan(pl));
+    if (k != 0 && !(k & 1)) { set_last_error("automorphism index must be odd (or 0 for none)"); return CKKS_ERR_ARG; }
+    const size_t n = pl->n;
+    InnerProductArgs ip = ip_args(pl, nullptr, raised, evk, 0, pl->ext, out_qp, out_qp + (size_t)pl->ext * n);
+    ip.galois = k & (2 * pl->n - 1);
+    ip.lift_b = ct_b;
+    ip.pmod = pl->d_pmod;
+    ip.pmod_s = pl->d_pmod_s;
+    return inner_product_launch(ip, ctx->d_slots, (cudaStream_t)stream);
 }
 
 // ---- giant steps sharing one ModDown ---------------------------------------------------

@@ -86,6 +86,15 @@ inner_product_kernel(InnerProductArgs p, const ModSlot* __restrict__ slots) {
     }
     uint32_t* oa = p.acc_a + (size_t)(row - p.row_lo) * n + i;
     uint32_t* ob = p.acc_b + (size_t)(row - p.row_lo) * n + i;
+    if (p.lift_b && row < p.l) {
+        const uint32_t pm = p.pmod[row], pms = p.pmod_s[row];
+        const uint32_t* bsrc = p.lift_b + (size_t)row * n;
+#pragma unroll
+        for (int w = 0; w < W; ++w) {
+            const uint32_t bv = p.galois ? bsrc[galois_src((uint32_t)i + w, p.galois, p.n, p.lg)] : bsrc[i + w];
+            rb[w] = add_mod(rb[w], shoup_mul(bv, pm, pms, m.q), m.q);
+        }
+    }
     if (p.accumulate) {
 #pragma unroll
         for (int w = 0; w < W; ++w) {

@@ -267,6 +267,13 @@ class Engine:
                                             self.stream()))
         return out
 
+    def ks_hoisted_raw(self, plan: int, raised, k: int, evk, ct_b, ext: int):
+        """Q||P accumulator [2, ext, n] of the ciphertext rotated by X -> X^k (no ModDown)."""
+        out = self.empty(2, ext, ct_b.shape[1])
+        _lib.check(self.lib.ckks_ks_hoisted_raw(self.ctx, plan, raised.data_ptr(), k, evk.data_ptr(),
+                                                ct_b.data_ptr(), out.data_ptr(), self.stream()))
+        return out
+
     def ks_accumulate(self, plan: int, ct_a, evk, first: bool):
         _lib.check(self.lib.ckks_ks_accumulate(self.ctx, plan, ct_a.data_ptr(), evk.data_ptr(),
                                                int(first), self.stream()))
