@@ -210,6 +210,15 @@ int ckks_ks_hoisted(ckks_ctx* ctx, int32_t plan, const uint32_t* raised, uint32_
 int ckks_ks_hoisted_raw(ckks_ctx* ctx, int32_t plan, const uint32_t* raised, uint32_t k,
                         const uint32_t* evk, const uint32_t* ct_b, uint32_t* out_qp, void* stream);
 
+/* Relinearisation fused with the rescale that follows it: key switch of d2 under evk,
+ * plus (d1, d0) lifted into the Q||P accumulator, then ONE ModDown by P * (the k dropped
+ * limbs) through `md_plan` = ckks_moddown_plan_create(l - k limbs, P' = dropped limbs then
+ * P).  Output [l-k][n] per half.  Equals rescale(relinearize(d0, d1, d2)) up to the rounding
+ * of one division instead of two. */
+int ckks_ks_relin_rescale(ckks_ctx* ctx, int32_t ks_plan, int32_t md_plan, const uint32_t* d2,
+                          const uint32_t* d1, const uint32_t* d0, const uint32_t* evk,
+                          uint32_t* out_a, uint32_t* out_b, void* stream);
+
 /* Key switches whose results are summed (giant steps of a BSGS linear transform) can
  * share one ModDown: ckks_ks_accumulate runs stages 1-2 of keyswitch.py:444-453 for
  * (ct_a, evk) and adds the Q||P accumulator into the current lane's workspace (first !=

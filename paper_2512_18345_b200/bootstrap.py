@@ -377,7 +377,7 @@ class Bootstrapper:
 
     def _mul(self, x, y):
         lvl = min(ckks.level_of(x), ckks.level_of(y))
-        return ckks.rescale(ckks.hmult(ckks.mod_drop(x, lvl), ckks.mod_drop(y, lvl), self.keys.relin), 2)
+        return ckks.hmult_rescale(ckks.mod_drop(x, lvl), ckks.mod_drop(y, lvl), self.keys.relin, 2)
 
     def _exp_taylor(self, x, coef):
         """sum_k coef[k] x^k by a balanced power tree (depth ceil(log2(degree+1)))."""

@@ -377,6 +377,31 @@ def hmult(x: Ciphertext, y: Ciphertext, rlk: ks.SwitchingKey) -> Ciphertext:
     return relinearize(d0, d1, d2, rlk, x.scale * y.scale)
 
 
+def hmult_rescale(x: Ciphertext, y: Ciphertext, rlk: ks.SwitchingKey, k: int = 1) -> Ciphertext:
+    """rescale(hmult(x, y), k) with the relinearisation ModDown and the rescale merged into
+    one division by P * (the k dropped limbs): one base conversion and one NTT fewer per
+    multiplication.  Same value as the two-step route up to the rounding of the division."""
+    from .engine import get_engine
+
+    _same_level(x.a, y.a)
+    eng = get_engine()
+    params = rlk.params
+    level = level_of(x)
+    n = x.a.n
+    if n % 4 or level <= k:
+        return rescale(hmult(x, y, rlk), k)
+    basis = x.a.basis
+    if tuple(m.q for m in basis) != tuple(m.q for m in params.q_basis[:level]):
+        raise StructureError("ciphertext basis is not a prefix of the parameter q-basis")
+    rest, dropped = basis[:level - k], basis[level - k:]
+    d = eng.tensor(ct_tensor(x), ct_tensor(y), eng.row_slots(basis))
+    ks_plan = eng.ks_plan(n, basis, params.p_basis, params.alpha, params.l + params.alpha, params.l)
+    md_plan = eng.moddown_plan(n, rest, dropped + params.p_basis)
+    out = eng.ks_relin_rescale(ks_plan, md_plan, d, rlk.matrix(), level - k)
+    return Ciphertext(a=Polynomial(rest, out[0], EVALUATION), b=Polynomial(rest, out[1], EVALUATION),
+                      scale=x.scale * y.scale / math.prod(m.q for m in dropped))
+
+
 def rescale(ct: Ciphertext, k: int = 1) -> Ciphertext:
     """Drop the last k limbs, dividing message and scale by their product P: one ModDown
     pass with P = the dropped limbs, (x_rest - NTT(BConv_{P -> rest}(INTT(x_P)))) * P^-1.

@@ -120,6 +120,8 @@ struct BconvTable {
     std::vector<void*> owned;
 };
 
+constexpr int kMaxMergedDrop = 4;   // limbs a fused relinearise+rescale may drop
+
 struct KsPlan {
     uint32_t n = 0;
     int l = 0, alpha = 0, beta = 0, ext = 0, evk_ext = 0;
@@ -623,7 +625,7 @@ static int plan_create(ckks_ctx* ctx, uint32_t n, int l, int alpha, const int32_
         pl->off_raised = at; at += moddown_only ? 0 : nn * pl->beta * ext;
         pl->off_acc = at;    at += moddown_only ? 0 : nn * 2 * ext;
         pl->off_conv = at;   at += nn * 2 * l;
-        pl->off_pc = at;     at += nn * 2 * alpha;
+        pl->off_pc = at;     at += nn * 2 * (alpha + (moddown_only ? 0 : kMaxMergedDrop));
         pl->ws_words = at;
         if (at > ctx->ws_words) {
             CK(cudaDeviceSynchronize());
@@ -704,16 +706,19 @@ static uint32_t log2u(uint32_t n) {
 static int stage3_core(ckks_ctx* ctx, KsPlan* pl, const uint32_t* q_a, const uint32_t* q_b,
                        const uint32_t* p_a, const uint32_t* p_b, const uint32_t* fold_b,
                        uint32_t* out_a, uint32_t* out_b, cudaStream_t st, uint32_t galois = 0,
-                       const uint32_t* fold_a = nullptr) {
+                       const uint32_t* fold_a = nullptr, uint32_t* ws_conv = nullptr,
+                       uint32_t* ws_pc = nullptr) {
     const size_t n = pl->n;
+    if (!ws_conv) ws_conv = pl->ws_conv;     // a plan borrowed by another plan's call works in
+    if (!ws_pc) ws_pc = pl->ws_pc;           // the caller's workspace (arena layouts differ)
     const RowMap id{nullptr, nullptr};
     if (p_b == p_a + (size_t)pl->ext * n) {
         // accumulator laid out [2][ext][n]: both P parts in one launch through the row map
-        CKS(ntt_launch(p_a - (size_t)pl->l * n, pl->ws_pc, pl->d_s3_p_slot, ctx->d_slots,
+        CKS(ntt_launch(p_a - (size_t)pl->l * n, ws_pc, pl->d_s3_p_slot, ctx->d_slots,
                        RowMap{pl->d_s3_in_row, nullptr}, 2 * pl->alpha, pl->n, 1, st));
     } else {
-        CKS(ntt_launch(p_a, pl->ws_pc, pl->d_s3_p_slot, ctx->d_slots, id, pl->alpha, pl->n, 1, st));
-        CKS(ntt_launch(p_b, pl->ws_pc + (size_t)pl->alpha * n, pl->d_s3_p_slot, ctx->d_slots, id,
+        CKS(ntt_launch(p_a, ws_pc, pl->d_s3_p_slot, ctx->d_slots, id, pl->alpha, pl->n, 1, st));
+        CKS(ntt_launch(p_b, ws_pc + (size_t)pl->alpha * n, pl->d_s3_p_slot, ctx->d_slots, id,
                        pl->alpha, pl->n, 1, st));
     }
     BconvJobs jobs;
@@ -721,16 +726,16 @@ static int stage3_core(ckks_ctx* ctx, KsPlan* pl, const uint32_t* q_a, const uin
     for (int h = 0; h < 2; ++h) {
         BconvJob& j = jobs.job[h];
         j.tab = ctx->tables[pl->moddown_table]->dev;
-        j.in = pl->ws_pc + (size_t)h * pl->alpha * n;
+        j.in = ws_pc + (size_t)h * pl->alpha * n;
         j.in_stride = n;
-        j.out = pl->ws_conv + (size_t)h * pl->l * n;
+        j.out = ws_conv + (size_t)h * pl->l * n;
         j.out_stride = n;
         j.out_row = nullptr;
     }
     CKS(bconv_launch_jobs(jobs, ctx->d_slots, n, st));
-    CKS(ntt_launch(pl->ws_conv, pl->ws_conv, pl->d_s3_q_slot, ctx->d_slots, id, 2 * pl->l, pl->n, 0, st));
+    CKS(ntt_launch(ws_conv, ws_conv, pl->d_s3_q_slot, ctx->d_slots, id, 2 * pl->l, pl->n, 0, st));
     ModDownEpilogueArgs e{};
-    e.xq_a = q_a; e.xq_b = q_b; e.conv = pl->ws_conv; e.fold_a = fold_a; e.fold_b = fold_b;
+    e.xq_a = q_a; e.xq_b = q_b; e.conv = ws_conv; e.fold_a = fold_a; e.fold_b = fold_b;
     e.out_a = out_a; e.out_b = out_b;
     e.q_slot = pl->d_q_slot; e.pinv = pl->d_pinv; e.pinv_s = pl->d_pinv_s;
     e.l = pl->l; e.n = pl->n;
@@ -747,7 +752,7 @@ static InnerProductArgs ip_args(KsPlan* pl, const uint32_t* carry, const uint32_
     a.l = pl->l; a.alpha = pl->alpha; a.beta = pl->beta; a.ext = pl->ext; a.evk_ext = pl->evk_ext;
     a.row_lo = row_lo; a.row_hi = row_hi; a.n = pl->n;
     a.galois = 0; a.lg = log2u(pl->n); a.accumulate = 0;
-    a.lift_b = nullptr; a.pmod = nullptr; a.pmod_s = nullptr;
+    a.lift_a = nullptr; a.lift_b = nullptr; a.pmod = nullptr; a.pmod_s = nullptr;
     return a;
 }
 
@@ -833,6 +838,39 @@ int ckks_ks_hoisted_raw(ckks_ctx* ctx, int32_t plan, const uint32_t* raised, uin
     ip.pmod = pl->d_pmod;
     ip.pmod_s = pl->d_pmod_s;
     return inner_product_launch(ip, ctx->d_slots, (cudaStream_t)stream);
+}
+
+// Relinearisation (or any key switch) fused with the rescale that follows it: the
+// polynomials the switched pair is added to (d1, d0) are lifted into the Q||P accumulator
+// (times P on the Q rows), and ONE ModDown divides by P * q_{l-1} * ... * q_{l-k}: the
+// accumulator rows [l-k, l+alpha) are contiguous, so they serve as the "P part" of a
+// ModDown plan built for Q_{l-k} with P' = {q_{l-k}..q_{l-1}} U P.
+int ckks_ks_relin_rescale(ckks_ctx* ctx, int32_t ks_plan, int32_t md_plan, const uint32_t* d2,
+                          const uint32_t* d1, const uint32_t* d0, const uint32_t* evk,
+                          uint32_t* out_a, uint32_t* out_b, void* stream) {
+    KsPlan *pl, *md;
+    CKS(get_plan(ctx, ks_plan, &pl));
+    CKS(need_full_plan(pl));
+    CKS(get_plan(ctx, md_plan, &md));
+    if (md->n != pl->n || md->l + md->alpha != pl->ext || md->l >= pl->l) {
+        set_last_error("ModDown plan (l=%d, alpha=%d) does not tile the key-switch accumulator (l=%d, ext=%d)",
+                       md->l, md->alpha, pl->l, pl->ext);
+        return CKKS_ERR_ARG;
+    }
+    cudaStream_t st = (cudaStream_t)stream;
+    const size_t n = pl->n;
+    CKS(stage1_core(ctx, pl, d2, pl->ws_raised, false, st));
+    uint32_t* acc_a = pl->ws_acc;
+    uint32_t* acc_b = pl->ws_acc + (size_t)pl->ext * n;
+    InnerProductArgs ip = ip_args(pl, d2, pl->ws_raised, evk, 0, pl->ext, acc_a, acc_b);
+    ip.lift_a = d1;
+    ip.lift_b = d0;
+    ip.pmod = pl->d_pmod;
+    ip.pmod_s = pl->d_pmod_s;
+    CKS(inner_product_launch(ip, ctx->d_slots, st));
+    if (md->alpha > pl->alpha + kMaxMergedDrop) { set_last_error("merged rescale drops more than %d limbs", kMaxMergedDrop); return CKKS_ERR_UNSUPPORTED; }
+    return stage3_core(ctx, md, acc_a, acc_b, acc_a + (size_t)md->l * n, acc_b + (size_t)md->l * n,
+                       nullptr, out_a, out_b, st, 0, nullptr, pl->ws_conv, pl->ws_pc);
 }
 
 // ---- giant steps sharing one ModDown ---------------------------------------------------

@@ -127,6 +127,7 @@ struct InnerProductArgs {
     uint32_t n;
     uint32_t galois, lg;        // galois != 0: read digit columns through X -> X^galois (hoisting)
     int accumulate;             // add into acc instead of overwriting it
+    const uint32_t* lift_a;     // non-null: add (P mod q_i) * lift_a to the Q rows of acc_a (no automorphism)
     const uint32_t* lift_b;     // non-null: add (P mod q_i) * sigma(lift_b) to the Q rows of acc_b, i.e.
     const uint32_t* pmod;       //   fold the rotated ciphertext's b-part into the Q||P accumulator
     const uint32_t* pmod_s;     //   (double hoisting: no ModDown per rotation)

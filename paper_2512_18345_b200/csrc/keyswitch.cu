@@ -95,6 +95,12 @@ inner_product_kernel(InnerProductArgs p, const ModSlot* __restrict__ slots) {
             rb[w] = add_mod(rb[w], shoup_mul(bv, pm, pms, m.q), m.q);
         }
     }
+    if (p.lift_a && row < p.l) {
+        const uint32_t pm = p.pmod[row], pms = p.pmod_s[row];
+        const uint32_t* asrc = p.lift_a + (size_t)row * n;
+#pragma unroll
+        for (int w = 0; w < W; ++w) ra[w] = add_mod(ra[w], shoup_mul(asrc[i + w], pm, pms, m.q), m.q);
+    }
     if (p.accumulate) {
 #pragma unroll
         for (int w = 0; w < W; ++w) {

@@ -274,6 +274,14 @@ class Engine:
                                                 ct_b.data_ptr(), out.data_ptr(), self.stream()))
         return out
 
+    def ks_relin_rescale(self, ks_plan: int, md_plan: int, d, evk, out_rows: int):
+        """d = [3, l, n] tensor product (d0, d1, d2) -> rescaled relinearised ciphertext [2, out_rows, n]."""
+        out = self.empty(2, out_rows, d.shape[2])
+        _lib.check(self.lib.ckks_ks_relin_rescale(self.ctx, ks_plan, md_plan, d[2].data_ptr(),
+                                                  d[1].data_ptr(), d[0].data_ptr(), evk.data_ptr(),
+                                                  out[0].data_ptr(), out[1].data_ptr(), self.stream()))
+        return out
+
     def ks_accumulate(self, plan: int, ct_a, evk, first: bool):
         _lib.check(self.lib.ckks_ks_accumulate(self.ctx, plan, ct_a.data_ptr(), evk.data_ptr(),
                                                int(first), self.stream()))

@@ -131,6 +131,12 @@ def test_slotwise_semantics_rotation_conjugation_mult(env):
     assert np.abs(got - np.roll(z1, -5)).max() < tol
     sq = ck.rescale(ck.hmult(low, ck.mod_drop(ct2, 7), keys.relin), 2)
     assert np.abs(ck.decrypt_decode(sq, sk, p) - z1 * z2).max() < tol
+    # relinearisation and rescale merged into one ModDown
+    fused = ck.hmult_rescale(ct1, ct2, keys.relin, 2)
+    assert ck.level_of(fused) == p.l - 2 and fused.scale == pytest.approx(prod.scale)
+    assert np.abs(ck.decrypt_decode(fused, sk, p) - z1 * z2).max() < tol
+    fused_low = ck.hmult_rescale(low, ck.mod_drop(ct2, 7), keys.relin, 2)
+    assert np.abs(ck.decrypt_decode(fused_low, sk, p) - z1 * z2).max() < tol
     # hoisted rotations (one ModUp shared) decode to the same slots as plain HRot
     hoisted = ck.hrot_hoisted(low, [0, 1, 5], keys)
     for r in (0, 1, 5):
