@@ -24,14 +24,25 @@
 
 namespace ckks {
 
-// Output limbs are split over blockIdx.z in chunks of kOutChunk: one ciphertext has only
-// N = 2^16 columns, too few threads to fill 148 SMs unless the output walk is shared out
-// (the l_in pre-scale is recomputed per chunk: l_in Shoup products against l_in * kOutChunk MACs).
-constexpr int kOutChunk = 64;
+// Output limbs are split over blockIdx.z in chunks: one ciphertext has only N = 2^16 columns,
+// i.e. 256 CTAs per conversion, too few to fill 148 SMs x 8 resident CTAs unless the output
+// walk is shared out (the l_in pre-scale is recomputed per chunk: l_in Shoup products against
+// l_in * chunk MACs, so chunks stay >= 8 limbs).
+constexpr int kTargetCtas = 148 * 8;
+constexpr int kMinChunk = 8;
+
+static int out_chunk(size_t ctas_xy, int l_out_max) {
+    int z = (int)((kTargetCtas + ctas_xy - 1) / ctas_xy);
+    if (z < 1) z = 1;
+    int chunk = (l_out_max + z - 1) / z;
+    if (chunk < kMinChunk) chunk = kMinChunk;
+    if (chunk > l_out_max) chunk = l_out_max > 0 ? l_out_max : 1;
+    return chunk;
+}
 
 template <int LIN, int CPT>
 __global__ void __launch_bounds__(128)
-bconv_fast(BconvJobs jobs, const ModSlot* __restrict__ slots, size_t cols) {
+bconv_fast(BconvJobs jobs, const ModSlot* __restrict__ slots, size_t cols, int chunk) {
     constexpr int G = (LIN + 3) / 4;         // groups of four terms
     constexpr int LINP = 4 * G;
     extern __shared__ uint4 sm4[];
@@ -41,11 +52,13 @@ bconv_fast(BconvJobs jobs, const ModSlot* __restrict__ slots, size_t cols) {
     uint4* s_om = sm4 + (size_t)l_out * G;   // [l_out]     {q, qinv, out row, 2q}
     uint4* s_in = s_om + l_out;              // [LIN]       {q, inv_qhat, shoup(inv_qhat), -}
     uint32_t* s_tw = reinterpret_cast<uint32_t*>(s_t);
-    for (int idx = threadIdx.x; idx < l_out * LINP; idx += blockDim.x) {
+    // only this CTA's chunk of output rows is staged
+    const int i_lo = blockIdx.z * chunk, i_hi = min(l_out, i_lo + chunk);
+    for (int idx = i_lo * LINP + threadIdx.x; idx < i_hi * LINP; idx += blockDim.x) {
         const int i = idx / LINP, k = idx - i * LINP;
         s_tw[idx] = k < LIN ? job.tab.t_mont[i * LIN + k] : 0u;
     }
-    for (int i = threadIdx.x; i < l_out; i += blockDim.x) {
+    for (int i = i_lo + threadIdx.x; i < i_hi; i += blockDim.x) {
         const ModSlot& m = slots[job.tab.out_slot[i]];
         s_om[i] = make_uint4(m.q, m.qinv, job.out_row ? (uint32_t)job.out_row[i] : (uint32_t)i, 2u * m.q);
     }
@@ -73,7 +86,6 @@ bconv_fast(BconvJobs jobs, const ModSlot* __restrict__ slots, size_t cols) {
             for (int p = 0; p < CPT; ++p) y[p][k] = 0;
         }
     }
-    const int i_lo = blockIdx.z * kOutChunk, i_hi = min(l_out, i_lo + kOutChunk);
 #pragma unroll 2
     for (int i = i_lo; i < i_hi; ++i) {
         const uint4 om = s_om[i];
@@ -112,7 +124,7 @@ bconv_fast(BconvJobs jobs, const ModSlot* __restrict__ slots, size_t cols) {
 // through one REDC and yields the exact canonical residue.
 template <int LIN>
 __global__ void __launch_bounds__(128)
-bconv_f64(BconvJobs jobs, const ModSlot* __restrict__ slots, size_t cols) {
+bconv_f64(BconvJobs jobs, const ModSlot* __restrict__ slots, size_t cols, int chunk) {
     constexpr int LINP = (LIN + 1) / 2 * 2;
     extern __shared__ uint4 sm4[];
     const BconvJob& job = jobs.job[blockIdx.y];
@@ -147,7 +159,7 @@ bconv_f64(BconvJobs jobs, const ModSlot* __restrict__ slots, size_t cols) {
         }
     }
     const double seed = 4503599627370496.0;     // 2^52
-    const int i_lo = blockIdx.z * kOutChunk, i_hi = min(l_out, i_lo + kOutChunk);
+    const int i_lo = blockIdx.z * chunk, i_hi = min(l_out, i_lo + chunk);
     constexpr int U = 4;                        // outputs in flight: 2*U independent DFMA chains
     for (int i0 = i_lo; i0 < i_hi; i0 += U) {
         double a0[U], a1[U];
@@ -220,27 +232,31 @@ static int launch_fast(const BconvJobs& jobs, const ModSlot* slots, size_t cols,
     if (bconv_variant() == 1) {
         constexpr int LINP = (LIN + 1) / 2 * 2;
         const size_t sm = sizeof(double) * (size_t)l_out_max * LINP + sizeof(uint4) * ((size_t)l_out_max + LIN);
-        dim3 grid((unsigned)((cols + 127) / 128), jobs.count, (l_out_max + kOutChunk - 1) / kOutChunk);
+        const unsigned gx = (unsigned)((cols + 127) / 128);
+        const int chunk = out_chunk((size_t)gx * jobs.count, l_out_max);
+        dim3 grid(gx, jobs.count, (l_out_max + chunk - 1) / chunk);
         ProfScope ps("bconv", st, jobs_bytes(jobs, cols));
         if (sm > 48 * 1024)
             CK(cudaFuncSetAttribute(bconv_f64<LIN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-        bconv_f64<LIN><<<grid, 128, sm, st>>>(jobs, slots, cols);
+        bconv_f64<LIN><<<grid, 128, sm, st>>>(jobs, slots, cols, chunk);
         CK(cudaGetLastError());
         return CKKS_OK;
     }
     constexpr int G = (LIN + 3) / 4;
     const size_t sm = sizeof(uint4) * ((size_t)l_out_max * G + l_out_max + LIN);
     const size_t work = pairs ? cols / 2 : cols;
-    dim3 grid((unsigned)((work + 127) / 128), jobs.count, (l_out_max + kOutChunk - 1) / kOutChunk);
+    const unsigned gx = (unsigned)((work + 127) / 128);
+    const int chunk = out_chunk((size_t)gx * jobs.count, l_out_max);
+    dim3 grid(gx, jobs.count, (l_out_max + chunk - 1) / chunk);
     ProfScope ps("bconv", st, jobs_bytes(jobs, cols));
     if (pairs) {
         if (sm > 48 * 1024)
             CK(cudaFuncSetAttribute(bconv_fast<LIN, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-        bconv_fast<LIN, 2><<<grid, 128, sm, st>>>(jobs, slots, cols);
+        bconv_fast<LIN, 2><<<grid, 128, sm, st>>>(jobs, slots, cols, chunk);
     } else {
         if (sm > 48 * 1024)
             CK(cudaFuncSetAttribute(bconv_fast<LIN, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-        bconv_fast<LIN, 1><<<grid, 128, sm, st>>>(jobs, slots, cols);
+        bconv_fast<LIN, 1><<<grid, 128, sm, st>>>(jobs, slots, cols, chunk);
     }
     CK(cudaGetLastError());
     return CKKS_OK;

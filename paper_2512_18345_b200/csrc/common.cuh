@@ -91,10 +91,20 @@ __device__ __forceinline__ uint32_t mul_mod(uint32_t a, uint32_t b, const ModSlo
 
 // ---- memory helpers -------------------------------------------------------------
 
-__device__ __forceinline__ uint4 ld_stream(const uint4* p) {
+// Streaming loads for data read exactly once per kernel (switching keys, encoded
+// plaintext diagonals): no L1 allocation and an L2 evict-first policy, so that the
+// ~8 GB a bootstrap streams do not push the working set the next kernel re-reads
+// (raised digits, accumulators, twiddles) out of the 126 MB L2.
+__device__ __forceinline__ uint64_t l2_evict_first_policy() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+
+__device__ __forceinline__ uint4 ld_stream(const uint4* p, uint64_t pol) {
     uint4 v;
-    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
-                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p), "l"(pol));
     return v;
 }
 

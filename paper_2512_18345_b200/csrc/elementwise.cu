@@ -229,6 +229,7 @@ fused_terms_kernel(FusedTerms terms, uint4* out, const int32_t* __restrict__ row
     const ModSlot m = slots[row_slot[row]];
     const size_t half = (size_t)rows * cols4;
     const size_t stride = (size_t)gridDim.x * blockDim.x;
+    const uint64_t pol = l2_evict_first_policy();
     for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < cols4; i += stride) {
         const size_t at = row * cols4 + i;
         uint64_t sa[4] = {0, 0, 0, 0}, sb[4] = {0, 0, 0, 0};
@@ -238,7 +239,7 @@ fused_terms_kernel(FusedTerms terms, uint4* out, const int32_t* __restrict__ row
             const uint4* x = reinterpret_cast<const uint4*>(terms.x[t]);
             const uint4 xa = x[at], xb = x[half + at];
             if (terms.p[t]) {
-                const uint4 pv = reinterpret_cast<const uint4*>(terms.p[t])[at];
+                const uint4 pv = ld_stream(reinterpret_cast<const uint4*>(terms.p[t]) + at, pol);
                 sa[0] += (uint64_t)xa.x * pv.x; sa[1] += (uint64_t)xa.y * pv.y;
                 sa[2] += (uint64_t)xa.z * pv.z; sa[3] += (uint64_t)xa.w * pv.w;
                 sb[0] += (uint64_t)xb.x * pv.x; sb[1] += (uint64_t)xb.y * pv.y;

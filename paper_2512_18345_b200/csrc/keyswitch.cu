@@ -25,7 +25,10 @@ __device__ __forceinline__ uint32_t galois_src(uint32_t t, uint32_t k, uint32_t 
     return __brev((e - 1) >> 1) >> (32 - lg);
 }
 
-template <bool VEC>
+// BETA > 0: digit count known at compile time -- the loop is unrolled and all 3 * BETA
+// 16-byte loads of a thread are issued before the first product, which is what keeps
+// enough bytes in flight per SM to stream the key at HBM speed.  BETA = 0: runtime count.
+template <bool VEC, int BETA>
 __global__ void __launch_bounds__(256)
 inner_product_kernel(InnerProductArgs p, const ModSlot* __restrict__ slots) {
     const int row = p.row_lo + blockIdx.y;
@@ -36,51 +39,77 @@ inner_product_kernel(InnerProductArgs p, const ModSlot* __restrict__ slots) {
     constexpr int W = VEC ? 4 : 1;
     const size_t i = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) * W;
     if (i >= n) return;
-    uint64_t sa[W], sb[W];
+    const int beta = BETA > 0 ? BETA : p.beta;
+    const uint64_t pol = l2_evict_first_policy();
     uint32_t ra[W], rb[W];
 #pragma unroll
-    for (int w = 0; w < W; ++w) { sa[w] = sb[w] = 0; ra[w] = rb[w] = 0; }
-    for (int t = 0; t < p.beta; ++t) {
-        const uint32_t* dsrc = (p.carry && t == digit_of_row)
-                                   ? p.carry + (size_t)row * n
-                                   : p.raised + ((size_t)t * p.ext + row) * n;
-        const uint32_t* ka = p.evk + (((size_t)t * 2 + 0) * p.evk_ext + erow) * n;
-        const uint32_t* kb = p.evk + (((size_t)t * 2 + 1) * p.evk_ext + erow) * n;
-        uint32_t d[W], xa[W], xb[W];
-        if (VEC && p.galois) {
-            // hoisted rotation: the raised digit is read through the automorphism
-            // (sigma_k commutes with ModUp up to a multiple of the digit modulus)
+    for (int w = 0; w < W; ++w) ra[w] = rb[w] = 0;
+    uint32_t gsrc[W];
+    if (p.galois) {
 #pragma unroll
-            for (int w = 0; w < W; ++w) d[w] = dsrc[galois_src((uint32_t)i + w, p.galois, p.n, p.lg)];
-            const uint4 av = ld_stream(reinterpret_cast<const uint4*>(ka + i));
-            const uint4 bv = ld_stream(reinterpret_cast<const uint4*>(kb + i));
-            xa[0] = av.x; xa[W > 1 ? 1 : 0] = av.y; xa[W > 2 ? 2 : 0] = av.z; xa[W > 3 ? 3 : 0] = av.w;
-            xb[0] = bv.x; xb[W > 1 ? 1 : 0] = bv.y; xb[W > 2 ? 2 : 0] = bv.z; xb[W > 3 ? 3 : 0] = bv.w;
-        } else if (VEC) {
-            const uint4 dv = *reinterpret_cast<const uint4*>(dsrc + i);
-            const uint4 av = ld_stream(reinterpret_cast<const uint4*>(ka + i));
-            const uint4 bv = ld_stream(reinterpret_cast<const uint4*>(kb + i));
-            d[0] = dv.x; d[W > 1 ? 1 : 0] = dv.y; d[W > 2 ? 2 : 0] = dv.z; d[W > 3 ? 3 : 0] = dv.w;
-            xa[0] = av.x; xa[W > 1 ? 1 : 0] = av.y; xa[W > 2 ? 2 : 0] = av.z; xa[W > 3 ? 3 : 0] = av.w;
-            xb[0] = bv.x; xb[W > 1 ? 1 : 0] = bv.y; xb[W > 2 ? 2 : 0] = bv.z; xb[W > 3 ? 3 : 0] = bv.w;
-        } else {
-            d[0] = p.galois ? dsrc[galois_src((uint32_t)i, p.galois, p.n, p.lg)] : dsrc[i];
-            xa[0] = ka[i]; xb[0] = kb[i];
-        }
+        for (int w = 0; w < W; ++w) gsrc[w] = galois_src((uint32_t)i + w, p.galois, p.n, p.lg);
+    }
+    constexpr int CH = BETA > 0 ? BETA : 4;      // digits per 64-bit accumulation chunk (four 62-bit products fit)
+    for (int t0 = 0; t0 < beta; t0 += CH) {
+        uint32_t d[CH][W], xa[CH][W], xb[CH][W];
 #pragma unroll
-        for (int w = 0; w < W; ++w) {
-            sa[w] = mad64(d[w], xa[w], sa[w]);
-            sb[w] = mad64(d[w], xb[w], sb[w]);
+        for (int c = 0; c < CH; ++c) {
+            const int t = t0 + c;
+            if (BETA == 0 && t >= beta) {
+#pragma unroll
+                for (int w = 0; w < W; ++w) d[c][w] = xa[c][w] = xb[c][w] = 0;
+                continue;
+            }
+            const uint32_t* dsrc = (p.carry && t == digit_of_row)
+                                       ? p.carry + (size_t)row * n
+                                       : p.raised + ((size_t)t * p.ext + row) * n;
+            const uint32_t* ka = p.evk + (((size_t)t * 2 + 0) * p.evk_ext + erow) * n;
+            const uint32_t* kb = p.evk + (((size_t)t * 2 + 1) * p.evk_ext + erow) * n;
+            if (VEC) {
+                const uint4 av = ld_stream(reinterpret_cast<const uint4*>(ka + i), pol);
+                const uint4 bv = ld_stream(reinterpret_cast<const uint4*>(kb + i), pol);
+                xa[c][0] = av.x; xa[c][W > 1 ? 1 : 0] = av.y; xa[c][W > 2 ? 2 : 0] = av.z; xa[c][W > 3 ? 3 : 0] = av.w;
+                xb[c][0] = bv.x; xb[c][W > 1 ? 1 : 0] = bv.y; xb[c][W > 2 ? 2 : 0] = bv.z; xb[c][W > 3 ? 3 : 0] = bv.w;
+                if (p.galois) {
+                    // hoisted rotation: the raised digit is read through the automorphism
+                    // (sigma_k commutes with ModUp up to a multiple of the digit modulus)
+#pragma unroll
+                    for (int w = 0; w < W; ++w) d[c][w] = dsrc[gsrc[w]];
+                } else {
+                    const uint4 dv = *reinterpret_cast<const uint4*>(dsrc + i);
+                    d[c][0] = dv.x; d[c][W > 1 ? 1 : 0] = dv.y; d[c][W > 2 ? 2 : 0] = dv.z; d[c][W > 3 ? 3 : 0] = dv.w;
+                }
+            } else {
+                d[c][0] = p.galois ? dsrc[gsrc[0]] : dsrc[i];
+                xa[c][0] = ka[i]; xb[c][0] = kb[i];
+            }
         }
-        // four products below q^2 < 2^62 fit in 64 bits; fold before a fifth
-        if ((t & 3) == 3 || t == p.beta - 1 || !m.fast) {
+        if (m.fast) {
+            uint64_t sa[W], sb[W];
+#pragma unroll
+            for (int w = 0; w < W; ++w) { sa[w] = sb[w] = 0; }
+#pragma unroll
+            for (int c = 0; c < CH; ++c) {
+#pragma unroll
+                for (int w = 0; w < W; ++w) {
+                    sa[w] = mad64(d[c][w], xa[c][w], sa[w]);
+                    sb[w] = mad64(d[c][w], xb[c][w], sb[w]);
+                }
+            }
 #pragma unroll
             for (int w = 0; w < W; ++w) {
-                ra[w] = m.q >> 31 ? (uint32_t)(((uint64_t)ra[w] + reduce64(sa[w], m)) % m.q)
-                                  : add_mod(ra[w], reduce64(sa[w], m), m.q);
-                rb[w] = m.q >> 31 ? (uint32_t)(((uint64_t)rb[w] + reduce64(sb[w], m)) % m.q)
-                                  : add_mod(rb[w], reduce64(sb[w], m), m.q);
-                sa[w] = sb[w] = 0;
+                ra[w] = add_mod(ra[w], reduce64(sa[w], m), m.q);
+                rb[w] = add_mod(rb[w], reduce64(sb[w], m), m.q);
+            }
+        } else {
+            // any modulus below 2^32: reduce every product
+#pragma unroll
+            for (int c = 0; c < CH; ++c) {
+#pragma unroll
+                for (int w = 0; w < W; ++w) {
+                    ra[w] = (uint32_t)(((uint64_t)ra[w] + (uint64_t)d[c][w] * xa[c][w] % m.q) % m.q);
+                    rb[w] = (uint32_t)(((uint64_t)rb[w] + (uint64_t)d[c][w] * xb[c][w] % m.q) % m.q);
+                }
             }
         }
     }
@@ -91,7 +120,7 @@ inner_product_kernel(InnerProductArgs p, const ModSlot* __restrict__ slots) {
         const uint32_t* bsrc = p.lift_b + (size_t)row * n;
 #pragma unroll
         for (int w = 0; w < W; ++w) {
-            const uint32_t bv = p.galois ? bsrc[galois_src((uint32_t)i + w, p.galois, p.n, p.lg)] : bsrc[i + w];
+            const uint32_t bv = p.galois ? bsrc[gsrc[w]] : bsrc[i + w];
             rb[w] = add_mod(rb[w], shoup_mul(bv, pm, pms, m.q), m.q);
         }
     }
@@ -117,6 +146,12 @@ inner_product_kernel(InnerProductArgs p, const ModSlot* __restrict__ slots) {
     }
 }
 
+template <int BETA>
+static void inner_product_dispatch(const InnerProductArgs& a, const ModSlot* slots, dim3 grid, bool vec, cudaStream_t st) {
+    if (vec) inner_product_kernel<true, BETA><<<grid, 256, 0, st>>>(a, slots);
+    else inner_product_kernel<false, BETA><<<grid, 256, 0, st>>>(a, slots);
+}
+
 int inner_product_launch(const InnerProductArgs& a, const ModSlot* slots, cudaStream_t st) {
     const int rows = a.row_hi - a.row_lo;
     if (rows <= 0) return CKKS_OK;
@@ -124,8 +159,13 @@ int inner_product_launch(const InnerProductArgs& a, const ModSlot* slots, cudaSt
     const size_t work = vec ? a.n / 4 : a.n;
     dim3 grid((unsigned)((work + 255) / 256), rows);
     ProfScope ps("inner_product", st, 4.0 * a.n * rows * (3.0 * a.beta + 2.0));
-    if (vec) inner_product_kernel<true><<<grid, 256, 0, st>>>(a, slots);
-    else inner_product_kernel<false><<<grid, 256, 0, st>>>(a, slots);
+    switch (a.beta) {
+        case 1: inner_product_dispatch<1>(a, slots, grid, vec, st); break;
+        case 2: inner_product_dispatch<2>(a, slots, grid, vec, st); break;
+        case 3: inner_product_dispatch<3>(a, slots, grid, vec, st); break;
+        case 4: inner_product_dispatch<4>(a, slots, grid, vec, st); break;
+        default: inner_product_dispatch<0>(a, slots, grid, vec, st); break;
+    }
     CK(cudaGetLastError());
     return CKKS_OK;
 }

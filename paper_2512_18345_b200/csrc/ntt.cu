@@ -191,23 +191,55 @@ ntt16_inv_strided(const uint32_t* in, uint32_t* out, const int32_t* __restrict__
 // blk*272 + e + (e >> 4).
 //
 // Twiddles.  The four stages next to the data (forward 12..15, inverse 0..3)
-// use N/2 + N/4 + N/8 + N/16 distinct twiddles per limb -- as many bytes as the
-// limb itself if read from the table.  Their slot index is
-// [1][B:8][e:4][g:s] (block, thread, local group), and psi^bitrev(slot)
-// factors as X_s[B] * YZ_s[g][e]:
-//     X_s[B]     = table[((256 + B) * 16) << s]             (4 per block)
-//     YZ_s[g][e] = psi^(2^(12-s) brev4(e) + 2^(16-s) brev_s(g))   (240 per modulus)
-// so those butterflies do two chained Shoup multiplications and read no
-// per-butterfly table entry.  The other four stages need 15 twiddles per block,
-// staged through shared memory at kernel start.
+// use N/2 + N/4 + N/8 + N/16 distinct twiddles per limb.  For the 16 consecutive
+// elements a thread holds in that pass they are the table entries
+//     [idx0], [2 idx0 .. +2), [4 idx0 .. +4), [8 idx0 .. +8),   idx0 = (256 + B) * 16 + e,
+// i.e. 15 Shoup pairs = 120 B in five aligned vector loads (8 + 16 + 32 + 64 B),
+// consecutive threads reading consecutive addresses.  They are fetched with the
+// data at kernel start.  (An earlier version rebuilt them on the fly from a
+// 240-entry split table with a second Shoup product per butterfly; on B200 the
+// integer multiplier -- the fmaheavy pipe -- is the busiest unit of this kernel
+// while L2 has headroom, so table reads win.)  The other four stages need 15
+// twiddles per block, staged through shared memory by the block's own lanes.
 // ---------------------------------------------------------------------------------
-__device__ __forceinline__ int yz_index(int s, int gi, int e) { return 16 * ((1 << s) - 1) + gi * 16 + e; }
+struct Tw15 {
+    uint2 t1, t2[2], t4[4], t8[8];
+};
+
+__device__ __forceinline__ void ld256(const void* p, uint32_t (&r)[8]) {
+    asm volatile("ld.global.nc.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+                 : "l"(p));
+}
+
+__device__ __forceinline__ void st256(void* p, const uint32_t (&r)[8]) {
+    asm volatile("st.global.v8.u32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};"
+                 :: "l"(p), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
+                 : "memory");
+}
+
+__device__ __forceinline__ void load_tw15(const uint2* __restrict__ tab, uint32_t idx0, Tw15& t) {
+    t.t1 = __ldg(tab + idx0);
+    const uint4 a = __ldg(reinterpret_cast<const uint4*>(tab + 2 * idx0));
+    t.t2[0] = make_uint2(a.x, a.y);
+    t.t2[1] = make_uint2(a.z, a.w);
+    uint32_t r[8];
+    ld256(tab + 4 * idx0, r);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) t.t4[j] = make_uint2(r[2 * j], r[2 * j + 1]);
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        ld256(tab + 8 * idx0 + 4 * h, r);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) t.t8[4 * h + j] = make_uint2(r[2 * j], r[2 * j + 1]);
+    }
+}
 
 __global__ void __launch_bounds__(256)
 ntt16_fwd_contig(const uint32_t* in, uint32_t* out, const int32_t* __restrict__ row_slot,
                  const ModSlot* __restrict__ slots, RowMap rm) {
     __shared__ uint32_t tile[16 * 272];
-    __shared__ uint2 s_blk[16][20];      // per block: 15 twiddles of stages 8..11, then X_0..X_3
+    __shared__ uint2 s_blk[16][16];      // per block: the 15 twiddles of stages 8..11
     const int tid = threadIdx.x;
     const int e = tid & 15, blk = tid >> 4;
     const ModSlot& m = slots[row_slot[blockIdx.y]];
@@ -215,20 +247,14 @@ ntt16_fwd_contig(const uint32_t* in, uint32_t* out, const int32_t* __restrict__ 
     const uint32_t B = blockIdx.x * 16 + blk;          // 256-element block index within the limb
     const uint32_t* src = in + rm.in_row(blockIdx.y) * kN16 + B * 256;
     const uint2* __restrict__ fwd = m.fwd;
-    const uint2* __restrict__ yz = m.otf_fwd;
-    // the 16 threads of a 256-block stage that block's 19 table entries themselves: the whole
+    // the 16 threads of a 256-block stage that block's table entries themselves: the whole
     // kernel then only needs warp-level synchronisation (a block's exchange is half a warp)
-    for (int j = e; j < 19; j += 16) {
-        const uint32_t Bb = 256 + B;
-        uint32_t idx;
-        if (j < 15) {
-            const int st = 31 - __clz(j + 1);          // local stage, group = j + 1 - 2^st
-            idx = (Bb << st) + (j + 1 - (1 << st));
-        } else {
-            idx = (Bb * 16) << (j - 15);
-        }
-        s_blk[blk][j] = fwd[idx];
+    if (e < 15) {
+        const int st = 31 - __clz(e + 1);              // local stage, group = e + 1 - 2^st
+        s_blk[blk][e] = fwd[((256 + B) << st) + (e + 1 - (1 << st))];
     }
+    Tw15 tw;
+    load_tw15(fwd, (256 + B) * 16 + e, tw);
     uint32_t v[16];
 #pragma unroll
     for (int k = 0; k < 16; ++k) v[k] = src[e + 16 * k];
@@ -240,62 +266,49 @@ ntt16_fwd_contig(const uint32_t* in, uint32_t* out, const int32_t* __restrict__ 
     __syncwarp();
 #pragma unroll
     for (int k = 0; k < 16; ++k) v[k] = tile[blk * 272 + 17 * e + k];
-    // global stages 12..15: elements 16e + k, twiddle = X_s[B] * YZ_s[g][e]
-    uint2 X[4];
+    // global stages 12..15: elements 16e + k, slot = ((256 + B) * 16 + e) * 2^s + group
+    ct16(v, q, TW_MUL(s == 0 ? tw.t1 : (s == 1 ? tw.t2[gi & 1] : (s == 2 ? tw.t4[gi & 3] : tw.t8[gi & 7]))));
+    uint32_t* dst = out + rm.out_row(blockIdx.y) * kN16 + B * 256 + 16 * e;
 #pragma unroll
-    for (int st = 0; st < 4; ++st) X[st] = s_blk[blk][15 + st];
-    ct16(v, q, [&](int s, int gi, uint32_t y) {
-        const uint2 yzv = __ldg(&yz[yz_index(s, gi, e)]);
-        return shoup_mul(shoup_lazy(y, yzv.x, yzv.y, q), X[s].x, X[s].y, q);
-    });
-    uint4* dst = reinterpret_cast<uint4*>(out + rm.out_row(blockIdx.y) * kN16 + B * 256 + 16 * e);
+    for (int h = 0; h < 2; ++h) {
+        uint32_t r[8];
 #pragma unroll
-    for (int k = 0; k < 4; ++k)
-        dst[k] = make_uint4(csub(v[4 * k], q), csub(v[4 * k + 1], q), csub(v[4 * k + 2], q),
-                            csub(v[4 * k + 3], q));
+        for (int k = 0; k < 8; ++k) r[k] = csub(v[8 * h + k], q);
+        st256(dst + 8 * h, r);
+    }
 }
 
 __global__ void __launch_bounds__(256)
 ntt16_inv_contig(const uint32_t* in, uint32_t* out, const int32_t* __restrict__ row_slot,
                  const ModSlot* __restrict__ slots, RowMap rm) {
     __shared__ uint32_t tile[16 * 272];
-    __shared__ uint2 s_blk[16][20];      // per block: 15 twiddles of stages 4..7, then X_0..X_3
+    __shared__ uint2 s_blk[16][16];      // per block: the 15 twiddles of stages 4..7, laid out 8 | 4 | 2 | 1
     const int tid = threadIdx.x;
     const int e = tid & 15, blk = tid >> 4;
     const ModSlot& m = slots[row_slot[blockIdx.y]];
     const uint32_t q = m.q;
     const uint32_t B = blockIdx.x * 16 + blk;
-    const uint4* src = reinterpret_cast<const uint4*>(in + rm.in_row(blockIdx.y) * kN16 + B * 256 + 16 * e);
+    const uint32_t* src = in + rm.in_row(blockIdx.y) * kN16 + B * 256 + 16 * e;
     const uint2* __restrict__ inv = m.inv;
-    const uint2* __restrict__ yz = m.otf_inv;
-    for (int j = e; j < 19; j += 16) {
-        const uint32_t Bb = 256 + B;
-        uint32_t idx;
-        if (j < 15) {
-            // stage s of 4..7 has (8 >> s) groups; entries laid out 8 | 4 | 2 | 1
-            const int st = j < 8 ? 0 : (j < 12 ? 1 : (j < 14 ? 2 : 3));
-            const int off = st == 0 ? 0 : (st == 1 ? 8 : (st == 2 ? 12 : 14));
-            idx = Bb * (8 >> st) + (j - off);
-        } else {
-            idx = (Bb * 16) << (j - 15);
-        }
-        s_blk[blk][j] = inv[idx];
+    if (e < 15) {
+        // stage s of 4..7 has (8 >> s) groups
+        const int st = e < 8 ? 0 : (e < 12 ? 1 : (e < 14 ? 2 : 3));
+        const int off = st == 0 ? 0 : (st == 1 ? 8 : (st == 2 ? 12 : 14));
+        s_blk[blk][e] = inv[(256 + B) * (8 >> st) + (e - off)];
     }
+    Tw15 tw;
+    load_tw15(inv, (256 + B) * 16 + e, tw);
     uint32_t v[16];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-        const uint4 u = src[k];
-        v[4 * k] = u.x; v[4 * k + 1] = u.y; v[4 * k + 2] = u.z; v[4 * k + 3] = u.w;
+    for (int h = 0; h < 2; ++h) {
+        uint32_t r[8];
+        ld256(src + 8 * h, r);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) v[8 * h + k] = r[k];
     }
     __syncwarp();
-    // global stages 0..3 on elements 16e + k: slot = [1][B][e][g] with (3 - s) group bits
-    uint2 X[4];
-#pragma unroll
-    for (int st = 0; st < 4; ++st) X[st] = s_blk[blk][15 + st];
-    gs16(v, q, [&](int s, int gi, uint32_t d) {
-        const uint2 yzv = __ldg(&yz[yz_index(3 - s, gi, e)]);
-        return shoup_mul(shoup_lazy(d, yzv.x, yzv.y, q), X[3 - s].x, X[3 - s].y, q);
-    });
+    // global stages 0..3 on elements 16e + k: slot = ((256 + B) * 16 + e) * (8 >> s) + group
+    gs16(v, q, TW_MUL(s == 0 ? tw.t8[gi & 7] : (s == 1 ? tw.t4[gi & 3] : (s == 2 ? tw.t2[gi & 1] : tw.t1))));
 #pragma unroll
     for (int k = 0; k < 16; ++k) tile[blk * 272 + 17 * e + k] = v[k];
     __syncwarp();
