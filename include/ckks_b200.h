@@ -130,6 +130,16 @@ int ckks_pmult_accumulate(ckks_ctx* ctx, const uint32_t* x, const uint32_t* p, u
 int ckks_fused_terms(ckks_ctx* ctx, int count, const uint32_t* const* x, const uint32_t* const* p,
                      uint32_t* out, const int32_t* row_slot, int rows, size_t cols, void* stream);
 
+/* All giant-step inner sums of a BSGS linear transform in one pass:
+ * out[g] = sum_b x[b] (.) p[g * nb + b] for g < ng <= 8, b < nb <= 16; x[b] and out[g]
+ * are [2][rows][cols] ciphertexts, p[.] [rows][cols] plaintexts or NULL (diagonal
+ * absent: `zero`, a DEVICE [rows][cols] matrix of zeros, is read in its place, so it may
+ * be NULL only when no p[.] is); pointer arrays are HOST arrays.  Same arithmetic as ng
+ * calls of ckks_fused_terms, but every x[b] is read once. */
+int ckks_fused_terms_multi(ckks_ctx* ctx, int nb, int ng, const uint32_t* const* x,
+                           const uint32_t* const* p, const uint32_t* zero, uint32_t* const* out,
+                           const int32_t* row_slot, int rows, size_t cols, void* stream);
+
 /* Tensor product (front of HMult): x, y [2][rows][cols] -> out [3][rows][cols] =
  * (b1*b2, a1*b2 + a2*b1, a1*a2). */
 int ckks_tensor(ckks_ctx* ctx, const uint32_t* x, const uint32_t* y, uint32_t* out,
@@ -222,8 +232,9 @@ int ckks_ks_relin_rescale(ckks_ctx* ctx, int32_t ks_plan, int32_t md_plan, const
 /* Key switches whose results are summed (giant steps of a BSGS linear transform) can
  * share one ModDown: ckks_ks_accumulate runs stages 1-2 of keyswitch.py:444-453 for
  * (ct_a, evk) and adds the Q||P accumulator into the current lane's workspace (first !=
- * 0 overwrites); ckks_ks_finish sums the accumulators of lanes [0, lanes_used), runs
- * stage 3 once on lane 0 and adds fold_a / fold_b (may be NULL) to the two halves.
+ * 0 overwrites); ckks_ks_finish sums the accumulators of lanes [c, c + lanes_used), c the
+ * currently selected lane (0 unless the caller itself runs inside a lane group), runs
+ * stage 3 once on lane c and adds fold_a / fold_b (may be NULL) to the two halves.
  * ModDown is linear up to its rounding, so this equals the sum of separate key switches
  * up to key-switch noise. */
 int ckks_ks_accumulate(ckks_ctx* ctx, int32_t plan, const uint32_t* ct_a, const uint32_t* evk,

@@ -197,9 +197,18 @@ class LinearTransform:
             x = ckks.ct_tensor(ct)
             acc[0] = torch.cat([x, torch.zeros((2, alpha, n_ring), dtype=x.dtype, device=x.device)], dim=1)
 
+        # every giant step's inner sum over Q||P in one pass (each baby step read once) ...
+        babies = sorted(acc)
+        giants = self.giants
+        qps = {}
+        for g0 in range(0, len(giants), 8):
+            chunk = giants[g0:g0 + 8]
+            table = [[self.table[g][b].poly.data if b in self.table[g] else None for b in babies] for g in chunk]
+            qps.update(zip(chunk, eng.fused_terms_multi([acc[b] for b in babies], table, ext_slots)))
+
         def inner_sum(g):
-            row = self.table[g]
-            qp = eng.fused_terms([acc[b] for b in row], [pt.poly.data for pt in row.values()], ext_slots)
+            # ... then one ModDown per giant step
+            qp = qps[g]
             return eng.ks_stage3(plan, qp[0, :level], qp[1, :level], qp[0, level:], qp[1, level:])
 
         return inner_sum
@@ -250,7 +259,7 @@ class LinearTransform:
                 return rot
 
             rots = eng.fork([(lambda lane, nth, g=g: giant(lane, nth, g)) for g in moving], with_lane=True)
-            lanes_used = min(getattr(eng, "lanes", 1), len(moving))
+            lanes_used = min(eng.lane_count(), len(moving))
             terms = list(rots) + ([base] if base is not None else [])
             b_sum = eng.fused_terms(terms, [None] * len(terms), slots) if len(terms) > 1 else terms[0]
             out_t = eng.ks_finish(plan, lanes_used, None if base is None else base[0], b_sum[1],
@@ -381,6 +390,9 @@ class Bootstrapper:
 
     def _exp_taylor(self, x, coef):
         """sum_k coef[k] x^k by a balanced power tree (depth ceil(log2(degree+1)))."""
+        from .engine import get_engine
+
+        eng = get_engine()
         d = len(coef) - 1
         depth = math.ceil(math.log2(d + 1))
         powers = {1: x}
@@ -409,10 +421,15 @@ class Bootstrapper:
             lvl_in = want_level + 2
             xp_d = ckks.mod_drop(xp, lvl_in) if ckks.level_of(xp) > lvl_in else xp
             dropped = math.prod(m.q for m in self.params.q_basis[want_level:lvl_in])
-            r = realise(right, want_scale * dropped / xp_d.scale, lvl_in)
-            prod = self._mul(r, xp_d)
-            prod = ckks.Ciphertext(prod.a, prod.b, want_scale)
-            return ckks.add(prod, realise(left, want_scale, want_level))
+
+            def high():
+                r = realise(right, want_scale * dropped / xp_d.scale, lvl_in)
+                prod = self._mul(r, xp_d)
+                return ckks.Ciphertext(prod.a, prod.b, want_scale)
+
+            # the two halves are independent: spread them over the lanes this branch owns
+            prod, low = eng.fork([high, lambda: realise(left, want_scale, want_level)])
+            return ckks.add(prod, low)
 
         tree = build(0, 1 << depth)
         out_level = ckks.level_of(x) - 2 * depth

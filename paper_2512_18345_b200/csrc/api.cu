@@ -461,6 +461,29 @@ int ckks_fused_terms(ckks_ctx* ctx, int count, const uint32_t* const* x, const u
     return fused_terms_launch(t, out, row_slot, ctx->d_slots, rows, cols, (cudaStream_t)stream);
 }
 
+int ckks_fused_terms_multi(ckks_ctx* ctx, int nb, int ng, const uint32_t* const* x,
+                           const uint32_t* const* p, const uint32_t* zero, uint32_t* const* out,
+                           const int32_t* row_slot, int rows, size_t cols, void* stream) {
+    CKS(check_ctx(ctx));
+    if (nb < 1 || nb > kMaxTerms || ng < 1 || ng > kMaxGiants || !x || !p || !out) {
+        set_last_error("fused_terms_multi: %d terms x %d outputs out of range [1, %d] x [1, %d]", nb, ng, kMaxTerms, kMaxGiants);
+        return CKKS_ERR_ARG;
+    }
+    FusedMulti a{};
+    a.nb = nb;
+    a.ng = ng;
+    for (int b = 0; b < nb; ++b) a.x[b] = x[b];
+    for (int g = 0; g < ng; ++g) {
+        a.out[g] = out[g];
+        for (int b = 0; b < nb; ++b) {
+            a.p[g][b] = p[(size_t)g * nb + b] ? p[(size_t)g * nb + b] : zero;
+            if (!a.p[g][b]) { set_last_error("fused_terms_multi: absent diagonal (%d, %d) but no zero plaintext given", g, b); return CKKS_ERR_ARG; }
+        }
+    }
+    a.zero = zero;
+    return fused_terms_multi_launch(a, row_slot, ctx->d_slots, rows, cols, (cudaStream_t)stream);
+}
+
 int ckks_tensor(ckks_ctx* ctx, const uint32_t* x, const uint32_t* y, uint32_t* out,
                 const int32_t* row_slot, int rows, size_t cols, void* stream) {
     CKS(check_ctx(ctx));
@@ -733,13 +756,15 @@ static int stage3_core(ckks_ctx* ctx, KsPlan* pl, const uint32_t* q_a, const uin
         j.out_row = nullptr;
     }
     CKS(bconv_launch_jobs(jobs, ctx->d_slots, n, st));
-    CKS(ntt_launch(ws_conv, ws_conv, pl->d_s3_q_slot, ctx->d_slots, id, 2 * pl->l, pl->n, 0, st));
     ModDownEpilogueArgs e{};
     e.xq_a = q_a; e.xq_b = q_b; e.conv = ws_conv; e.fold_a = fold_a; e.fold_b = fold_b;
     e.out_a = out_a; e.out_b = out_b;
     e.q_slot = pl->d_q_slot; e.pinv = pl->d_pinv; e.pinv_s = pl->d_pinv_s;
     e.l = pl->l; e.n = pl->n;
     e.galois = galois; e.lg = log2u(pl->n);
+    if (ntt_can_fuse_moddown(pl->n))       // epilogue applied inside the transform's last kernel
+        return ntt_launch(ws_conv, ws_conv, pl->d_s3_q_slot, ctx->d_slots, id, 2 * pl->l, pl->n, 0, st, &e);
+    CKS(ntt_launch(ws_conv, ws_conv, pl->d_s3_q_slot, ctx->d_slots, id, 2 * pl->l, pl->n, 0, st));
     return moddown_epilogue_launch(e, ctx->d_slots, st);
 }
 
@@ -894,13 +919,11 @@ int ckks_ks_accumulate(ckks_ctx* ctx, int32_t plan, const uint32_t* ct_a, const 
 
 int ckks_ks_finish(ckks_ctx* ctx, int32_t plan, int lanes_used, const uint32_t* fold_a,
                    const uint32_t* fold_b, uint32_t* out_a, uint32_t* out_b, void* stream) {
-    if (!ctx || lanes_used < 1 || lanes_used > ctx->lanes) { set_last_error("bad lane count %d", lanes_used); return CKKS_ERR_ARG; }
-    const int keep = ctx->lane;
-    ctx->lane = 0;
+    // the accumulators of lanes [current lane, current lane + lanes_used) are summed into the
+    // current lane's (the caller's home lane; 0 outside nested forks)
+    if (!ctx || lanes_used < 1 || ctx->lane + lanes_used > ctx->lanes) { set_last_error("bad lane count %d", lanes_used); return CKKS_ERR_ARG; }
     KsPlan* pl;
-    int rc = get_plan(ctx, plan, &pl);
-    ctx->lane = keep;
-    CKS(rc);
+    CKS(get_plan(ctx, plan, &pl));
     CKS(need_full_plan(pl));
     cudaStream_t st = (cudaStream_t)stream;
     const size_t n = pl->n;

@@ -89,6 +89,14 @@ __device__ __forceinline__ uint32_t mul_mod(uint32_t a, uint32_t b, const ModSlo
     return (uint32_t)(((uint64_t)a * b) % m.q);
 }
 
+// Source column of output column t under the evaluation-domain automorphism X -> X^k
+// (closed form of reference rns.py:268-292, SURVEY 8a'.4).
+__device__ __forceinline__ uint32_t galois_src(uint32_t t, uint32_t k, uint32_t n, uint32_t lg) {
+    const uint32_t u = __brev(t) >> (32 - lg);
+    const uint32_t e = ((2 * u + 1) * k) & (2 * n - 1);
+    return __brev((e - 1) >> 1) >> (32 - lg);
+}
+
 // ---- memory helpers -------------------------------------------------------------
 
 // Streaming loads for data read exactly once per kernel (switching keys, encoded
@@ -105,6 +113,13 @@ __device__ __forceinline__ uint4 ld_stream(const uint4* p, uint64_t pol) {
     uint4 v;
     asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
                  : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p), "l"(pol));
+    return v;
+}
+
+__device__ __forceinline__ uint2 ld_stream2(const uint2* p, uint64_t pol) {
+    uint2 v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.u32 {%0,%1}, [%2], %3;"
+                 : "=r"(v.x), "=r"(v.y) : "l"(p), "l"(pol));
     return v;
 }
 

@@ -277,6 +277,86 @@ int fused_terms_launch(const FusedTerms& terms, uint32_t* out, const int32_t* ro
     return CKKS_OK;
 }
 
+// All giant-step inner sums of a BSGS linear transform in one pass:
+//     out[g] = sum_b x[b] (.) p[g][b]          (absent diagonal: p[g][b] = a.zero, all zeros)
+// Every baby-step ciphertext x[b] is read once for all NG outputs instead of once per
+// giant step; only the plaintext diagonals (each used exactly once) scale with NG * NB.
+// Two columns per thread keep the NG * 2 * 2 64-bit accumulators in registers.
+template <int NG>
+__global__ void __launch_bounds__(256)
+fused_terms_multi_kernel(FusedMulti a, const int32_t* __restrict__ row_slot,
+                         const ModSlot* __restrict__ slots, int rows, size_t cols2) {
+    const size_t row = blockIdx.y;
+    const ModSlot m = slots[row_slot[row]];
+    const size_t half = (size_t)rows * cols2;
+    const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= cols2) return;
+    const size_t at = row * cols2 + i;
+    const uint64_t pol = l2_evict_first_policy();
+    uint64_t sa[NG][2], sb[NG][2];
+    uint32_t ra[NG][2], rb[NG][2];
+#pragma unroll
+    for (int g = 0; g < NG; ++g) {
+        sa[g][0] = sa[g][1] = sb[g][0] = sb[g][1] = 0;
+        ra[g][0] = ra[g][1] = rb[g][0] = rb[g][1] = 0;
+    }
+    for (int b0 = 0; b0 < a.nb; b0 += 4) {
+        // four 62-bit products fit a 64-bit accumulator: fold after every chunk of four terms
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            const int b = b0 + c;
+            if (b < a.nb) {
+                const uint2* x = reinterpret_cast<const uint2*>(a.x[b]);
+                const uint2 xa = x[at], xb = x[half + at];
+#pragma unroll
+                for (int g = 0; g < NG; ++g) {
+                    // absent diagonals point at a zero plaintext (host side): no branch, so the
+                    // loads of a chunk are all issued before the first product
+                    const uint2 pv = ld_stream2(reinterpret_cast<const uint2*>(a.p[g][b]) + at, pol);
+                    sa[g][0] += (uint64_t)xa.x * pv.x; sa[g][1] += (uint64_t)xa.y * pv.y;
+                    sb[g][0] += (uint64_t)xb.x * pv.x; sb[g][1] += (uint64_t)xb.y * pv.y;
+                }
+            }
+        }
+#pragma unroll
+        for (int g = 0; g < NG; ++g) {
+#pragma unroll
+            for (int k = 0; k < 2; ++k) {
+                ra[g][k] = add_mod(ra[g][k], reduce64(sa[g][k], m), m.q);
+                rb[g][k] = add_mod(rb[g][k], reduce64(sb[g][k], m), m.q);
+                sa[g][k] = sb[g][k] = 0;
+            }
+        }
+    }
+#pragma unroll
+    for (int g = 0; g < NG; ++g) {
+        uint2* o = reinterpret_cast<uint2*>(a.out[g]);
+        o[at] = make_uint2(ra[g][0], ra[g][1]);
+        o[half + at] = make_uint2(rb[g][0], rb[g][1]);
+    }
+}
+
+int fused_terms_multi_launch(const FusedMulti& a, const int32_t* row_slot, const ModSlot* slots,
+                             int rows, size_t cols, cudaStream_t st) {
+    if (rows <= 0 || cols == 0) return CKKS_OK;
+    if (cols % 2 || rows > 65535 || a.nb < 1 || a.nb > kMaxTerms || a.ng < 1 || a.ng > kMaxGiants) {
+        set_last_error("fused_terms_multi needs even cols, <= 65535 rows, <= %d terms, <= %d outputs", kMaxTerms, kMaxGiants);
+        return CKKS_ERR_UNSUPPORTED;
+    }
+    double limbs = 2.0 * a.nb + 2.0 * a.ng;
+    for (int g = 0; g < a.ng; ++g)
+        for (int b = 0; b < a.nb; ++b) limbs += a.p[g][b] != a.zero ? 1.0 : 0.0;
+    ProfScope ps("fused_terms", st, 4.0 * cols * rows * limbs);
+    dim3 grid((unsigned)((cols / 2 + 255) / 256), rows);
+    switch (a.ng) {
+#define MULTI_CASE(G) case G: fused_terms_multi_kernel<G><<<grid, 256, 0, st>>>(a, row_slot, slots, rows, cols / 2); break;
+        MULTI_CASE(1) MULTI_CASE(2) MULTI_CASE(3) MULTI_CASE(4) MULTI_CASE(5) MULTI_CASE(6) MULTI_CASE(7) MULTI_CASE(8)
+#undef MULTI_CASE
+    }
+    CK(cudaGetLastError());
+    return CKKS_OK;
+}
+
 // Tensor product of two ciphertexts in one pass (the front of HMult):
 // d0 = b1*b2, d1 = a1*b2 + a2*b1, d2 = a1*a2; x, y are [2][rows][n] (a then b),
 // out is [3][rows][n] (d0, d1, d2).

@@ -50,8 +50,13 @@ struct ProfScope {
 };
 
 // ntt.cu
+struct ModDownEpilogueArgs;
+// epi != null (forward, N = 2^16, rows = 2 l only): the last kernel applies the ModDown
+// epilogue to its registers and stores the key-switch result instead of the transform.
 int ntt_launch(const uint32_t* in, uint32_t* out, const int32_t* row_slot, const ModSlot* slots,
-               RowMap rm, int rows, uint32_t n, int inverse, cudaStream_t st);
+               RowMap rm, int rows, uint32_t n, int inverse, cudaStream_t st,
+               const ModDownEpilogueArgs* epi = nullptr);
+bool ntt_can_fuse_moddown(uint32_t n);
 int ntt_stages_launch(const uint32_t* in, uint32_t* out, const int32_t* row_slot,
                       const ModSlot* slots, int rows, uint32_t n, int inverse, uint32_t s_lo,
                       uint32_t s_hi, cudaStream_t st);
@@ -78,6 +83,16 @@ struct FusedTerms {
 };
 int fused_terms_launch(const FusedTerms& terms, uint32_t* out, const int32_t* row_slot,
                        const ModSlot* slots, int rows, size_t cols, cudaStream_t st);
+constexpr int kMaxGiants = 8;
+struct FusedMulti {
+    int nb, ng;
+    const uint32_t* x[kMaxTerms];               // baby-step ciphertexts [2][rows][n]
+    const uint32_t* p[kMaxGiants][kMaxTerms];   // plaintext diagonal of (giant g, baby b), or `zero`
+    const uint32_t* zero;                       // [rows][n] zeros standing in for absent diagonals
+    uint32_t* out[kMaxGiants];                  // [2][rows][n] each
+};
+int fused_terms_multi_launch(const FusedMulti& a, const int32_t* row_slot, const ModSlot* slots,
+                             int rows, size_t cols, cudaStream_t st);
 int tensor_launch(const uint32_t* x, const uint32_t* y, uint32_t* out, const int32_t* row_slot,
                   const ModSlot* slots, int rows, size_t cols, cudaStream_t st);
 

@@ -17,14 +17,6 @@ __device__ __forceinline__ uint64_t mad64(uint32_t a, uint32_t b, uint64_t c) {
     return (uint64_t)a * b + c;
 }
 
-// Source column of output column t under the evaluation-domain automorphism X -> X^k
-// (same closed form as automorphism_eval_kernel).
-__device__ __forceinline__ uint32_t galois_src(uint32_t t, uint32_t k, uint32_t n, uint32_t lg) {
-    const uint32_t u = __brev(t) >> (32 - lg);
-    const uint32_t e = ((2 * u + 1) * k) & (2 * n - 1);
-    return __brev((e - 1) >> 1) >> (32 - lg);
-}
-
 // BETA > 0: digit count known at compile time -- the loop is unrolled and all 3 * BETA
 // 16-byte loads of a thread are issued before the first product, which is what keeps
 // enough bytes in flight per SM to stream the key at HBM speed.  BETA = 0: runtime count.

@@ -235,9 +235,14 @@ __device__ __forceinline__ void load_tw15(const uint2* __restrict__ tab, uint32_
     }
 }
 
+// EPI: the ModDown epilogue (reference keyswitch.py:412-418, :452) runs on the transform's
+// registers instead of a separate pass: the rows are conv = NTT(BConv_{P->Q}(..)) of both
+// halves, and the kernel stores (x_Q - conv) * P^-1 (+ fold) straight into the result, so conv
+// is never written or re-read.
+template <bool EPI>
 __global__ void __launch_bounds__(256)
 ntt16_fwd_contig(const uint32_t* in, uint32_t* out, const int32_t* __restrict__ row_slot,
-                 const ModSlot* __restrict__ slots, RowMap rm) {
+                 const ModSlot* __restrict__ slots, RowMap rm, ModDownEpilogueArgs ep) {
     __shared__ uint32_t tile[16 * 272];
     __shared__ uint2 s_blk[16][16];      // per block: the 15 twiddles of stages 8..11
     const int tid = threadIdx.x;
@@ -245,6 +250,15 @@ ntt16_fwd_contig(const uint32_t* in, uint32_t* out, const int32_t* __restrict__ 
     const ModSlot& m = slots[row_slot[blockIdx.y]];
     const uint32_t q = m.q;
     const uint32_t B = blockIdx.x * 16 + blk;          // 256-element block index within the limb
+    const int ep_row = EPI ? blockIdx.y % ep.l : 0, ep_half = EPI ? blockIdx.y / ep.l : 0;
+    const size_t ep_at = (size_t)ep_row * kN16 + B * 256 + 16 * e;
+    if (EPI) {
+        // x_Q (and the folded polynomial) are needed only after the last stage: pull their
+        // lines into L2 now
+        asm volatile("prefetch.global.L2 [%0];" :: "l"((ep_half ? ep.xq_b : ep.xq_a) + ep_at));
+        const uint32_t* f = ep_half ? ep.fold_b : ep.fold_a;
+        if (f && !ep.galois) asm volatile("prefetch.global.L2 [%0];" :: "l"(f + ep_at));
+    }
     const uint32_t* src = in + rm.in_row(blockIdx.y) * kN16 + B * 256;
     const uint2* __restrict__ fwd = m.fwd;
     // the 16 threads of a 256-block stage that block's table entries themselves: the whole
@@ -268,6 +282,32 @@ ntt16_fwd_contig(const uint32_t* in, uint32_t* out, const int32_t* __restrict__ 
     for (int k = 0; k < 16; ++k) v[k] = tile[blk * 272 + 17 * e + k];
     // global stages 12..15: elements 16e + k, slot = ((256 + B) * 16 + e) * 2^s + group
     ct16(v, q, TW_MUL(s == 0 ? tw.t1 : (s == 1 ? tw.t2[gi & 1] : (s == 2 ? tw.t4[gi & 3] : tw.t8[gi & 7]))));
+    if (EPI) {
+        const uint32_t pinv = ep.pinv[ep_row], pinv_s = ep.pinv_s[ep_row];
+        const uint32_t* x = (ep_half ? ep.xq_b : ep.xq_a) + ep_at;
+        const uint32_t* fsrc = ep_half ? ep.fold_b : ep.fold_a;
+        uint32_t* o = (ep_half ? ep.out_b : ep.out_a) + ep_at;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            uint32_t xv[8], r[8];
+            ld256(x + 8 * h, xv);
+#pragma unroll
+            for (int k = 0; k < 8; ++k) r[k] = shoup_mul(xv[k] - csub(v[8 * h + k], q) + q, pinv, pinv_s, q);
+            if (fsrc && ep.galois) {
+                const uint32_t* f = fsrc + (size_t)ep_row * kN16;
+#pragma unroll
+                for (int k = 0; k < 8; ++k)
+                    r[k] = add_mod(r[k], f[galois_src(B * 256 + 16 * e + 8 * h + k, ep.galois, kN16, 16)], q);
+            } else if (fsrc) {
+                uint32_t fv[8];
+                ld256(fsrc + ep_at + 8 * h, fv);
+#pragma unroll
+                for (int k = 0; k < 8; ++k) r[k] = add_mod(r[k], fv[k], q);
+            }
+            st256(o + 8 * h, r);
+        }
+        return;
+    }
     uint32_t* dst = out + rm.out_row(blockIdx.y) * kN16 + B * 256 + 16 * e;
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
@@ -359,9 +399,16 @@ static int launch_generic(const uint32_t* in, uint32_t* out, const int32_t* row_
     return CKKS_OK;
 }
 
+bool ntt_can_fuse_moddown(uint32_t n) { return n == (uint32_t)kN16; }
+
 int ntt_launch(const uint32_t* in, uint32_t* out, const int32_t* row_slot, const ModSlot* slots,
-               RowMap rm, int rows, uint32_t n, int inverse, cudaStream_t st) {
+               RowMap rm, int rows, uint32_t n, int inverse, cudaStream_t st,
+               const ModDownEpilogueArgs* epi) {
     if (rows <= 0) return CKKS_OK;
+    if (epi && (inverse || !ntt_can_fuse_moddown(n) || rows != 2 * epi->l)) {
+        set_last_error("fused ModDown epilogue needs a forward N = 2^16 transform over 2 l rows");
+        return CKKS_ERR_ARG;
+    }
     if (n == (uint32_t)kN16) {
         constexpr int COLS = 16;
         dim3 g_str(256 / COLS, rows), g_con(16, rows);
@@ -369,8 +416,14 @@ int ntt_launch(const uint32_t* in, uint32_t* out, const int32_t* row_slot, const
         if (!inverse) {
             { ProfScope ps("ntt16_fwd_strided", st, 8.0 * rows * kN16);
               ntt16_fwd_strided<COLS><<<g_str, 16 * COLS, 0, st>>>(in, out, row_slot, slots, rm); }
-            { ProfScope ps("ntt16_fwd_contig", st, 8.0 * rows * kN16);
-              ntt16_fwd_contig<<<g_con, 256, 0, st>>>(out, out, row_slot, slots, rm2); }
+            if (epi) {
+                // reads conv + x_Q (+ fold), writes the result: (3 or 4) limbs per row
+                ProfScope ps("ntt16_fwd_contig_moddown", st, 4.0 * rows * kN16 * (epi->fold_b ? 3.5 : 3.0));
+                ntt16_fwd_contig<true><<<g_con, 256, 0, st>>>(out, out, row_slot, slots, rm2, *epi);
+            } else {
+                ProfScope ps("ntt16_fwd_contig", st, 8.0 * rows * kN16);
+                ntt16_fwd_contig<false><<<g_con, 256, 0, st>>>(out, out, row_slot, slots, rm2, ModDownEpilogueArgs{});
+            }
         } else {
             { ProfScope ps("ntt16_inv_contig", st, 8.0 * rows * kN16);
               ntt16_inv_contig<<<g_con, 256, 0, st>>>(in, out, row_slot, slots, rm); }
@@ -398,7 +451,7 @@ int ntt_stages_launch(const uint32_t* in, uint32_t* out, const int32_t* row_slot
         dim3 g_str(256 / COLS, rows), g_con(16, rows);
         const bool strided = inverse ? (s_lo == 8) : (s_lo == 0);
         if (!inverse && strided) ntt16_fwd_strided<COLS><<<g_str, 16 * COLS, 0, st>>>(in, out, row_slot, slots, rm);
-        if (!inverse && !strided) ntt16_fwd_contig<<<g_con, 256, 0, st>>>(in, out, row_slot, slots, rm);
+        if (!inverse && !strided) ntt16_fwd_contig<false><<<g_con, 256, 0, st>>>(in, out, row_slot, slots, rm, ModDownEpilogueArgs{});
         if (inverse && !strided) ntt16_inv_contig<<<g_con, 256, 0, st>>>(in, out, row_slot, slots, rm);
         if (inverse && strided) ntt16_inv_strided<COLS><<<g_str, 16 * COLS, 0, st>>>(in, out, row_slot, slots, rm);
         CK(cudaGetLastError());

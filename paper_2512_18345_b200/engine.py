@@ -52,36 +52,64 @@ class Engine:
         _lib.check(self.lib.ckks_set_lanes(self.ctx, count))
         self.lanes = count
         self.lane_streams = [None] + [self.torch.cuda.Stream(device=self.device) for _ in range(count - 1)]
+        self._lane_group = None
 
     def fork(self, jobs, with_lane: bool = False):
-        """Run the callables in `jobs` round-robin over the lanes (each on its lane's
-        stream and workspace), joined back into the current stream.  Results in order."""
+        """Run the callables in `jobs` concurrently over the lanes the caller owns (each on
+        its lane's stream and workspace), joined back into the current stream.  Results in
+        order.  Forks nest: with fewer jobs than lanes the caller's lanes are split into one
+        contiguous group per job, and a fork issued inside a job spreads over that job's
+        group only, so concurrent jobs never share a workspace lane."""
         torch = self.torch
-        lanes = getattr(self, "lanes", 1)
-        if lanes == 1 or len(jobs) < 2:
-            return [job(0, i) if with_lane else job() for i, job in enumerate(jobs)]
+        outer = getattr(self, "_lane_group", None)
+        group = outer if outer is not None else list(range(getattr(self, "lanes", 1)))
+        if len(group) == 1 or len(jobs) < 2:
+            return [job(group[0], i) if with_lane else job() for i, job in enumerate(jobs)]
+        width = min(len(jobs), len(group))
+        if with_lane:
+            # lane-indexed jobs (per-lane accumulators reduced by ks_finish): the first `width`
+            # lanes of the group, one each, no nesting
+            subs = [[lane] for lane in group[:width]]
+        else:
+            # sub-groups: job i runs on lane sub[i % width][0] and may fork over sub[i % width]
+            base, extra = divmod(len(group), width)
+            subs, at = [], 0
+            for w in range(width):
+                size = base + (1 if w < extra else 0)
+                subs.append(group[at:at + size])
+                at += size
+        home = group[0]
         main = torch.cuda.current_stream(self.device)
         start = torch.cuda.Event()
         start.record(main)
         used = set()
         out = []
-        for i, job in enumerate(jobs):
-            lane = i % lanes
-            if lane == 0:
-                _lib.check(self.lib.ckks_select_lane(self.ctx, 0))
-                out.append(job(0, i // lanes) if with_lane else job())
-                continue
-            side = self.lane_streams[lane]
-            if lane not in used:
-                side.wait_event(start)
-                used.add(lane)
-            _lib.check(self.lib.ckks_select_lane(self.ctx, lane))
-            with torch.cuda.stream(side):
-                out.append(job(lane, i // lanes) if with_lane else job())
-        _lib.check(self.lib.ckks_select_lane(self.ctx, 0))
+        try:
+            for i, job in enumerate(jobs):
+                sub = subs[i % width]
+                lane = sub[0]
+                self._lane_group = sub
+                _lib.check(self.lib.ckks_select_lane(self.ctx, lane))
+                if lane == home:
+                    out.append(job(lane, i // width) if with_lane else job())
+                    continue
+                side = self.lane_streams[lane]
+                if lane not in used:
+                    side.wait_event(start)
+                    used.add(lane)
+                with torch.cuda.stream(side):
+                    out.append(job(lane, i // width) if with_lane else job())
+        finally:
+            self._lane_group = outer
+            _lib.check(self.lib.ckks_select_lane(self.ctx, home))
         for lane in used:
             main.wait_stream(self.lane_streams[lane])
         return out
+
+    def lane_count(self) -> int:
+        """Lanes the caller may fork over right now (all of them outside a fork)."""
+        group = getattr(self, "_lane_group", None)
+        return len(group) if group is not None else getattr(self, "lanes", 1)
 
     # ---- modulus slots ----------------------------------------------------
     def slot(self, m, n: int) -> int:
@@ -179,6 +207,26 @@ class Engine:
         _lib.check(self.lib.ckks_fused_terms(self.ctx, count, xp, pp, out.data_ptr(), row_slot.data_ptr(),
                                              xs[0].shape[1], xs[0].shape[2], self.stream()))
         return out
+
+    def fused_terms_multi(self, xs, table, row_slot):
+        """outs[g] = sum_b xs[b] * table[g][b] for every giant step g in one pass
+        (table[g][b] None: no such diagonal); xs are [2, rows, n] tensors."""
+        nb, ng = len(xs), len(table)
+        outs = [self.torch.empty_like(xs[0]) for _ in range(ng)]
+        xp = (ctypes.c_void_p * nb)(*[x.data_ptr() for x in xs])
+        flat = [None if pt is None else pt.data_ptr() for row in table for pt in row]
+        pp = (ctypes.c_void_p * (nb * ng))(*flat)
+        op = (ctypes.c_void_p * ng)(*[o.data_ptr() for o in outs])
+        zero = None
+        if any(f is None for f in flat):
+            key = ("zero_plain", xs[0].shape[1], xs[0].shape[2])
+            zero = self._tables.get(key)
+            if zero is None:
+                zero = self._tables[key] = self.torch.zeros(xs[0].shape[1:], dtype=self.torch.int32, device=self.device)
+            zero = zero.data_ptr()
+        _lib.check(self.lib.ckks_fused_terms_multi(self.ctx, nb, ng, xp, pp, zero, op, row_slot.data_ptr(),
+                                                   xs[0].shape[1], xs[0].shape[2], self.stream()))
+        return outs
 
     def tensor(self, x, y, row_slot):
         """(d0, d1, d2) of two [2, rows, n] ciphertext tensors as one [3, rows, n] tensor."""
