@@ -533,8 +533,23 @@ int ckks_bconv_table_create(ckks_ctx* ctx, const int32_t* in_slot, int l_in, con
     CKS(upload(inv_s, &d_invs));
     CKS(upload(t_mont, &d_tm));
     CKS(upload(tab->t_plain, &d_tp));
-    tab->owned = {d_in, d_out, d_inv, d_invs, d_tm, d_tp};
-    tab->dev = BconvDev{l_in, l_out, all31, d_in, d_out, d_inv, d_invs, d_tm, d_tp};
+    // operands of bconv_dmma in their final form
+    const int kp = (l_in + 3) & ~3, lo8 = (l_out + 7) & ~7;
+    std::vector<double> t_f64((size_t)lo8 * kp, 0.0);
+    std::vector<uint4> om(lo8, make_uint4(3u, 0u, 0u, 0u)), inc(kp, make_uint4(3u, 0u, 0u, 0u));
+    for (int i = 0; i < l_out; ++i) {
+        for (int j = 0; j < l_in; ++j) t_f64[(size_t)i * kp + j] = (double)t_mont[(size_t)i * l_in + j];
+        const ModSlot& m = ctx->h_slots[out_slot[i]];
+        om[i] = make_uint4(m.q, m.qinv, (uint32_t)i, (uint32_t)(((uint64_t)m.r1 << 16) % m.q));
+    }
+    for (int j = 0; j < l_in; ++j) inc[j] = make_uint4(qs[j], tab->inv_qhat[j], inv_s[j], 0u);
+    double* d_tf;
+    uint4 *d_om, *d_inc;
+    CKS(upload(t_f64, &d_tf));
+    CKS(upload(om, &d_om));
+    CKS(upload(inc, &d_inc));
+    tab->owned = {d_in, d_out, d_inv, d_invs, d_tm, d_tp, d_tf, d_om, d_inc};
+    tab->dev = BconvDev{l_in, l_out, all31, d_in, d_out, d_inv, d_invs, d_tm, d_tp, kp, d_tf, d_om, d_inc};
     *table = (int32_t)ctx->tables.size();
     ctx->tables.push_back(std::move(tab));
     return CKKS_OK;

@@ -191,6 +191,125 @@ bconv_f64(BconvJobs jobs, const ModSlot* __restrict__ slots, size_t cols, int ch
     }
 }
 
+// FP64 tensor-core variant (DMMA, mma.sync m8n8k4).  Measured on B200
+// (profiles/microbench/dmma.cu): DMMA sustains 63.7 FMA/clk/SM, the same as DFMA, but one
+// warp instruction carries 256 of them, so the contraction needs ~1 instruction per 10
+// outputs instead of 12 IMAD.WIDE (2.8 integer-pipe slots each) per output.  Exactness is
+// the same split as bconv_f64: y = y1 * 2^16 + y0, every T * y0, T * y1 < 2^47, sums of up
+// to 16 terms < 2^51, accumulators seeded with 2^52 so the integer sum sits in the mantissa.
+//
+// GEMM view per conversion: D[i][c] = sum_k T[i][k] * y[k][c] with M = output limbs (tiles
+// of 8), K = input limbs (padded to a multiple of 4), N = columns (tiles of 8).  A warp owns
+// 16 columns: it pre-scales them once (each lane 1 column x KS limbs per tile = the B
+// fragments), then walks the output tiles; A fragments come from a shared-memory copy of
+// the table in double.  Each lane finishes two adjacent columns of one output limb.
+__device__ __forceinline__ void dmma884(double (&c)[2], double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                 : "+d"(c[0]), "+d"(c[1]) : "d"(a), "d"(b));
+}
+
+// exact u32 (< 2^32) -> double without the slow I2F path
+__device__ __forceinline__ double u2d(uint32_t x) {
+    return __hiloint2double(0x43300000, (int)x) - 4503599627370496.0;
+}
+
+template <int KS>
+__global__ void __launch_bounds__(128)
+bconv_dmma(BconvJobs jobs, const ModSlot* __restrict__ slots, size_t cols, int chunk) {
+    constexpr int KP = 4 * KS;
+    extern __shared__ uint4 sm4[];
+    const BconvJob& job = jobs.job[blockIdx.y];
+    const int l_in = job.tab.l_in, l_out = job.tab.l_out;
+    const int i_lo = blockIdx.z * chunk, i_hi = min(l_out, i_lo + chunk);
+    if (i_lo >= i_hi) return;
+    const int rows_pad = (i_hi - i_lo + 7) & ~7;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int kk = lane & 3, cc = lane >> 2;
+    // A warp walks column tiles of 16; the table staging below is paid once per CTA and the
+    // next tile's residues are in flight while the current tile is contracted.
+    const size_t tiles = cols / 16;
+    const size_t warps = (size_t)gridDim.x * 4;
+    size_t tile = (size_t)blockIdx.x * 4 + warp;
+    uint32_t raw[2][KS];
+    auto fetch = [&](size_t tl) {
+#pragma unroll
+        for (int j = 0; j < KS; ++j) {
+            const int k = 4 * j + kk;
+#pragma unroll
+            for (int t = 0; t < 2; ++t)
+                raw[t][j] = k < l_in ? job.in[(size_t)k * job.in_stride + tl * 16 + 8 * t + cc] : 0u;
+        }
+    };
+    if (tile < tiles) fetch(tile);              // first residues: in flight during the staging
+    // operands come ready-made from the table (api.cu): one level of loads, no arithmetic
+    double* s_t = reinterpret_cast<double*>(sm4);                          // [rows_pad][KP]
+    uint4* s_om = sm4 + ((size_t)((chunk + 7) & ~7) * KP * sizeof(double)) / sizeof(uint4);   // {q, qinv, out row, 2^48 mod q}
+    uint4* s_in = s_om + ((chunk + 7) & ~7);                               // {q, inv_qhat, shoup(inv_qhat), -}
+    {
+        const uint4* src = reinterpret_cast<const uint4*>(job.tab.t_f64 + (size_t)i_lo * KP);
+        uint4* dst = reinterpret_cast<uint4*>(s_t);
+        for (int idx = threadIdx.x; idx < rows_pad * KP / 2; idx += blockDim.x) dst[idx] = src[idx];
+    }
+    for (int r = threadIdx.x; r < rows_pad; r += blockDim.x) {
+        uint4 om = job.tab.om[i_lo + r];
+        if (job.out_row && i_lo + r < i_hi) om.z = (uint32_t)job.out_row[i_lo + r];
+        s_om[r] = om;
+    }
+    for (int k = threadIdx.x; k < KP; k += blockDim.x) s_in[k] = job.tab.inc[k];
+    __syncthreads();
+    if (tile >= tiles) return;
+    const double seed = 4503599627370496.0;     // 2^52
+    for (; tile < tiles; tile += warps) {
+        // B fragments: lane (kk, cc) holds y[4j + kk][16 tile + 8t + cc], split in 16-bit halves
+        double y0[2][KS], y1[2][KS];
+#pragma unroll
+        for (int j = 0; j < KS; ++j) {
+            const uint4 im = s_in[4 * j + kk];
+#pragma unroll
+            for (int t = 0; t < 2; ++t) {
+                const uint32_t y = 4 * j + kk < l_in ? shoup_mul(raw[t][j], im.y, im.z, im.x) : 0u;
+                y0[t][j] = u2d(y & 0xFFFFu);
+                y1[t][j] = u2d(y >> 16);
+            }
+        }
+        const size_t c_base = tile * 16;
+        if (tile + warps < tiles) fetch(tile + warps);
+        for (int m0 = 0; m0 < rows_pad; m0 += 8) {
+            double a[KS];
+#pragma unroll
+            for (int j = 0; j < KS; ++j) a[j] = s_t[(m0 + cc) * KP + 4 * j + kk];
+            double c0[2][2], c1[2][2];
+#pragma unroll
+            for (int t = 0; t < 2; ++t) c0[t][0] = c0[t][1] = c1[t][0] = c1[t][1] = seed;
+#pragma unroll
+            for (int j = 0; j < KS; ++j) {
+#pragma unroll
+                for (int t = 0; t < 2; ++t) {
+                    dmma884(c0[t], a[j], y0[t][j]);
+                    dmma884(c1[t], a[j], y1[t][j]);
+                }
+            }
+            // lane holds D[m0 + cc][2 kk + {0, 1}] of both column tiles
+            const uint4 om = s_om[m0 + cc];
+            if (i_lo + m0 + cc < i_hi) {
+                uint32_t* dst = job.out + (size_t)om.z * job.out_stride + c_base + 2 * kk;
+#pragma unroll
+                for (int t = 0; t < 2; ++t) {
+                    uint32_t r[2];
+#pragma unroll
+                    for (int e = 0; e < 2; ++e) {
+                        const uint64_t b0 = (uint64_t)__double_as_longlong(c0[t][e]) & 0xFFFFFFFFFFFFFull;
+                        const uint64_t b1 = (uint64_t)__double_as_longlong(c1[t][e]) & 0xFFFFFFFFFFFFFull;
+                        const uint64_t v = (uint64_t)(uint32_t)(b1 >> 32) * om.w + ((b1 & 0xFFFFFFFFull) << 16) + b0;
+                        r[e] = redc((uint32_t)v, (uint32_t)(v >> 32), om.x, om.y);
+                    }
+                    *reinterpret_cast<uint2*>(dst + 8 * t) = make_uint2(r[0], r[1]);
+                }
+            }
+        }
+    }
+}
+
 // Any modulus below 2^32; one column per thread; exact '%' folds.
 __global__ void __launch_bounds__(128)
 bconv_generic(BconvJobs jobs, const ModSlot* __restrict__ slots, size_t cols) {
@@ -220,16 +339,40 @@ static double jobs_bytes(const BconvJobs& jobs, size_t cols) {
 static int bconv_variant() {
     static int v = -1;
     if (v < 0) {
+        // default: FP64 tensor-core kernel; CKKS_BCONV=int: IMAD.WIDE kernel; CKKS_BCONV=f64: DFMA kernel
         const char* e = getenv("CKKS_BCONV");
-        v = (e && e[0] == 'f') ? 1 : 0;       // default: IMAD.WIDE kernel; CKKS_BCONV=f64: FP64-pipe kernel
+        v = !e ? 2 : (e[0] == 'f' ? 1 : (e[0] == 'i' ? 0 : 2));
     }
     return v;
+}
+
+template <int KS>
+static int launch_dmma(const BconvJobs& jobs, const ModSlot* slots, size_t cols, int l_out_max, cudaStream_t st) {
+    // tiles per warp: as many as still leave ~6 CTAs per SM (the per-CTA table staging is
+    // amortised over them); the output walk is split over blockIdx.z when one conversion is too small
+    const size_t tiles = cols / 16;
+    const int z_max = (l_out_max + 7) / 8;
+    int tpw = 4;
+    while (tpw > 1 && ((tiles + 4 * tpw - 1) / (4 * tpw)) * jobs.count * z_max < (size_t)148 * 6) tpw >>= 1;
+    const unsigned gx = (unsigned)((tiles + 4 * tpw - 1) / (4 * tpw));
+    const size_t ctas_xy = (size_t)gx * jobs.count;
+    int z = (int)(((size_t)148 * 6 + ctas_xy - 1) / ctas_xy);
+    if (z > z_max) z = z_max;
+    const int chunk = (((l_out_max + z - 1) / z) + 7) & ~7;
+    const size_t sm = sizeof(double) * (size_t)chunk * 4 * KS + sizeof(uint4) * ((size_t)chunk + 4 * KS);
+    dim3 grid(gx, jobs.count, (l_out_max + chunk - 1) / chunk);
+    ProfScope ps("bconv", st, jobs_bytes(jobs, cols));
+    if (sm > 48 * 1024)
+        CK(cudaFuncSetAttribute(bconv_dmma<KS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    bconv_dmma<KS><<<grid, 128, sm, st>>>(jobs, slots, cols, chunk);
+    CK(cudaGetLastError());
+    return CKKS_OK;
 }
 
 template <int LIN>
 static int launch_fast(const BconvJobs& jobs, const ModSlot* slots, size_t cols, int l_out_max,
                        bool pairs, cudaStream_t st) {
-    if (bconv_variant() == 1) {
+    if (bconv_variant() == 1) {          // CKKS_BCONV=f64
         constexpr int LINP = (LIN + 1) / 2 * 2;
         const size_t sm = sizeof(double) * (size_t)l_out_max * LINP + sizeof(uint4) * ((size_t)l_out_max + LIN);
         const unsigned gx = (unsigned)((cols + 127) / 128);
@@ -277,6 +420,19 @@ int bconv_launch_jobs(const BconvJobs& jobs, const ModSlot* slots, size_t cols, 
         fast = fast && jb.tab.all31;
         pairs = pairs && (((uintptr_t)jb.in | (uintptr_t)jb.out) % 8 == 0) &&
                 jb.in_stride % 2 == 0 && jb.out_stride % 2 == 0;
+    }
+    if (fast && l_in <= 16 && cols % 16 == 0 && bconv_variant() == 2) {
+        bool aligned = true;
+        for (int j = 0; j < jobs.count; ++j)
+            aligned = aligned && ((uintptr_t)jobs.job[j].out % 8 == 0) && jobs.job[j].out_stride % 2 == 0;
+        if (aligned) {
+            switch ((l_in + 3) / 4) {
+                case 1: return launch_dmma<1>(jobs, slots, cols, l_out_max, st);
+                case 2: return launch_dmma<2>(jobs, slots, cols, l_out_max, st);
+                case 3: return launch_dmma<3>(jobs, slots, cols, l_out_max, st);
+                default: return launch_dmma<4>(jobs, slots, cols, l_out_max, st);
+            }
+        }
     }
     if (fast && l_in <= 16) {
         switch (l_in) {

@@ -107,6 +107,11 @@ struct BconvDev {
     const uint32_t* inv_qhat_s; // [l_in]   Shoup companions
     const uint32_t* t_mont;     // [l_out][l_in]  (Q*/Q_j) * 2^32 mod P_i  (Montgomery form)
     const uint32_t* t_plain;    // [l_out][l_in]  (Q*/Q_j) mod P_i
+    // ready-made operands of the FP64 tensor-core kernel (one load level in its prologue):
+    int kp;                     // l_in rounded up to a multiple of 4
+    const double* t_f64;        // [l_out rounded up to 8][kp]  t_mont as doubles, zero padded
+    const uint4* om;            // [l_out rounded up to 8]  {P_i, -P_i^-1.. (qinv), i, 2^48 mod P_i}
+    const uint4* inc;           // [kp]  {Q_k, inv_qhat, shoup(inv_qhat), 0}; padding {3, 0, 0, 0}
 };
 
 struct BconvJob {
