@@ -240,7 +240,7 @@ bconv_dmma(BconvJobs jobs, const ModSlot* __restrict__ slots, size_t cols, int c
                 raw[t][j] = k < l_in ? job.in[(size_t)k * job.in_stride + tl * 16 + 8 * t + cc] : 0u;
         }
     };
-    if (tile < tiles) fetch(tile);              // first residues: in flight during the staging
+    pdl_trigger();
     // operands come ready-made from the table (api.cu): one level of loads, no arithmetic
     double* s_t = reinterpret_cast<double*>(sm4);                          // [rows_pad][KP]
     uint4* s_om = sm4 + ((size_t)((chunk + 7) & ~7) * KP * sizeof(double)) / sizeof(uint4);   // {q, qinv, out row, 2^48 mod q}
@@ -256,6 +256,8 @@ bconv_dmma(BconvJobs jobs, const ModSlot* __restrict__ slots, size_t cols, int c
         s_om[r] = om;
     }
     for (int k = threadIdx.x; k < KP; k += blockDim.x) s_in[k] = job.tab.inc[k];
+    pdl_wait();                                 // tables are static; the residues are not
+    if (tile < tiles) fetch(tile);
     __syncthreads();
     if (tile >= tiles) return;
     const double seed = 4503599627370496.0;     // 2^52
@@ -364,7 +366,7 @@ static int launch_dmma(const BconvJobs& jobs, const ModSlot* slots, size_t cols,
     ProfScope ps("bconv", st, jobs_bytes(jobs, cols));
     if (sm > 48 * 1024)
         CK(cudaFuncSetAttribute(bconv_dmma<KS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    bconv_dmma<KS><<<grid, 128, sm, st>>>(jobs, slots, cols, chunk);
+    CK(launch_pdl(bconv_dmma<KS>, grid, dim3(128), sm, st, jobs, slots, cols, chunk));
     CK(cudaGetLastError());
     return CKKS_OK;
 }

@@ -97,6 +97,17 @@ __device__ __forceinline__ uint32_t galois_src(uint32_t t, uint32_t k, uint32_t 
     return __brev((e - 1) >> 1) >> (32 - lg);
 }
 
+// ---- programmatic dependent launch --------------------------------------------------
+// Kernels on the hot path are launched with programmatic stream serialisation
+// (internal.h launch_pdl): a kernel may start while its predecessor in the stream is
+// still draining.  pdl_trigger() (first statement) lets the NEXT kernel begin launching;
+// everything before pdl_wait() may only touch static tables (twiddles, conversion tables,
+// switching keys); pdl_wait() returns once the predecessor grid has completed and its
+// writes are visible, and must precede the first access to any operand buffer.  Both are
+// no-ops for a kernel launched the ordinary way.
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 // ---- memory helpers -------------------------------------------------------------
 
 // Streaming loads for data read exactly once per kernel (switching keys, encoded

@@ -20,6 +20,8 @@ elementwise_vec4(const uint4* a, const uint4* b, uint4* out, const int32_t* __re
                  const ModSlot* __restrict__ slots, size_t cols4) {
     const size_t row = blockIdx.y;
     const ModSlot m = slots[row_slot[row]];
+    pdl_trigger();
+    pdl_wait();
     const size_t stride = (size_t)gridDim.x * blockDim.x;
     for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < cols4; i += stride) {
         const uint4 x = a[row * cols4 + i], y = b[row * cols4 + i];
@@ -56,8 +58,8 @@ int elementwise_launch(const uint32_t* a, const uint32_t* b, uint32_t* out, cons
     ProfScope ps("elementwise", st, 12.0 * rows * cols);
 #define EW_DISPATCH(K)                                                                             \
     if (vec)                                                                                       \
-        elementwise_vec4<K><<<grid, 256, 0, st>>>((const uint4*)a, (const uint4*)b, (uint4*)out,   \
-                                                  row_slot, slots, work);                          \
+        launch_pdl(elementwise_vec4<K>, grid, dim3(256), 0, st, (const uint4*)a, (const uint4*)b,   \
+                   (uint4*)out, row_slot, slots, work);                                            \
     else                                                                                           \
         elementwise_scalar<K><<<grid, 256, 0, st>>>(a, b, out, row_slot, slots, work);
     if (kind == 0) { EW_DISPATCH(0) }
@@ -78,6 +80,8 @@ int elementwise_launch(const uint32_t* a, const uint32_t* b, uint32_t* out, cons
 __global__ void __launch_bounds__(256)
 automorphism_eval_kernel(const uint32_t* __restrict__ in, uint32_t* __restrict__ out, uint32_t n,
                          uint32_t lg, uint32_t k) {
+    pdl_trigger();
+    pdl_wait();
     const size_t row = blockIdx.y;
     const uint32_t stride = gridDim.x * blockDim.x;
     for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += stride) {
@@ -102,7 +106,7 @@ int automorphism_eval_launch(const uint32_t* in, uint32_t* out, int rows, uint32
     unsigned gx = (n + 255) / 256;
     if (gx > 256) gx = 256;
     ProfScope ps("automorphism_eval", st, 8.0 * rows * n);
-    automorphism_eval_kernel<<<dim3(gx, rows), 256, 0, st>>>(in, out, n, lg, k);
+    CK(launch_pdl(automorphism_eval_kernel, dim3(gx, rows), dim3(256), 0, st, in, out, n, lg, k));
     CK(cudaGetLastError());
     return CKKS_OK;
 }
@@ -227,6 +231,8 @@ fused_terms_kernel(FusedTerms terms, uint4* out, const int32_t* __restrict__ row
                    const ModSlot* __restrict__ slots, int rows, size_t cols4) {
     const size_t row = blockIdx.y;
     const ModSlot m = slots[row_slot[row]];
+    pdl_trigger();
+    pdl_wait();
     const size_t half = (size_t)rows * cols4;
     const size_t stride = (size_t)gridDim.x * blockDim.x;
     const uint64_t pol = l2_evict_first_policy();
@@ -272,7 +278,7 @@ int fused_terms_launch(const FusedTerms& terms, uint32_t* out, const int32_t* ro
     }
     ProfScope ps("fused_terms", st, 4.0 * cols * rows * (3.0 * terms.count + 2.0));
     unsigned gx = (unsigned)((cols / 4 + 255) / 256);
-    fused_terms_kernel<<<dim3(gx, rows), 256, 0, st>>>(terms, (uint4*)out, row_slot, slots, rows, cols / 4);
+    CK(launch_pdl(fused_terms_kernel, dim3(gx, rows), dim3(256), 0, st, terms, (uint4*)out, row_slot, slots, rows, cols / 4));
     CK(cudaGetLastError());
     return CKKS_OK;
 }
@@ -288,6 +294,8 @@ fused_terms_multi_kernel(FusedMulti a, const int32_t* __restrict__ row_slot,
                          const ModSlot* __restrict__ slots, int rows, size_t cols2) {
     const size_t row = blockIdx.y;
     const ModSlot m = slots[row_slot[row]];
+    pdl_trigger();
+    pdl_wait();
     const size_t half = (size_t)rows * cols2;
     const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= cols2) return;
@@ -349,7 +357,7 @@ int fused_terms_multi_launch(const FusedMulti& a, const int32_t* row_slot, const
     ProfScope ps("fused_terms", st, 4.0 * cols * rows * limbs);
     dim3 grid((unsigned)((cols / 2 + 255) / 256), rows);
     switch (a.ng) {
-#define MULTI_CASE(G) case G: fused_terms_multi_kernel<G><<<grid, 256, 0, st>>>(a, row_slot, slots, rows, cols / 2); break;
+#define MULTI_CASE(G) case G: CK(launch_pdl(fused_terms_multi_kernel<G>, grid, dim3(256), 0, st, a, row_slot, slots, rows, cols / 2)); break;
         MULTI_CASE(1) MULTI_CASE(2) MULTI_CASE(3) MULTI_CASE(4) MULTI_CASE(5) MULTI_CASE(6) MULTI_CASE(7) MULTI_CASE(8)
 #undef MULTI_CASE
     }
@@ -366,6 +374,8 @@ tensor_kernel(const uint4* __restrict__ x, const uint4* __restrict__ y, uint4* o
               size_t cols4) {
     const size_t row = blockIdx.y;
     const ModSlot m = slots[row_slot[row]];
+    pdl_trigger();
+    pdl_wait();
     const size_t half = (size_t)rows * cols4;
     const size_t stride = (size_t)gridDim.x * blockDim.x;
     for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < cols4; i += stride) {
@@ -392,8 +402,8 @@ int tensor_launch(const uint32_t* x, const uint32_t* y, uint32_t* out, const int
     if (cols % 4 || rows > 65535) { set_last_error("tensor needs cols %% 4 == 0 and <= 65535 rows"); return CKKS_ERR_UNSUPPORTED; }
     ProfScope ps("tensor", st, 4.0 * cols * rows * 7.0);
     unsigned gx = (unsigned)((cols / 4 + 255) / 256);
-    tensor_kernel<<<dim3(gx, rows), 256, 0, st>>>((const uint4*)x, (const uint4*)y, (uint4*)out, row_slot,
-                                                  slots, rows, cols / 4);
+    CK(launch_pdl(tensor_kernel, dim3(gx, rows), dim3(256), 0, st, (const uint4*)x, (const uint4*)y, (uint4*)out, row_slot,
+                                                  slots, rows, cols / 4));
     CK(cudaGetLastError());
     return CKKS_OK;
 }

@@ -27,6 +27,26 @@ void set_last_error(const char* fmt, ...);
         if (_s != CKKS_OK) return _s;     \
     } while (0)
 
+// Launch with programmatic stream serialisation (see common.cuh pdl_*): the launch latency
+// and the table-loading prologue of kernel N+1 overlap the tail of kernel N; inside CUDA
+// graphs this becomes a programmatic dependency edge.  CKKS_PDL=0 falls back to ordinary
+// launches (the kernels' pdl_* calls are then no-ops).
+bool pdl_enabled();
+template <class... P, class... A>
+inline cudaError_t launch_pdl(void (*kernel)(P...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, A&&... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kernel, P(args)...);
+}
+
 // Logical row r of a launch lives at physical row in[r] of the source buffer
 // and out[r] of the destination (identity when null).  Lets the key-switch
 // pipeline transform scattered limbs (e.g. the converted rows of a raised

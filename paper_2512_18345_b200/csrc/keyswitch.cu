@@ -33,6 +33,10 @@ inner_product_kernel(InnerProductArgs p, const ModSlot* __restrict__ slots) {
     if (i >= n) return;
     const int beta = BETA > 0 ? BETA : p.beta;
     const uint64_t pol = l2_evict_first_policy();
+    pdl_trigger();
+    // the key is static: with BETA known its loads are issued before waiting for the kernel
+    // that produces the digits (complementary pipelining at kernel granularity)
+    if (BETA == 0) pdl_wait();
     uint32_t ra[W], rb[W];
 #pragma unroll
     for (int w = 0; w < W; ++w) ra[w] = rb[w] = 0;
@@ -62,6 +66,19 @@ inner_product_kernel(InnerProductArgs p, const ModSlot* __restrict__ slots) {
                 const uint4 bv = ld_stream(reinterpret_cast<const uint4*>(kb + i), pol);
                 xa[c][0] = av.x; xa[c][W > 1 ? 1 : 0] = av.y; xa[c][W > 2 ? 2 : 0] = av.z; xa[c][W > 3 ? 3 : 0] = av.w;
                 xb[c][0] = bv.x; xb[c][W > 1 ? 1 : 0] = bv.y; xb[c][W > 2 ? 2 : 0] = bv.z; xb[c][W > 3 ? 3 : 0] = bv.w;
+            } else {
+                xa[c][0] = ka[i]; xb[c][0] = kb[i];
+            }
+        }
+        if (BETA > 0) pdl_wait();
+#pragma unroll
+        for (int c = 0; c < CH; ++c) {
+            const int t = t0 + c;
+            if (BETA == 0 && t >= beta) continue;
+            const uint32_t* dsrc = (p.carry && t == digit_of_row)
+                                       ? p.carry + (size_t)row * n
+                                       : p.raised + ((size_t)t * p.ext + row) * n;
+            if (VEC) {
                 if (p.galois) {
                     // hoisted rotation: the raised digit is read through the automorphism
                     // (sigma_k commutes with ModUp up to a multiple of the digit modulus)
@@ -73,7 +90,6 @@ inner_product_kernel(InnerProductArgs p, const ModSlot* __restrict__ slots) {
                 }
             } else {
                 d[c][0] = p.galois ? dsrc[gsrc[0]] : dsrc[i];
-                xa[c][0] = ka[i]; xb[c][0] = kb[i];
             }
         }
         if (m.fast) {
@@ -140,8 +156,8 @@ inner_product_kernel(InnerProductArgs p, const ModSlot* __restrict__ slots) {
 
 template <int BETA>
 static void inner_product_dispatch(const InnerProductArgs& a, const ModSlot* slots, dim3 grid, bool vec, cudaStream_t st) {
-    if (vec) inner_product_kernel<true, BETA><<<grid, 256, 0, st>>>(a, slots);
-    else inner_product_kernel<false, BETA><<<grid, 256, 0, st>>>(a, slots);
+    if (vec) launch_pdl(inner_product_kernel<true, BETA>, grid, dim3(256), 0, st, a, slots);
+    else launch_pdl(inner_product_kernel<false, BETA>, grid, dim3(256), 0, st, a, slots);
 }
 
 int inner_product_launch(const InnerProductArgs& a, const ModSlot* slots, cudaStream_t st) {
@@ -223,6 +239,8 @@ lane_reduce_kernel(uint4* acc0, size_t lane_stride4, int lanes, const int32_t* _
                    const ModSlot* __restrict__ slots, int ext, size_t cols4) {
     const int row = blockIdx.y % ext;
     const uint32_t q = slots[ext_slot[row]].q;
+    pdl_trigger();
+    pdl_wait();
     const size_t stride = (size_t)gridDim.x * blockDim.x;
     for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < cols4; i += stride) {
         const size_t at = (size_t)blockIdx.y * cols4 + i;
@@ -242,8 +260,8 @@ int lane_reduce_launch(uint32_t* acc0, size_t lane_stride_words, int lanes, cons
     if (n % 4 || lane_stride_words % 4) { set_last_error("lane reduction needs n %% 4 == 0"); return CKKS_ERR_UNSUPPORTED; }
     ProfScope ps("lane_reduce", st, 4.0 * n * 2 * ext * (lanes + 1));
     unsigned gx = (unsigned)((n / 4 + 255) / 256);
-    lane_reduce_kernel<<<dim3(gx, 2 * ext), 256, 0, st>>>((uint4*)acc0, lane_stride_words / 4, lanes, ext_slot,
-                                                          slots, ext, n / 4);
+    CK(launch_pdl(lane_reduce_kernel, dim3(gx, 2 * ext), dim3(256), 0, st, (uint4*)acc0, lane_stride_words / 4, lanes, ext_slot,
+                                                          slots, ext, n / 4));
     CK(cudaGetLastError());
     return CKKS_OK;
 }

@@ -127,9 +127,11 @@ ntt16_fwd_strided(const uint32_t* in, uint32_t* out, const int32_t* __restrict__
     const int c = tid % COLS, g = tid / COLS;
     const ModSlot& m = slots[row_slot[blockIdx.y]];
     const uint32_t q = m.q;
+    pdl_trigger();
     for (int i = tid; i < 256; i += 16 * COLS) s_tw[i] = m.fwd[i];
     const uint32_t* src = in + rm.in_row(blockIdx.y) * kN16 + blockIdx.x * COLS + c;
     uint32_t v[16];
+    pdl_wait();
 #pragma unroll
     for (int k = 0; k < 16; ++k) v[k] = src[(g + 16 * k) * 256];
     __syncthreads();
@@ -157,9 +159,11 @@ ntt16_inv_strided(const uint32_t* in, uint32_t* out, const int32_t* __restrict__
     const int c = tid % COLS, g = tid / COLS;
     const ModSlot& m = slots[row_slot[blockIdx.y]];
     const uint32_t q = m.q;
+    pdl_trigger();
     for (int i = tid; i < 256; i += 16 * COLS) s_tw[i] = m.inv[i];
     const uint32_t* src = in + rm.in_row(blockIdx.y) * kN16 + blockIdx.x * COLS + c;
     uint32_t v[16];
+    pdl_wait();
 #pragma unroll
     for (int k = 0; k < 16; ++k) v[k] = src[(16 * g + k) * 256];
     __syncthreads();
@@ -252,6 +256,7 @@ ntt16_fwd_contig(const uint32_t* in, uint32_t* out, const int32_t* __restrict__ 
     const uint32_t B = blockIdx.x * 16 + blk;          // 256-element block index within the limb
     const int ep_row = EPI ? blockIdx.y % ep.l : 0, ep_half = EPI ? blockIdx.y / ep.l : 0;
     const size_t ep_at = (size_t)ep_row * kN16 + B * 256 + 16 * e;
+    pdl_trigger();
     if (EPI) {
         // x_Q (and the folded polynomial) are needed only after the last stage: pull their
         // lines into L2 now
@@ -270,6 +275,7 @@ ntt16_fwd_contig(const uint32_t* in, uint32_t* out, const int32_t* __restrict__ 
     Tw15 tw;
     load_tw15(fwd, (256 + B) * 16 + e, tw);
     uint32_t v[16];
+    pdl_wait();
 #pragma unroll
     for (int k = 0; k < 16; ++k) v[k] = src[e + 16 * k];
     __syncwarp();
@@ -330,6 +336,7 @@ ntt16_inv_contig(const uint32_t* in, uint32_t* out, const int32_t* __restrict__ 
     const uint32_t B = blockIdx.x * 16 + blk;
     const uint32_t* src = in + rm.in_row(blockIdx.y) * kN16 + B * 256 + 16 * e;
     const uint2* __restrict__ inv = m.inv;
+    pdl_trigger();
     if (e < 15) {
         // stage s of 4..7 has (8 >> s) groups
         const int st = e < 8 ? 0 : (e < 12 ? 1 : (e < 14 ? 2 : 3));
@@ -339,6 +346,7 @@ ntt16_inv_contig(const uint32_t* in, uint32_t* out, const int32_t* __restrict__ 
     Tw15 tw;
     load_tw15(inv, (256 + B) * 16 + e, tw);
     uint32_t v[16];
+    pdl_wait();
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
         uint32_t r[8];
@@ -415,20 +423,20 @@ int ntt_launch(const uint32_t* in, uint32_t* out, const int32_t* row_slot, const
         const RowMap rm2{rm.out, rm.out};
         if (!inverse) {
             { ProfScope ps("ntt16_fwd_strided", st, 8.0 * rows * kN16);
-              ntt16_fwd_strided<COLS><<<g_str, 16 * COLS, 0, st>>>(in, out, row_slot, slots, rm); }
+              CK(launch_pdl(ntt16_fwd_strided<COLS>, g_str, dim3(16 * COLS), 0, st, in, out, row_slot, slots, rm)); }
             if (epi) {
                 // reads conv + x_Q (+ fold), writes the result: (3 or 4) limbs per row
                 ProfScope ps("ntt16_fwd_contig_moddown", st, 4.0 * rows * kN16 * (epi->fold_b ? 3.5 : 3.0));
-                ntt16_fwd_contig<true><<<g_con, 256, 0, st>>>(out, out, row_slot, slots, rm2, *epi);
+                CK(launch_pdl(ntt16_fwd_contig<true>, g_con, dim3(256), 0, st, out, out, row_slot, slots, rm2, *epi));
             } else {
                 ProfScope ps("ntt16_fwd_contig", st, 8.0 * rows * kN16);
-                ntt16_fwd_contig<false><<<g_con, 256, 0, st>>>(out, out, row_slot, slots, rm2, ModDownEpilogueArgs{});
+                CK(launch_pdl(ntt16_fwd_contig<false>, g_con, dim3(256), 0, st, out, out, row_slot, slots, rm2, ModDownEpilogueArgs{}));
             }
         } else {
             { ProfScope ps("ntt16_inv_contig", st, 8.0 * rows * kN16);
-              ntt16_inv_contig<<<g_con, 256, 0, st>>>(in, out, row_slot, slots, rm); }
+              CK(launch_pdl(ntt16_inv_contig, g_con, dim3(256), 0, st, in, out, row_slot, slots, rm)); }
             { ProfScope ps("ntt16_inv_strided", st, 8.0 * rows * kN16);
-              ntt16_inv_strided<COLS><<<g_str, 16 * COLS, 0, st>>>(out, out, row_slot, slots, rm2); }
+              CK(launch_pdl(ntt16_inv_strided<COLS>, g_str, dim3(16 * COLS), 0, st, out, out, row_slot, slots, rm2)); }
         }
         CK(cudaGetLastError());
         return CKKS_OK;

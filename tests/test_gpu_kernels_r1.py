@@ -1,0 +1,142 @@
+"""Parity of the kernel variants added after the first CUDA path: the FP64 tensor-core
+(DMMA) base conversion at ragged shapes, the multi-output fused inner sums, the ModDown
+epilogue fused into the last NTT kernel, and the table-twiddle contiguous NTT phase.  All
+integer work: bit-exact against the CPU oracle or against the unfused CUDA composition."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def env(golden):
+    import torch
+
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    from paper_2512_18345_b200 import baseconv, keyswitch, params, rns
+    from paper_2512_18345_b200.engine import get_engine
+
+    class NS:
+        pass
+
+    ns = NS()
+    ns.torch, ns.baseconv, ns.ks, ns.rns, ns.eng = torch, baseconv, keyswitch, rns, get_engine()
+    ns.ks48 = params.ParameterSet.from_dict(golden["params"]["ks48"])
+    return ns
+
+
+def qs(basis):
+    return [m.q for m in basis]
+
+
+def rand_rows(basis, cols, rng):
+    return np.stack([rng.integers(0, m.q, cols, dtype=np.uint64) for m in basis])
+
+
+# l_in not a multiple of 4 (K padding), l_out not a multiple of 8 (M padding), l_out large enough
+# to be split over blockIdx.z, column counts that are / are not multiples of 16 (DMMA vs integer path)
+@pytest.mark.parametrize("l_in,l_out,cols", [
+    (1, 5, 65536), (2, 9, 4096), (3, 8, 65536), (5, 17, 1024), (7, 30, 65536), (12, 48, 65536),
+    (13, 33, 2048), (14, 46, 65536), (16, 44, 512), (12, 36, 48), (12, 36, 1000), (9, 3, 16),
+])
+def test_bconv_shapes_match_oracle(env, oracle_mod, l_in, l_out, cols):
+    p = env.ks48
+    ext = p.ext_basis
+    src, dst = ext[:l_in], ext[l_in:l_in + l_out]
+    assert len(dst) == l_out
+    table = env.baseconv.build_bconv_table(src, dst)
+    rng = np.random.default_rng(1000 * l_in + l_out)
+    x = rand_rows(src, cols, rng)
+    # edge columns: all-zero and all-maximal residues
+    x[:, 0] = 0
+    x[:, -1] = [m.q - 1 for m in src]
+    got = env.baseconv.convert(env.rns.Polynomial(src, x, env.rns.COEFFICIENT), table).coeffs
+    want = oracle_mod.bconv(qs(src), qs(dst), x)
+    assert np.array_equal(got, want)
+
+
+def test_stage1_stacked_conversions_match_plain_calls(env):
+    """The stacked conversions of key-switch stage 1 (all digits in one launch, outputs written
+    through row maps into the raised layout) agree with one plain convert() call per digit."""
+    p = env.ks48
+    tabs = env.ks._tables(p)
+    rng = np.random.default_rng(77)
+    coeff = rand_rows(p.q_basis, p.n, rng)
+    poly = env.rns.Polynomial(p.q_basis, coeff, env.rns.COEFFICIENT)
+    from paper_2512_18345_b200.transform import ntt_polynomial
+
+    ev = ntt_polynomial(poly, "forward")
+    raised = env.ks.keyswitch_stage1(ev, p)
+    for t in range(p.dnum):
+        digit = p.q_basis[p.digit_slice(t)]
+        x = coeff[p.digit_slice(t)]
+        conv = env.baseconv.convert(env.rns.Polynomial(digit, x, env.rns.COEFFICIENT), tabs.raise_tables[t])
+        want = ntt_polynomial(conv, "forward").coeffs
+        rows = [i for i, m in enumerate(p.ext_basis) if m not in digit]
+        assert np.array_equal(raised[t].coeffs[rows], want)
+
+
+def test_fused_terms_multi_matches_single(env):
+    eng, torch, p = env.eng, env.torch, env.ks48
+    rows, n = 9, p.n
+    basis = p.ext_basis[:rows]
+    slots = eng.row_slots(basis)
+    rng = np.random.default_rng(5)
+
+    def rnd(*lead):
+        return eng.upload(np.stack([rng.integers(0, m.q, (*lead, n), dtype=np.uint64) for m in basis], axis=len(lead))
+                          .reshape(*lead, rows, n))
+
+    for nb, ng in ((1, 1), (3, 2), (5, 5), (16, 4), (7, 8)):
+        xs = [rnd(2) for _ in range(nb)]
+        table = [[rnd() if (g + b) % 5 != 3 else None for b in range(nb)] for g in range(ng)]
+        outs = eng.fused_terms_multi(xs, table, slots)
+        for g in range(ng):
+            present = [b for b in range(nb) if table[g][b] is not None]
+            if present:
+                want = eng.fused_terms([xs[b] for b in present], [table[g][b] for b in present], slots)
+            else:
+                want = torch.zeros_like(xs[0])
+            assert torch.equal(outs[g], want), (nb, ng, g)
+
+
+def test_fused_moddown_epilogue_matches_reference_composition(env, oracle_mod):
+    """keyswitch_stage3 (iNTT -> BConv -> NTT with the ModDown epilogue applied inside the last
+    NTT kernel) against the oracle's stage 3 on the same accumulators, at N = 2^16."""
+    from oracle import oracle
+
+    p = env.ks48
+    rng = np.random.default_rng(11)
+    ext = p.ext_basis
+    acc = [rand_rows(ext, p.n, rng) for _ in range(2)]
+    L = p.l
+
+    def pair(lo, hi):
+        basis = ext[lo:hi]
+        return env.ks.PolyPair(a=env.rns.Polynomial(basis, acc[0][lo:hi], env.rns.EVALUATION),
+                               b=env.rns.Polynomial(basis, acc[1][lo:hi], env.rns.EVALUATION))
+
+    got = env.ks.keyswitch_stage3(pair(0, L), pair(L, L + p.alpha), p)
+    op = oracle.OParams(p.n, p.l, p.dnum, p.alpha, p.delta, p.h_dense,
+                        tuple((m.q, m.psi) for m in p.q_basis), tuple((m.q, m.psi) for m in p.p_basis))
+    orc = oracle.Oracle(p.n, op.ext_basis)
+    want_a = orc.ks_moddown(op, acc[0][:L], acc[0][L:])
+    want_b = orc.ks_moddown(op, acc[1][:L], acc[1][L:])
+    assert np.array_equal(got.a.coeffs, want_a) and np.array_equal(got.b.coeffs, want_b)
+
+
+def test_ntt_phases_compose_and_invert_at_2_16(env):
+    """The two fast kernels of each direction, run one at a time through ntt_stages, equal the
+    whole transform; forward then inverse is the identity (table twiddles, 256-bit accesses)."""
+    eng, torch, p = env.eng, env.torch, env.ks48
+    basis = p.ext_basis
+    slots = eng.row_slots(basis, p.n)
+    rng = np.random.default_rng(21)
+    x = eng.upload(rand_rows(basis, p.n, rng))
+    fwd = eng.ntt(x, slots, False)
+    half = eng.ntt_stages(x, slots, False, 0, 8)
+    assert torch.equal(eng.ntt_stages(half, slots, False, 8, 16), fwd)
+    back = eng.ntt(fwd, slots, True)
+    assert torch.equal(back, x)
+    half = eng.ntt_stages(fwd, slots, True, 0, 8)
+    assert torch.equal(eng.ntt_stages(half, slots, True, 8, 16), x)
