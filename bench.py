@@ -54,7 +54,7 @@ UNIT = {"bootstrap": "bootstraps/s", "keyswitch": "keyswitch/s", "ntt": "ntt/s"}
 CONFIG = {
     "bootstrap": {"workload": "full CKKS bootstrapping, 2^15 complex slots, N=2^16, ks48 moduli (L=48 31-bit "
                               "limbs, alpha=12, dnum=4), sparse secret h=32, input level 2 scale 2^52, "
-                              "output level 18; one ciphertext per step, CUDA-graph replay with 4 stream lanes",
+                              "output level 18; one ciphertext per step, CUDA-graph replay with {lanes} stream lanes",
                   "l2_policy": "each step streams ~8 GB of keys and plaintext diagonals (>> 126 MB L2)"},
     "keyswitch": {"workload": "keyswitch ks48 (N=2^16, L=48, alpha=12, dnum=4, 31-bit primes), one ciphertext per step",
                   "l2_policy": "inputs rotate through >126 MB"},
@@ -121,6 +121,20 @@ class ClockSampler:
         med = float(np.median(self.samples)) if self.samples else None
         return {"sm_mhz": med, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
                 "samples": len(self.samples)}
+
+
+def measured_traffic(workload, kernel):
+    """DRAM bytes per launch (dram__bytes_read.sum + dram__bytes_write.sum) of `kernel` from the
+    committed ncu capture of this same workload (profiles/traffic_<workload>.json, written from
+    an ncu run of `bench.py --steps 1`; ncu numbers are never taken inside a timed run)."""
+    path = ROOT / "profiles" / f"traffic_{workload}.json"
+    if not path.exists():
+        return None, None
+    doc = json.loads(path.read_text())
+    for name, rec in doc.get("kernels", {}).items():
+        if name.startswith(kernel):
+            return (rec["dram_read_mb_per_launch"] + rec["dram_write_mb_per_launch"]) * 1e6, doc.get("source")
+    return None, None
 
 
 def read_profile(eng):
@@ -402,9 +416,10 @@ def run_b200(args):
     peak, peak_src = load_peaks()
     cnt, ms_top, bytes_top = prof[top]
     achieved = bytes_top / (ms_top * 1e-3) / 1e9
+    traffic, traffic_src = measured_traffic(wl, top)
     roofline = {
         "bound": "hbm", "kernel": top, "achieved": achieved, "peak": peak, "unit": "GB/s",
-        "frac": achieved / peak, "traffic": None, "peak_source": peak_src,
+        "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src, "peak_source": peak_src,
         "avg_launch_us": ms_top / cnt * 1e3, "alg_bytes_per_launch": bytes_top / cnt,
         "share_of_step": ms_top / total_prof_ms,
         "note": "achieved = algorithmic bytes (operand limbs read+written once) / CUDA-event time of the "
@@ -425,7 +440,7 @@ def run_b200(args):
             "metric": METRIC[wl], "value": value, "unit": UNIT[wl], "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
-            "data": "synthetic", "config": CONFIG[wl],
+            "data": "synthetic", "config": {k: v.format(lanes=args.lanes) for k, v in CONFIG[wl].items()},
             "e2e": {"value": e2e_value, "unit": UNIT[wl], "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms / e2e_steps},
             "gpu_launches": int(round(launches_per_step * args.steps)),
@@ -448,7 +463,7 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--workload", default="bootstrap", choices=["bootstrap", "keyswitch", "ntt"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--lanes", type=int, default=4, help="workspace lanes / side streams of the bootstrap graph")
+    ap.add_argument("--lanes", type=int, default=8, help="workspace lanes / side streams of the bootstrap graph")
     args = ap.parse_args()
     if args.steps is None:
         args.steps = DEFAULT_STEPS[args.workload]
