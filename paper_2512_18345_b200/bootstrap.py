@@ -287,7 +287,12 @@ class Bootstrapper:
     refreshes a level-2 ciphertext of scale 2^log_delta_in to `out_level` limbs."""
 
     def __init__(self, params: ParameterSet, sk: ks.SecretKey, config: BootstrapConfig | None = None,
-                 seed: int = 7000):
+                 seed: int = 7000, sk_sparse: ks.SecretKey | None = None):
+        """`sk` is the key the ciphertexts live under and every evaluation key is generated
+        for.  With `sk_sparse` (sparse-secret encapsulation, PAPER.md / ks48.json h_sparse):
+        `sk` may be dense; the input is key-switched to `sk_sparse` on its two bottom limbs,
+        raised there (so that |I| stays within k_bound), and switched back to `sk` at the
+        top level: two extra key switches, one of them on two limbs only."""
         self.params, self.cfg = params, config or BootstrapConfig()
         cfg = self.cfg
         n = params.n // 2
@@ -323,6 +328,10 @@ class Bootstrapper:
         # ---- keys -----------------------------------------------------------------
         self.keys = ckks.EvaluationKeys(params, relin=ckks.relin_keygen(sk, params, seed=seed))
         self.keys.add_conjugation(sk, seed=seed + 1)
+        self.to_sparse = self.to_dense = None
+        if sk_sparse is not None:
+            self.to_sparse = ks.switching_keygen(sk, sk_sparse, params, seed=seed + 900_001)
+            self.to_dense = ks.switching_keygen(sk_sparse, sk, params, seed=seed + 900_002)
         rots = set()
         for lt in self.cts + self.stc:
             rots |= lt.rotations()
@@ -498,7 +507,12 @@ class Bootstrapper:
     def bootstrap(self, ct):
         if not ckks._close(ct.scale, self.delta_in):
             raise RnsError(f"bootstrap expects scale 2^{self.cfg.log_delta_in}, got {ct.scale}")
+        if self.to_sparse is not None:
+            ct = ckks.keyswitch_level(ct, self.to_sparse)       # two limbs: cheap
         raised = self.mod_raise(ct)
+        if self.to_dense is not None:
+            back = ckks.keyswitch_level(ckks.Ciphertext(raised.a, raised.b, raised.scale), self.to_dense)
+            raised = ckks.Ciphertext(a=back.a, b=back.b, scale=raised.scale)
         lo, hi = self.coeff_to_slot(raised)
         # (Q0 / (2*pi*Delta)) * sin(theta) = kappa * (E - conj E),  kappa = Q0 / (4*pi*i*Delta)
         kappa = self.q0 / (4.0 * math.pi * self.delta_in) / 1j

@@ -77,3 +77,28 @@ def test_bootstrap_rejects_wrong_inputs(boot_env):
         boot.bootstrap(ckks.encrypt(ckks.encode(z, p, level=3, scale=boot.delta_in), sk, p, seed=1))
     with pytest.raises(RnsError):
         boot.bootstrap(ckks.encrypt(ckks.encode(z, p, level=2, scale=2.0 ** 40), sk, p, seed=1))
+
+
+def test_sparse_secret_encapsulation(boot_env):
+    """Dense application key (h = 512), sparse key (h = 32) only around ModRaise: same
+    precision bar, and the raised ciphertext decrypts under the dense key."""
+    ckks, p, _sk, _boot = boot_env
+    from paper_2512_18345_b200 import keyswitch as ks
+    from paper_2512_18345_b200.bootstrap import BootstrapConfig, Bootstrapper
+
+    dense = ks.keygen(p, h=512, seed=11)
+    sparse = ks.keygen(p, h=p.h_sparse, seed=12)
+    boot = Bootstrapper(p, dense, BootstrapConfig(), sk_sparse=sparse)
+    rng = np.random.default_rng(4)
+    n = p.n // 2
+    z = rng.uniform(-1, 1, n) + 1j * rng.uniform(-1, 1, n)
+    ct = ckks.encrypt(ckks.encode(z, p, level=2, scale=boot.delta_in), dense, p, seed=6)
+    out = boot.bootstrap(ct)
+    assert ckks.level_of(out) == boot.out_level
+    err = np.abs(ckks.decrypt_decode(out, dense, p) - z).max()
+    assert err < 2.0 ** -20, f"encapsulated bootstrap precision 2^{math.log2(err):.1f}"
+    # without encapsulation the dense key pushes |I| past the EvalMod range and precision collapses
+    # (measured 2^-13 against 2^-20 and better with the sparse key around ModRaise)
+    plain = Bootstrapper(p, dense, BootstrapConfig())
+    bad = np.abs(ckks.decrypt_decode(plain.bootstrap(ct), dense, p) - z).max()
+    assert bad > 2.0 ** -17 and bad > 8 * err, (bad, err)
