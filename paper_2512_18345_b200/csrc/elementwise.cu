@@ -301,15 +301,13 @@ fused_terms_multi_kernel(FusedMulti a, const int32_t* __restrict__ row_slot,
     if (i >= cols2) return;
     const size_t at = row * cols2 + i;
     const uint64_t pol = l2_evict_first_policy();
+    // 64-bit accumulators only: after every chunk of four terms a sum is folded to its residue
+    // and carried as the seed of the next chunk (4 (q-1)^2 + q < 2^64 for q < 2^31), which
+    // leaves the registers to keep a whole chunk of loads in flight
     uint64_t sa[NG][2], sb[NG][2];
-    uint32_t ra[NG][2], rb[NG][2];
 #pragma unroll
-    for (int g = 0; g < NG; ++g) {
-        sa[g][0] = sa[g][1] = sb[g][0] = sb[g][1] = 0;
-        ra[g][0] = ra[g][1] = rb[g][0] = rb[g][1] = 0;
-    }
+    for (int g = 0; g < NG; ++g) sa[g][0] = sa[g][1] = sb[g][0] = sb[g][1] = 0;
     for (int b0 = 0; b0 < a.nb; b0 += 4) {
-        // four 62-bit products fit a 64-bit accumulator: fold after every chunk of four terms
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
             const int b = b0 + c;
@@ -330,17 +328,16 @@ fused_terms_multi_kernel(FusedMulti a, const int32_t* __restrict__ row_slot,
         for (int g = 0; g < NG; ++g) {
 #pragma unroll
             for (int k = 0; k < 2; ++k) {
-                ra[g][k] = add_mod(ra[g][k], reduce64(sa[g][k], m), m.q);
-                rb[g][k] = add_mod(rb[g][k], reduce64(sb[g][k], m), m.q);
-                sa[g][k] = sb[g][k] = 0;
+                sa[g][k] = m.fast ? reduce64(sa[g][k], m) : sa[g][k] % m.q;
+                sb[g][k] = m.fast ? reduce64(sb[g][k], m) : sb[g][k] % m.q;
             }
         }
     }
 #pragma unroll
     for (int g = 0; g < NG; ++g) {
         uint2* o = reinterpret_cast<uint2*>(a.out[g]);
-        o[at] = make_uint2(ra[g][0], ra[g][1]);
-        o[half + at] = make_uint2(rb[g][0], rb[g][1]);
+        o[at] = make_uint2((uint32_t)sa[g][0], (uint32_t)sa[g][1]);
+        o[half + at] = make_uint2((uint32_t)sb[g][0], (uint32_t)sb[g][1]);
     }
 }
 
