@@ -288,18 +288,51 @@ def _drop_plain(pt: Plaintext, level: int) -> Polynomial:
     return pt.poly if pt.level == level else pt.poly.rows(slice(0, level))
 
 
+def _halves(ct: Ciphertext):
+    """The [2, l, n] allocation behind a kernel-produced ciphertext, or None when its halves
+    are separate tensors."""
+    a, b = ct.a.data, ct.b.data
+    base = getattr(a, "_base", None)
+    if base is not None and base is getattr(b, "_base", None) and base.dim() == 3 and base.shape[0] == 2 \
+            and base.data_ptr() == a.data_ptr() and a.data_ptr() + a.numel() * 4 == b.data_ptr():
+        return base
+    return None
+
+
+def _both_halves(x: Ciphertext, y: Ciphertext, kind: str, scale: float) -> Ciphertext:
+    """x (op) y on both halves.  When both operands are single [2, l, n] allocations this is
+    one launch over 2 l rows and the result is again one allocation (so that the next tensor /
+    key switch reads it without a gathering copy); otherwise one launch per half
+    (poly_elementwise "add" / "sub", rns.py:243-258)."""
+    xt, yt = _halves(x), _halves(y)
+    if xt is None or yt is None or x.a.domain != y.a.domain or x.a.domain != x.b.domain:
+        return Ciphertext(a=poly_elementwise(x.a, y.a, kind), b=poly_elementwise(x.b, y.b, kind), scale=scale)
+    from .engine import get_engine
+    from .instrument import counters
+    from .rns import _KIND_CODE
+
+    eng = get_engine()
+    level, n = xt.shape[1], xt.shape[2]
+    out = eng.empty(2, level, n)
+    eng.elementwise(xt.view(2 * level, n), yt.view(2 * level, n), eng.row_slots(x.a.basis, repeat=2),
+                    _KIND_CODE[kind], out=out.view(2 * level, n))
+    counters.elementwise += 2 * level * n
+    return Ciphertext(a=Polynomial(x.a.basis, out[0], x.a.domain), b=Polynomial(x.a.basis, out[1], x.a.domain),
+                      scale=scale)
+
+
 def add(x: Ciphertext, y: Ciphertext) -> Ciphertext:
     _same_level(x.a, y.a)
     if not _close(x.scale, y.scale):
         raise RnsError(f"scale mismatch in add: {x.scale} vs {y.scale}")
-    return Ciphertext(a=poly_elementwise(x.a, y.a, "add"), b=poly_elementwise(x.b, y.b, "add"), scale=x.scale)
+    return _both_halves(x, y, "add", x.scale)
 
 
 def sub(x: Ciphertext, y: Ciphertext) -> Ciphertext:
     _same_level(x.a, y.a)
     if not _close(x.scale, y.scale):
         raise RnsError(f"scale mismatch in sub: {x.scale} vs {y.scale}")
-    return Ciphertext(a=poly_elementwise(x.a, y.a, "sub"), b=poly_elementwise(x.b, y.b, "sub"), scale=x.scale)
+    return _both_halves(x, y, "sub", x.scale)
 
 
 def add_plain(ct: Ciphertext, pt: Plaintext) -> Ciphertext:
@@ -311,6 +344,18 @@ def add_plain(ct: Ciphertext, pt: Plaintext) -> Ciphertext:
 def mul_plain(ct: Ciphertext, pt: Plaintext) -> Ciphertext:
     """PMult: slot-wise product with an encoded plaintext; scales multiply."""
     p = _drop_plain(pt, level_of(ct))
+    xt = _halves(ct)
+    if xt is not None and ct.a.domain == EVALUATION and p.domain == EVALUATION and ct.a.n % 4 == 0 \
+            and tuple(m.q for m in p.basis) == tuple(m.q for m in ct.a.basis):
+        # both halves against the same plaintext in one pass, result in one allocation
+        from .engine import get_engine
+        from .instrument import counters
+
+        eng = get_engine()
+        out = eng.fused_terms([xt], [p.data], eng.row_slots(ct.a.basis))
+        counters.elementwise += 2 * xt.shape[1] * xt.shape[2]
+        return Ciphertext(a=Polynomial(ct.a.basis, out[0], EVALUATION), b=Polynomial(ct.a.basis, out[1], EVALUATION),
+                          scale=ct.scale * pt.scale)
     return Ciphertext(a=poly_elementwise(ct.a, p, "mul"), b=poly_elementwise(ct.b, p, "mul"),
                       scale=ct.scale * pt.scale)
 
@@ -320,12 +365,8 @@ def ct_tensor(ct: Ciphertext):
     of one allocation, as every kernel-produced ciphertext is; a copy otherwise)."""
     import torch
 
-    a, b = ct.a.data, ct.b.data
-    base = getattr(a, "_base", None)
-    if base is not None and base is getattr(b, "_base", None) and base.dim() == 3 and base.shape[0] == 2 \
-            and base.data_ptr() == a.data_ptr() and a.data_ptr() + a.numel() * 4 == b.data_ptr():
-        return base
-    return torch.stack([a, b])
+    base = _halves(ct)
+    return base if base is not None else torch.stack([ct.a.data, ct.b.data])
 
 
 def ct_from_tensor(t, basis, scale) -> Ciphertext:

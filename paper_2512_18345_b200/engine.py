@@ -151,8 +151,8 @@ class Engine:
         return fwd, inv, n_inv.value
 
     # ---- kernels ----------------------------------------------------------
-    def elementwise(self, a, b, row_slot, kind: int):
-        out = self.torch.empty_like(a)
+    def elementwise(self, a, b, row_slot, kind: int, out=None):
+        out = self.torch.empty_like(a) if out is None else out
         _lib.check(self.lib.ckks_elementwise(self.ctx, a.data_ptr(), b.data_ptr(), out.data_ptr(),
                                              row_slot.data_ptr(), a.shape[0], a.shape[1], kind,
                                              self.stream()))
