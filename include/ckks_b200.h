@@ -144,6 +144,11 @@ int ckks_fused_terms_multi(ckks_ctx* ctx, int nb, int ng, const uint32_t* const*
  * (b1*b2, a1*b2 + a2*b1, a1*a2). */
 int ckks_tensor(ckks_ctx* ctx, const uint32_t* x, const uint32_t* y, uint32_t* out,
                 const int32_t* row_slot, int rows, size_t cols, void* stream);
+/* Same with the four halves as separate [rows][cols] matrices (ciphertexts whose a and b parts
+ * are views of larger allocations, e.g. after dropping limbs). */
+int ckks_tensor_halves(ckks_ctx* ctx, const uint32_t* xa, const uint32_t* xb, const uint32_t* ya,
+                       const uint32_t* yb, uint32_t* out, const int32_t* row_slot, int rows, size_t cols,
+                       void* stream);
 
 /* ---- base conversion: baseconv.py:57-151 ------------------------------------ */
 

@@ -385,7 +385,7 @@ def tensor(x: Ciphertext, y: Ciphertext):
         d0 = poly_elementwise(x.b, y.b, "mul")
         d1 = poly_elementwise(poly_elementwise(x.a, y.b, "mul"), poly_elementwise(y.a, x.b, "mul"), "add")
         return d0, d1, poly_elementwise(x.a, y.a, "mul")
-    d = eng.tensor(ct_tensor(x), ct_tensor(y), eng.row_slots(basis))
+    d = eng.tensor_halves(x.a.data, x.b.data, y.a.data, y.b.data, eng.row_slots(basis))
     return tuple(Polynomial(basis, d[i], EVALUATION) for i in range(3))
 
 
@@ -435,7 +435,7 @@ def hmult_rescale(x: Ciphertext, y: Ciphertext, rlk: ks.SwitchingKey, k: int = 1
     if tuple(m.q for m in basis) != tuple(m.q for m in params.q_basis[:level]):
         raise StructureError("ciphertext basis is not a prefix of the parameter q-basis")
     rest, dropped = basis[:level - k], basis[level - k:]
-    d = eng.tensor(ct_tensor(x), ct_tensor(y), eng.row_slots(basis))
+    d = eng.tensor_halves(x.a.data, x.b.data, y.a.data, y.b.data, eng.row_slots(basis))
     ks_plan = eng.ks_plan(n, basis, params.p_basis, params.alpha, params.l + params.alpha, params.l)
     md_plan = eng.moddown_plan(n, rest, dropped + params.p_basis)
     out = eng.ks_relin_rescale(ks_plan, md_plan, d, rlk.matrix(), level - k)

@@ -497,7 +497,15 @@ int ckks_fused_terms_multi(ckks_ctx* ctx, int nb, int ng, const uint32_t* const*
 int ckks_tensor(ckks_ctx* ctx, const uint32_t* x, const uint32_t* y, uint32_t* out,
                 const int32_t* row_slot, int rows, size_t cols, void* stream) {
     CKS(check_ctx(ctx));
-    return tensor_launch(x, y, out, row_slot, ctx->d_slots, rows, cols, (cudaStream_t)stream);
+    const size_t half = (size_t)rows * cols;
+    return tensor_launch(x, x + half, y, y + half, out, row_slot, ctx->d_slots, rows, cols, (cudaStream_t)stream);
+}
+
+int ckks_tensor_halves(ckks_ctx* ctx, const uint32_t* xa, const uint32_t* xb, const uint32_t* ya,
+                       const uint32_t* yb, uint32_t* out, const int32_t* row_slot, int rows, size_t cols,
+                       void* stream) {
+    CKS(check_ctx(ctx));
+    return tensor_launch(xa, xb, ya, yb, out, row_slot, ctx->d_slots, rows, cols, (cudaStream_t)stream);
 }
 
 // ---- base conversion ------------------------------------------------------------------

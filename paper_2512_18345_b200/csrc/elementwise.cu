@@ -363,12 +363,12 @@ int fused_terms_multi_launch(const FusedMulti& a, const int32_t* row_slot, const
 }
 
 // Tensor product of two ciphertexts in one pass (the front of HMult):
-// d0 = b1*b2, d1 = a1*b2 + a2*b1, d2 = a1*a2; x, y are [2][rows][n] (a then b),
-// out is [3][rows][n] (d0, d1, d2).
+// d0 = b1*b2, d1 = a1*b2 + a2*b1, d2 = a1*a2; the four halves are [rows][n] each (separate
+// pointers, so level-dropped views need no gathering copy), out is [3][rows][n] (d0, d1, d2).
 __global__ void __launch_bounds__(256)
-tensor_kernel(const uint4* __restrict__ x, const uint4* __restrict__ y, uint4* out,
-              const int32_t* __restrict__ row_slot, const ModSlot* __restrict__ slots, int rows,
-              size_t cols4) {
+tensor_kernel(const uint4* __restrict__ xa, const uint4* __restrict__ xb, const uint4* __restrict__ ya,
+              const uint4* __restrict__ yb, uint4* out, const int32_t* __restrict__ row_slot,
+              const ModSlot* __restrict__ slots, int rows, size_t cols4) {
     const size_t row = blockIdx.y;
     const ModSlot m = slots[row_slot[row]];
     pdl_trigger();
@@ -377,7 +377,7 @@ tensor_kernel(const uint4* __restrict__ x, const uint4* __restrict__ y, uint4* o
     const size_t stride = (size_t)gridDim.x * blockDim.x;
     for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < cols4; i += stride) {
         const size_t at = row * cols4 + i;
-        const uint4 a1 = x[at], b1 = x[half + at], a2 = y[at], b2 = y[half + at];
+        const uint4 a1 = xa[at], b1 = xb[at], a2 = ya[at], b2 = yb[at];
         const uint32_t A1[4] = {a1.x, a1.y, a1.z, a1.w}, B1[4] = {b1.x, b1.y, b1.z, b1.w};
         const uint32_t A2[4] = {a2.x, a2.y, a2.z, a2.w}, B2[4] = {b2.x, b2.y, b2.z, b2.w};
         uint32_t d0[4], d1[4], d2[4];
@@ -393,14 +393,15 @@ tensor_kernel(const uint4* __restrict__ x, const uint4* __restrict__ y, uint4* o
     }
 }
 
-int tensor_launch(const uint32_t* x, const uint32_t* y, uint32_t* out, const int32_t* row_slot,
-                  const ModSlot* slots, int rows, size_t cols, cudaStream_t st) {
+int tensor_launch(const uint32_t* xa, const uint32_t* xb, const uint32_t* ya, const uint32_t* yb,
+                  uint32_t* out, const int32_t* row_slot, const ModSlot* slots, int rows, size_t cols,
+                  cudaStream_t st) {
     if (rows <= 0 || cols == 0) return CKKS_OK;
     if (cols % 4 || rows > 65535) { set_last_error("tensor needs cols %% 4 == 0 and <= 65535 rows"); return CKKS_ERR_UNSUPPORTED; }
     ProfScope ps("tensor", st, 4.0 * cols * rows * 7.0);
     unsigned gx = (unsigned)((cols / 4 + 255) / 256);
-    CK(launch_pdl(tensor_kernel, dim3(gx, rows), dim3(256), 0, st, (const uint4*)x, (const uint4*)y, (uint4*)out, row_slot,
-                                                  slots, rows, cols / 4));
+    CK(launch_pdl(tensor_kernel, dim3(gx, rows), dim3(256), 0, st, (const uint4*)xa, (const uint4*)xb,
+                  (const uint4*)ya, (const uint4*)yb, (uint4*)out, row_slot, slots, rows, cols / 4));
     CK(cudaGetLastError());
     return CKKS_OK;
 }

@@ -113,8 +113,9 @@ struct FusedMulti {
 };
 int fused_terms_multi_launch(const FusedMulti& a, const int32_t* row_slot, const ModSlot* slots,
                              int rows, size_t cols, cudaStream_t st);
-int tensor_launch(const uint32_t* x, const uint32_t* y, uint32_t* out, const int32_t* row_slot,
-                  const ModSlot* slots, int rows, size_t cols, cudaStream_t st);
+int tensor_launch(const uint32_t* xa, const uint32_t* xb, const uint32_t* ya, const uint32_t* yb,
+                  uint32_t* out, const int32_t* row_slot, const ModSlot* slots, int rows, size_t cols,
+                  cudaStream_t st);
 
 // bconv.cu
 // Device image of one conversion table (reference baseconv.py:37-54).

@@ -235,6 +235,14 @@ class Engine:
                                         row_slot.data_ptr(), x.shape[1], x.shape[2], self.stream()))
         return out
 
+    def tensor_halves(self, xa, xb, ya, yb, row_slot):
+        """(d0, d1, d2) from four separate [rows, n] halves (no [2, rows, n] gathering copy)."""
+        out = self.empty(3, xa.shape[0], xa.shape[1])
+        _lib.check(self.lib.ckks_tensor_halves(self.ctx, xa.data_ptr(), xb.data_ptr(), ya.data_ptr(), yb.data_ptr(),
+                                               out.data_ptr(), row_slot.data_ptr(), xa.shape[0], xa.shape[1],
+                                               self.stream()))
+        return out
+
     def bconv_table(self, q_basis, p_basis) -> int:
         key = (tuple(m.q for m in q_basis), tuple(m.q for m in p_basis))
         t = self._tables.get(key)
