@@ -49,8 +49,9 @@ METRIC = {
     "bootstrap": "CKKS bootstrap throughput (2^15 slots, N=2^16); ms_per_step = bootstrap latency ms",
     "keyswitch": "hybrid key-switch throughput (CKKS HRot/relinearise core, N=2^16 L=48 dnum=4)",
     "ntt": "batched RNS NTT throughput (N=2^16, 60 limbs)",
+    "helr": "HELR-style logistic-regression iteration throughput (N=2^16, 128 samples x 256 features, level 20 -> 13)",
 }
-UNIT = {"bootstrap": "bootstraps/s", "keyswitch": "keyswitch/s", "ntt": "ntt/s"}
+UNIT = {"bootstrap": "bootstraps/s", "keyswitch": "keyswitch/s", "ntt": "ntt/s", "helr": "iterations/s"}
 CONFIG = {
     "bootstrap": {"workload": "full CKKS bootstrapping, 2^15 complex slots, N=2^16, ks48 moduli (L=48 31-bit "
                               "limbs, alpha=12, dnum=4), sparse secret h=32, input level 2 scale 2^52, "
@@ -60,8 +61,15 @@ CONFIG = {
                   "l2_policy": "inputs rotate through >126 MB"},
     "ntt": {"workload": "forward NTT of one 60-limb polynomial (ks48 extended basis) per step",
             "l2_policy": "inputs rotate through >126 MB"},
+    "helr": {"workload": "one HELR-style gradient step on ks48 moduli at 20 limbs (4 HMult+rescale, 3 PMult, 23 "
+                         "HRot, cubic sigmoid; BASELINE config 5), one CUDA-graph replay per step, {lanes} lanes",
+             "l2_policy": "each step streams ~1.5 GB of rotation / relinearisation keys (>> 126 MB L2)"},
 }
-DEFAULT_STEPS = {"bootstrap": 30, "keyswitch": 2000, "ntt": 2000}
+DEFAULT_STEPS = {"bootstrap": 30, "keyswitch": 2000, "ntt": 2000, "helr": 100}
+
+
+def config_for(workload, lanes):
+    return {k: v.format(lanes=lanes) for k, v in CONFIG[workload].items()}
 
 
 def load_peaks():
@@ -196,9 +204,15 @@ def bootstrap_keyswitch_levels():
     return levels
 
 
+# key switches of one HELR-style iteration by active limbs (paper_2512_18345_b200/helr.py):
+# relinearisations at 20, 18, 16, 15; 8 rotations at 19, 8 at 18, 7 at 14.
+def helr_keyswitch_levels():
+    return [20, 18, 16, 15] + [19] * 8 + [18] * 8 + [14] * 7
+
+
 def time_oracle(workload, steps, warmup):
     """(throughput, ms per unit, sample description) of the CPU port."""
-    base = "keyswitch" if workload == "bootstrap" else workload
+    base = "keyswitch" if workload in ("bootstrap", "helr") else workload
     step = oracle_step(base)
     for _ in range(warmup):
         step()
@@ -206,6 +220,12 @@ def time_oracle(workload, steps, warmup):
     for _ in range(steps):
         step()
     ms = (time.perf_counter() - t0) / steps * 1e3
+    if workload == "helr":
+        units = sum((-(-l // 12) + 2) * (l + 12) / 360.0 for l in helr_keyswitch_levels())
+        it_ms = ms * units
+        return 1e3 / it_ms, it_ms, (f"{steps} full-level ks48 key switches with oracle/ckks_oracle.c (OpenMP), scaled by "
+                                    f"the {units:.1f} full-level-equivalent key switches of one iteration "
+                                    "(PMult / rescale / automorphism time not included: lower bound)")
     if workload != "bootstrap":
         return 1e3 / ms, ms, f"{steps} steps of the workload, oracle/ckks_oracle.c with OpenMP"
     # a bootstrap on the CPU is dominated by its key switches; cost of one at l active limbs
@@ -228,7 +248,7 @@ def run_reference(args):
         "impl": "reference", "metric": METRIC[args.workload], "value": thr, "unit": unit,
         "n_gpus": args.gpus, "steps": steps, "warmup": warmup, "ms_per_step": ms,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
-        "data": "synthetic", "config": CONFIG[args.workload],
+        "data": "synthetic", "config": config_for(args.workload, args.lanes),
         "cpu_baseline": {"value": thr, "unit": unit, "cores": host_threads(), "kind": "port", "sample": sample},
         "e2e": {"value": thr, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -310,6 +330,59 @@ def run_b200(args):
         out = replay(cts[0])
         err = float(np.abs(ckks.decrypt_decode(out, sk, p) - msgs[0]).max())
         precision_bits = float(np.log2(err))
+    elif wl == "helr":
+        from paper_2512_18345_b200.helr import HelrShape, HelrTrainer, plain_iteration
+
+        eng.set_lanes(args.lanes)
+        sk = ks.keygen(p, h=p.h_dense, seed=1 + rank)
+        shape = HelrShape(samples=128, features=256)
+        trainer = HelrTrainer(p, sk, shape, level=20, lr=1.0)
+        rng = np.random.default_rng(rank)
+        xs = rng.uniform(-1, 1, (shape.samples, shape.features))
+        ys = np.where(rng.uniform(size=shape.samples) < 0.5, -1.0, 1.0)
+        z = (xs * ys[:, None]).reshape(-1)
+        w = np.tile(rng.uniform(-0.02, 0.02, shape.features), shape.samples)
+        ct_z, ct_w = trainer.encrypt(z, sk, seed=60), trainer.encrypt(w, sk, seed=61)
+        basis20 = ct_z.a.basis
+        static_in = torch.stack([torch.stack([c.a.data, c.b.data]) for c in (ct_z, ct_w)]).clone()   # [2, 2, 20, n]
+
+        def run_iteration():
+            cz = ckks.ct_from_tensor(static_in[0], basis20, ct_z.scale)
+            cw = ckks.ct_from_tensor(static_in[1], basis20, ct_w.scale)
+            return trainer.iteration(cz, cw)
+
+        run_iteration()
+        torch.cuda.synchronize()
+        graph = torch.cuda.CUDAGraph()
+        side = torch.cuda.Stream(device=dev)
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            run_iteration()
+            torch.cuda.synchronize()
+            with torch.cuda.graph(graph, stream=side):
+                out_ct = run_iteration()
+                static_out = torch.stack([out_ct.a.data, out_ct.b.data])
+        torch.cuda.current_stream().wait_stream(side)
+        fresh = static_in.clone()
+
+        def step(i):
+            static_in.copy_(fresh)
+            graph.replay()
+
+        profiled_step = lambda i: run_iteration()
+        host_in = [fresh.cpu().pin_memory() for _ in range(2)]
+        host_out = [torch.empty(tuple(static_out.shape), dtype=torch.int32).pin_memory() for _ in range(2)]
+
+        def e2e_step(i):
+            static_in.copy_(host_in[i % 2], non_blocking=True)
+            graph.replay()
+            host_out[i % 2].copy_(static_out, non_blocking=True)
+
+        h2d = int(fresh.numel()) * 4
+        d2h = int(static_out.numel()) * 4
+        graph.replay()
+        got = ckks.decrypt_decode(ckks.ct_from_tensor(static_out, out_ct.a.basis, out_ct.scale), sk, p).real
+        precision_bits = float(np.log2(np.abs(got - plain_iteration(z, w, shape, 1.0)).max()))
     elif wl == "keyswitch":
         n_ct, n_evk = 8, 4
         cts = [rand_limbs(p.q_basis, 2) for _ in range(n_ct)]               # 25 MB each
@@ -399,7 +472,7 @@ def run_b200(args):
     e2e_value = world * e2e_steps / (e2e_ms * 1e-3)
 
     # per-kernel pass: the same step, eager, every launch bracketed by CUDA events
-    prof_steps = max(2, min(args.steps, 3 if wl == "bootstrap" else 50))
+    prof_steps = max(2, min(args.steps, 3 if wl in ("bootstrap", "helr") else 50))
     lanes_saved = getattr(eng, "lanes", 1)
     eng.lanes = 1                      # one stream: per-kernel durations without overlap from other lanes
     profiled_step(0)
@@ -440,7 +513,7 @@ def run_b200(args):
             "metric": METRIC[wl], "value": value, "unit": UNIT[wl], "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
-            "data": "synthetic", "config": {k: v.format(lanes=args.lanes) for k, v in CONFIG[wl].items()},
+            "data": "synthetic", "config": config_for(wl, args.lanes),
             "e2e": {"value": e2e_value, "unit": UNIT[wl], "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms / e2e_steps},
             "gpu_launches": int(round(launches_per_step * args.steps)),
@@ -449,6 +522,7 @@ def run_b200(args):
         if wl == "bootstrap":
             line["latency_ms"] = ms_step
             line["paper_rtx5090_latency_ms"] = 15.2
+        if precision_bits is not None:
             line["precision_log2_max_err"] = precision_bits
         print(json.dumps(line))
     if world > 1:
@@ -461,14 +535,14 @@ def main():
     ap.add_argument("--steps", type=int, default=None)
     ap.add_argument("--warmup", type=int, default=None)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--workload", default="bootstrap", choices=["bootstrap", "keyswitch", "ntt"])
+    ap.add_argument("--workload", default="bootstrap", choices=["bootstrap", "keyswitch", "ntt", "helr"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--lanes", type=int, default=8, help="workspace lanes / side streams of the bootstrap graph")
     args = ap.parse_args()
     if args.steps is None:
         args.steps = DEFAULT_STEPS[args.workload]
     if args.warmup is None:
-        args.warmup = 3 if args.workload == "bootstrap" else 20
+        args.warmup = 3 if args.workload in ("bootstrap", "helr") else 20
     if args.impl == "reference":
         run_reference(args)
     else:
