@@ -244,6 +244,11 @@ int ckks_ks_relin_rescale(ckks_ctx* ctx, int32_t ks_plan, int32_t md_plan, const
  * up to key-switch noise. */
 int ckks_ks_accumulate(ckks_ctx* ctx, int32_t plan, const uint32_t* ct_a, const uint32_t* evk,
                        int first, void* stream);
+/* ckks_ks_accumulate for the rotation sigma_k of (ct_a, ct_b) without materialising it: the
+ * automorphism is a gather inside the inner product and P * sigma_k(ct_b) is lifted into the b
+ * accumulator (no separate automorphism pass, no separate sum of the b parts). */
+int ckks_ks_accumulate_rot(ckks_ctx* ctx, int32_t plan, const uint32_t* ct_a, const uint32_t* ct_b,
+                           uint32_t k, const uint32_t* evk, int first, void* stream);
 int ckks_ks_finish(ckks_ctx* ctx, int32_t plan, int lanes_used, const uint32_t* fold_a,
                    const uint32_t* fold_b, uint32_t* out_a, uint32_t* out_b, void* stream);
 

@@ -254,16 +254,14 @@ class LinearTransform:
                 k = ckks.galois_element(g * self.n1 * self.step, n_ring)
                 if k not in keys.galois:
                     raise RnsError(f"no Galois key for rotation {g * self.n1 * self.step}")
-                rot = eng.automorphism_eval(inners[g].view(2 * self.level, n_ring), k).view(2, self.level, n_ring)
-                eng.ks_accumulate(plan, rot[0], keys.galois[k].matrix(), first=(nth == 0))
-                return rot
+                # the rotation is never materialised: gather inside the inner product, b part lifted
+                eng.ks_accumulate_rot(plan, inners[g][0], inners[g][1], k, keys.galois[k].matrix(),
+                                      first=(nth == 0))
 
-            rots = eng.fork([(lambda lane, nth, g=g: giant(lane, nth, g)) for g in moving], with_lane=True)
+            eng.fork([(lambda lane, nth, g=g: giant(lane, nth, g)) for g in moving], with_lane=True)
             lanes_used = min(eng.lane_count(), len(moving))
-            terms = list(rots) + ([base] if base is not None else [])
-            b_sum = eng.fused_terms(terms, [None] * len(terms), slots) if len(terms) > 1 else terms[0]
-            out_t = eng.ks_finish(plan, lanes_used, None if base is None else base[0], b_sum[1],
-                                  self.level, n_ring)
+            out_t = eng.ks_finish(plan, lanes_used, None if base is None else base[0],
+                                  None if base is None else base[1], self.level, n_ring)
             total = ct_from_tensor(out_t, basis, scale)
         out = ckks.rescale(total, self.limbs)
         return ckks.Ciphertext(a=out.a, b=out.b, scale=ct.scale)

@@ -950,6 +950,29 @@ int ckks_ks_accumulate(ckks_ctx* ctx, int32_t plan, const uint32_t* ct_a, const 
     return inner_product_launch(ip, ctx->d_slots, st);
 }
 
+// Same for a ROTATED ciphertext without materialising the rotation: ModUp of the unrotated a
+// part, the automorphism applied as a gather inside the inner product (sigma_k commutes with
+// ModUp up to a multiple of the digit modulus), and P * sigma_k(ct_b) lifted into the b
+// accumulator, so the shared ModDown returns sum_g KS(sigma_g(a_g)) + sigma_g(b_g).
+int ckks_ks_accumulate_rot(ckks_ctx* ctx, int32_t plan, const uint32_t* ct_a, const uint32_t* ct_b,
+                           uint32_t k, const uint32_t* evk, int first, void* stream) {
+    KsPlan* pl;
+    CKS(get_plan(ctx, plan, &pl));
+    CKS(need_full_plan(pl));
+    if (!(k & 1)) { set_last_error("automorphism index must be odd"); return CKKS_ERR_ARG; }
+    cudaStream_t st = (cudaStream_t)stream;
+    const size_t n = pl->n;
+    CKS(stage1_core(ctx, pl, ct_a, pl->ws_raised, false, st));
+    InnerProductArgs ip = ip_args(pl, ct_a, pl->ws_raised, evk, 0, pl->ext, pl->ws_acc,
+                                  pl->ws_acc + (size_t)pl->ext * n);
+    ip.galois = k & (2 * pl->n - 1);
+    ip.lift_b = ct_b;
+    ip.pmod = pl->d_pmod;
+    ip.pmod_s = pl->d_pmod_s;
+    ip.accumulate = first ? 0 : 1;
+    return inner_product_launch(ip, ctx->d_slots, st);
+}
+
 int ckks_ks_finish(ckks_ctx* ctx, int32_t plan, int lanes_used, const uint32_t* fold_a,
                    const uint32_t* fold_b, uint32_t* out_a, uint32_t* out_b, void* stream) {
     // the accumulators of lanes [current lane, current lane + lanes_used) are summed into the

@@ -338,6 +338,12 @@ class Engine:
                                                   out[0].data_ptr(), out[1].data_ptr(), self.stream()))
         return out
 
+    def ks_accumulate_rot(self, plan: int, ct_a, ct_b, k: int, evk, first: bool):
+        """Stages 1-2 of the key switch of sigma_k(ct) into the current lane's Q||P accumulator,
+        the rotation applied as a gather (no automorphism pass), P * sigma_k(ct_b) lifted in."""
+        _lib.check(self.lib.ckks_ks_accumulate_rot(self.ctx, plan, ct_a.data_ptr(), ct_b.data_ptr(), k,
+                                                   evk.data_ptr(), int(first), self.stream()))
+
     def ks_accumulate(self, plan: int, ct_a, evk, first: bool):
         _lib.check(self.lib.ckks_ks_accumulate(self.ctx, plan, ct_a.data_ptr(), evk.data_ptr(),
                                                int(first), self.stream()))
