@@ -260,6 +260,13 @@ class LinearTransform:
 
             eng.fork([(lambda lane, nth, g=g: giant(lane, nth, g)) for g in moving], with_lane=True)
             lanes_used = min(eng.lane_count(), len(moving))
+            if n_ring % 4 == 0 and self.level > self.limbs:
+                # the shared ModDown and the rescale by the plaintext limbs as one division
+                rest, dropped = basis[:self.level - self.limbs], basis[self.level - self.limbs:]
+                md_plan = eng.moddown_plan(n_ring, rest, dropped + p.p_basis)
+                out_t = eng.ks_finish_rescale(plan, md_plan, lanes_used, None if base is None else base[0],
+                                              None if base is None else base[1], self.level - self.limbs, n_ring)
+                return ct_from_tensor(out_t, rest, ct.scale)
             out_t = eng.ks_finish(plan, lanes_used, None if base is None else base[0],
                                   None if base is None else base[1], self.level, n_ring)
             total = ct_from_tensor(out_t, basis, scale)
