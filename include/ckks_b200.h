@@ -253,12 +253,13 @@ int ckks_ks_finish(ckks_ctx* ctx, int32_t plan, int lanes_used, const uint32_t* 
                    const uint32_t* fold_b, uint32_t* out_a, uint32_t* out_b, void* stream);
 
 /* ckks_ks_finish and the rescale that follows it as one division: (fold_a, fold_b) joins the
- * accumulator times P, and `md_plan` = ckks_moddown_plan_create(Q_{l-k}, {q_{l-k}..q_{l-1}} U P)
+ * accumulator times P, raw_qp (may be NULL; a [2][l + alpha][n] accumulator already over Q||P)
+ * as it is, and `md_plan` = ckks_moddown_plan_create(Q_{l-k}, {q_{l-k}..q_{l-1}} U P)
  * divides by P * q_{l-1} ... q_{l-k}; outputs have l - k rows (same value as ks_finish +
  * rescale up to the rounding of the division). */
 int ckks_ks_finish_rescale(ckks_ctx* ctx, int32_t plan, int32_t md_plan, int lanes_used,
-                           const uint32_t* fold_a, const uint32_t* fold_b, uint32_t* out_a,
-                           uint32_t* out_b, void* stream);
+                           const uint32_t* fold_a, const uint32_t* fold_b, const uint32_t* raw_qp,
+                           uint32_t* out_a, uint32_t* out_b, void* stream);
 
 #ifdef __cplusplus
 }

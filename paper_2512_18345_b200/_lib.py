@@ -94,7 +94,7 @@ def load() -> ctypes.CDLL:
     L.ckks_ks_accumulate.argtypes = [vp, i32, vp, vp, ctypes.c_int, vp]
     L.ckks_ks_accumulate_rot.argtypes = [vp, i32, vp, vp, ctypes.c_uint32, vp, ctypes.c_int, vp]
     L.ckks_ks_finish.argtypes = [vp, i32, ctypes.c_int, vp, vp, vp, vp, vp]
-    L.ckks_ks_finish_rescale.argtypes = [vp, i32, i32, ctypes.c_int, vp, vp, vp, vp, vp]
+    L.ckks_ks_finish_rescale.argtypes = [vp, i32, i32, ctypes.c_int, vp, vp, vp, vp, vp, vp]
     for name in SYMBOLS:
         fn = getattr(L, name)
         if name not in ("ckks_last_error", "ckks_ctx_destroy"):

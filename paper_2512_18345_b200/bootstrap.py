@@ -126,6 +126,11 @@ ct_tensor = ckks.ct_tensor
 ct_from_tensor = ckks.ct_from_tensor
 
 
+def p_ok(lt) -> bool:
+    """The merged finish (ks_finish_rescale) is available: vector kernels need n % 4 == 0."""
+    return lt.double_hoist and lt.params.n % 4 == 0 and lt.level > lt.limbs
+
+
 class LinearTransform:
     """y = sum_d diag_d * rot(x, d) with offsets d = g*n1*step + b*step (mod n):
     inner_g = sum_b rot(diag_d, -g*n1*step) * rot(x, b*step);  y = sum_g rot(inner_g, g*n1*step).
@@ -211,6 +216,7 @@ class LinearTransform:
             qp = qps[g]
             return eng.ks_stage3(plan, qp[0, :level], qp[1, :level], qp[0, level:], qp[1, level:])
 
+        inner_sum.raw = qps          # the Q||P accumulators themselves (giant step 0 needs no ModDown)
         return inner_sum
 
     def rotations(self) -> set[int]:
@@ -237,9 +243,13 @@ class LinearTransform:
                 row = self.table[g]
                 return eng.fused_terms([rotated[b] for b in row], [pt.poly.data for pt in row.values()], slots)
 
-        inners = dict(zip(self.giants, eng.fork([(lambda g=g: inner_sum(g)) for g in self.giants])))
-        base = inners.get(0)
         moving = [g for g in self.giants if g]
+        # with rotated giant steps the unrotated inner sum joins their shared Q||P accumulator as
+        # it is: no ModDown of its own
+        base_raw = getattr(inner_sum, "raw", {}).get(0) if moving and p_ok(self) else None
+        todo = [g for g in self.giants if not (g == 0 and base_raw is not None)]
+        inners = dict(zip(todo, eng.fork([(lambda g=g: inner_sum(g)) for g in todo])))
+        base = inners.get(0)
         scale = ct.scale * self.pt_scale
         if not moving:
             total = ct_from_tensor(base, basis, scale)
@@ -265,7 +275,8 @@ class LinearTransform:
                 rest, dropped = basis[:self.level - self.limbs], basis[self.level - self.limbs:]
                 md_plan = eng.moddown_plan(n_ring, rest, dropped + p.p_basis)
                 out_t = eng.ks_finish_rescale(plan, md_plan, lanes_used, None if base is None else base[0],
-                                              None if base is None else base[1], self.level - self.limbs, n_ring)
+                                              None if base is None else base[1], self.level - self.limbs, n_ring,
+                                              raw_qp=base_raw)
                 return ct_from_tensor(out_t, rest, ct.scale)
             out_t = eng.ks_finish(plan, lanes_used, None if base is None else base[0],
                                   None if base is None else base[1], self.level, n_ring)

@@ -991,12 +991,13 @@ int ckks_ks_finish(ckks_ctx* ctx, int32_t plan, int lanes_used, const uint32_t* 
 }
 
 // ckks_ks_finish followed by a rescale by the top limbs, as ONE division: (fold_a, fold_b) is
-// lifted into the accumulator (times P) during the lane reduction, and the ModDown plan
+// lifted into the accumulator (times P) during the lane reduction, raw_qp (a [2][ext][n]
+// accumulator already over Q||P, e.g. the unrotated inner sum) is added as is, and the ModDown plan
 // `md_plan` (Q_{l-k} with P' = {q_{l-k}..q_{l-1}} U P, as in ckks_ks_relin_rescale) divides
 // everything by P * q_{l-1} ... q_{l-k}.  out_a / out_b have l - k rows.
 int ckks_ks_finish_rescale(ckks_ctx* ctx, int32_t plan, int32_t md_plan, int lanes_used,
-                           const uint32_t* fold_a, const uint32_t* fold_b, uint32_t* out_a,
-                           uint32_t* out_b, void* stream) {
+                           const uint32_t* fold_a, const uint32_t* fold_b, const uint32_t* raw_qp,
+                           uint32_t* out_a, uint32_t* out_b, void* stream) {
     if (!ctx || lanes_used < 1 || ctx->lane + lanes_used > ctx->lanes) { set_last_error("bad lane count %d", lanes_used); return CKKS_ERR_ARG; }
     KsPlan *pl, *md;
     CKS(get_plan(ctx, plan, &pl));
@@ -1011,7 +1012,7 @@ int ckks_ks_finish_rescale(ckks_ctx* ctx, int32_t plan, int32_t md_plan, int lan
     cudaStream_t st = (cudaStream_t)stream;
     const size_t n = pl->n;
     CKS(lane_reduce_launch(pl->ws_acc, ctx->ws_words, lanes_used, pl->d_ext_slot, ctx->d_slots, pl->ext, n, st,
-                           fold_a, fold_b, pl->d_pmod, pl->d_pmod_s, pl->l));
+                           fold_a, fold_b, pl->d_pmod, pl->d_pmod_s, pl->l, raw_qp));
     uint32_t* acc_a = pl->ws_acc;
     uint32_t* acc_b = pl->ws_acc + (size_t)pl->ext * n;
     return stage3_core(ctx, md, acc_a, acc_b, acc_a + (size_t)md->l * n, acc_b + (size_t)md->l * n,

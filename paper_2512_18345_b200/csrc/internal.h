@@ -194,6 +194,7 @@ int moddown_epilogue_launch(const ModDownEpilogueArgs& a, const ModSlot* slots, 
 int lane_reduce_launch(uint32_t* acc0, size_t lane_stride_words, int lanes, const int32_t* ext_slot,
                        const ModSlot* slots, int ext, size_t n, cudaStream_t st,
                        const uint32_t* lift_a = nullptr, const uint32_t* lift_b = nullptr,
-                       const uint32_t* pmod = nullptr, const uint32_t* pmod_s = nullptr, int l = 0);
+                       const uint32_t* pmod = nullptr, const uint32_t* pmod_s = nullptr, int l = 0,
+                       const uint32_t* raw = nullptr);
 
 }  // namespace ckks

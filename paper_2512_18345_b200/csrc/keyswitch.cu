@@ -235,12 +235,13 @@ int moddown_epilogue_launch(const ModDownEpilogueArgs& a, const ModSlot* slots, 
 // acc0 += acc1 + ... over the [2][ext][n] accumulators of several workspace lanes
 // (giant steps of a linear transform accumulate their inner products per lane); with
 // lift_a / lift_b also += (P mod q_i) * lift on the Q rows of the two halves, i.e. a ciphertext
-// that takes no key switch joins the accumulator before the shared ModDown.
+// that takes no key switch joins the accumulator before the shared ModDown; `raw` adds one more
+// [2][ext][n] accumulator that already lives over Q||P (an inner sum that is not rotated).
 __global__ void __launch_bounds__(256)
 lane_reduce_kernel(uint4* acc0, size_t lane_stride4, int lanes, const int32_t* __restrict__ ext_slot,
                    const ModSlot* __restrict__ slots, int ext, size_t cols4, const uint4* lift_a,
                    const uint4* lift_b, const uint32_t* __restrict__ pmod,
-                   const uint32_t* __restrict__ pmod_s, int l) {
+                   const uint32_t* __restrict__ pmod_s, int l, const uint4* raw) {
     const int row = blockIdx.y % ext;
     const int half = blockIdx.y / ext;
     const uint32_t q = slots[ext_slot[row]].q;
@@ -258,6 +259,11 @@ lane_reduce_kernel(uint4* acc0, size_t lane_stride4, int lanes, const int32_t* _
             r.x = add_mod(r.x, v.x, q); r.y = add_mod(r.y, v.y, q);
             r.z = add_mod(r.z, v.z, q); r.w = add_mod(r.w, v.w, q);
         }
+        if (raw) {                 // a [2][ext][n] accumulator that is already over Q||P
+            const uint4 v = raw[at];
+            r.x = add_mod(r.x, v.x, q); r.y = add_mod(r.y, v.y, q);
+            r.z = add_mod(r.z, v.z, q); r.w = add_mod(r.w, v.w, q);
+        }
         if (lifted) {
             const uint4 v = lift[(size_t)row * cols4 + i];
             r.x = add_mod(r.x, shoup_mul(v.x, pm, pms, q), q); r.y = add_mod(r.y, shoup_mul(v.y, pm, pms, q), q);
@@ -269,13 +275,14 @@ lane_reduce_kernel(uint4* acc0, size_t lane_stride4, int lanes, const int32_t* _
 
 int lane_reduce_launch(uint32_t* acc0, size_t lane_stride_words, int lanes, const int32_t* ext_slot,
                        const ModSlot* slots, int ext, size_t n, cudaStream_t st, const uint32_t* lift_a,
-                       const uint32_t* lift_b, const uint32_t* pmod, const uint32_t* pmod_s, int l) {
-    if (lanes < 2 && !lift_a && !lift_b) return CKKS_OK;
+                       const uint32_t* lift_b, const uint32_t* pmod, const uint32_t* pmod_s, int l,
+                       const uint32_t* raw) {
+    if (lanes < 2 && !lift_a && !lift_b && !raw) return CKKS_OK;
     if (n % 4 || lane_stride_words % 4) { set_last_error("lane reduction needs n %% 4 == 0"); return CKKS_ERR_UNSUPPORTED; }
-    ProfScope ps("lane_reduce", st, 4.0 * n * (2 * ext * (lanes + 1) + (lift_a ? l : 0) + (lift_b ? l : 0)));
+    ProfScope ps("lane_reduce", st, 4.0 * n * (2 * ext * (lanes + 1 + (raw ? 1 : 0)) + (lift_a ? l : 0) + (lift_b ? l : 0)));
     unsigned gx = (unsigned)((n / 4 + 255) / 256);
     CK(launch_pdl(lane_reduce_kernel, dim3(gx, 2 * ext), dim3(256), 0, st, (uint4*)acc0, lane_stride_words / 4, lanes,
-                  ext_slot, slots, ext, n / 4, (const uint4*)lift_a, (const uint4*)lift_b, pmod, pmod_s, l));
+                  ext_slot, slots, ext, n / 4, (const uint4*)lift_a, (const uint4*)lift_b, pmod, pmod_s, l, (const uint4*)raw));
     CK(cudaGetLastError());
     return CKKS_OK;
 }

@@ -356,12 +356,15 @@ class Engine:
                                            out[0].data_ptr(), out[1].data_ptr(), self.stream()))
         return out
 
-    def ks_finish_rescale(self, plan: int, md_plan: int, lanes_used: int, fold_a, fold_b, rows: int, n: int):
-        """ks_finish merged with the rescale that follows (one division by P and the dropped limbs)."""
+    def ks_finish_rescale(self, plan: int, md_plan: int, lanes_used: int, fold_a, fold_b, rows: int, n: int,
+                          raw_qp=None):
+        """ks_finish merged with the rescale that follows (one division by P and the dropped limbs);
+        raw_qp: a [2, ext, n] accumulator over Q||P added as it is."""
         out = self.empty(2, rows, n)
         _lib.check(self.lib.ckks_ks_finish_rescale(self.ctx, plan, md_plan, lanes_used,
                                                    None if fold_a is None else fold_a.data_ptr(),
                                                    None if fold_b is None else fold_b.data_ptr(),
+                                                   None if raw_qp is None else raw_qp.data_ptr(),
                                                    out[0].data_ptr(), out[1].data_ptr(), self.stream()))
         return out
 
