@@ -244,6 +244,17 @@ int ckks_ks_relin_rescale(ckks_ctx* ctx, int32_t ks_plan, int32_t md_plan, const
  * up to key-switch noise. */
 int ckks_ks_accumulate(ckks_ctx* ctx, int32_t plan, const uint32_t* ct_a, const uint32_t* evk,
                        int first, void* stream);
+/* Baby steps and inner sums of a double-hoisted BSGS linear transform in one pass:
+ * out[g] = sum_b p[g * nb + b] (.) u_b, u_b = the ckks_ks_hoisted_raw accumulator of rotation
+ * k[b] with key evk[b] (k[b] = 0: the ciphertext (ct_a, ct_b) on the Q rows, zero on the P
+ * rows; evk[b] ignored).  The u_b are formed in registers and never written; values equal
+ * ckks_ks_hoisted_raw + ckks_fused_terms_multi bit for bit.  p[.] are [l+alpha][n] plaintexts
+ * over Q||P (NULL: `zero` is read), out[g] are [2][l+alpha][n]; nb <= 16, ng <= 8; k, evk, p,
+ * out are HOST arrays. */
+int ckks_bsgs_inner(ckks_ctx* ctx, int32_t plan, const uint32_t* raised, const uint32_t* ct_a,
+                    const uint32_t* ct_b, int nb, const uint32_t* k, const uint32_t* const* evk, int ng,
+                    const uint32_t* const* p, const uint32_t* zero, uint32_t* const* out, void* stream);
+
 /* ckks_ks_accumulate for the rotation sigma_k of (ct_a, ct_b) without materialising it: the
  * automorphism is a gather inside the inner product and P * sigma_k(ct_b) is lifted into the b
  * accumulator (no separate automorphism pass, no separate sum of the b parts). */

@@ -139,8 +139,9 @@ class LinearTransform:
     unchanged (two limbs where 2^-31 relative plaintext precision is not enough)."""
 
     def __init__(self, diags: dict, params: ParameterSet, level: int, n1: int | None = None,
-                 factor: complex = 1.0, limbs: int = 1, double_hoist: bool = True):
+                 factor: complex = 1.0, limbs: int = 1, double_hoist: bool = True, fuse_baby_steps: bool = True):
         n = params.n // 2
+        self.fuse_baby_steps = fuse_baby_steps
         self.params, self.level, self.n, self.limbs = params, level, n, limbs
         self.double_hoist = double_hoist
         offs = sorted(diags)
@@ -197,19 +198,39 @@ class LinearTransform:
                 raise RnsError(f"no Galois key for rotation {b * self.step}")
             return eng.ks_hoisted_raw(plan, raised, k, keys.galois[k].matrix(), b_half, ext)
 
-        acc = dict(zip(moving, eng.fork([(lambda b=b: raw(b)) for b in moving])))
-        if 0 in self.baby:
-            x = ckks.ct_tensor(ct)
-            acc[0] = torch.cat([x, torch.zeros((2, alpha, n_ring), dtype=x.dtype, device=x.device)], dim=1)
-
-        # every giant step's inner sum over Q||P in one pass (each baby step read once) ...
-        babies = sorted(acc)
         giants = self.giants
         qps = {}
-        for g0 in range(0, len(giants), 8):
-            chunk = giants[g0:g0 + 8]
-            table = [[self.table[g][b].poly.data if b in self.table[g] else None for b in babies] for g in chunk]
-            qps.update(zip(chunk, eng.fused_terms_multi([acc[b] for b in babies], table, ext_slots)))
+        beta = -(-level // alpha)
+        if n_ring % 2 == 0 and len(self.baby) <= 16 and beta <= 4 and self.fuse_baby_steps:
+            # baby steps and inner sums in ONE pass: each rotated accumulator is formed in
+            # registers and multiplied into every giant step's sum, never written
+            babies = list(self.baby)
+            ks_idx, evks = [], []
+            for b in babies:
+                if b == 0:
+                    ks_idx.append(0)
+                    evks.append(None)
+                    continue
+                k = ckks.galois_element(b * self.step, n_ring)
+                if k not in keys.galois:
+                    raise RnsError(f"no Galois key for rotation {b * self.step}")
+                ks_idx.append(k)
+                evks.append(keys.galois[k].matrix())
+            for g0 in range(0, len(giants), 8):
+                chunk = giants[g0:g0 + 8]
+                table = [[self.table[g][b].poly.data if b in self.table[g] else None for b in babies] for g in chunk]
+                qps.update(zip(chunk, eng.bsgs_inner(plan, raised, ct.a.data, b_half, ks_idx, evks, table, ext)))
+        else:
+            acc = dict(zip(moving, eng.fork([(lambda b=b: raw(b)) for b in moving])))
+            if 0 in self.baby:
+                x = ckks.ct_tensor(ct)
+                acc[0] = torch.cat([x, torch.zeros((2, alpha, n_ring), dtype=x.dtype, device=x.device)], dim=1)
+            # every giant step's inner sum over Q||P in one pass (each baby step read once) ...
+            babies = sorted(acc)
+            for g0 in range(0, len(giants), 8):
+                chunk = giants[g0:g0 + 8]
+                table = [[self.table[g][b].poly.data if b in self.table[g] else None for b in babies] for g in chunk]
+                qps.update(zip(chunk, eng.fused_terms_multi([acc[b] for b in babies], table, ext_slots)))
 
         def inner_sum(g):
             # ... then one ModDown per giant step

@@ -898,6 +898,38 @@ int ckks_ks_hoisted_raw(ckks_ctx* ctx, int32_t plan, const uint32_t* raised, uin
     return inner_product_launch(ip, ctx->d_slots, (cudaStream_t)stream);
 }
 
+int ckks_bsgs_inner(ckks_ctx* ctx, int32_t plan, const uint32_t* raised, const uint32_t* ct_a,
+                    const uint32_t* ct_b, int nb, const uint32_t* k, const uint32_t* const* evk, int ng,
+                    const uint32_t* const* p, const uint32_t* zero, uint32_t* const* out, void* stream) {
+    KsPlan* pl;
+    CKS(get_plan(ctx, plan, &pl));
+    CKS(need_full_plan(pl));
+    if (nb < 1 || nb > kMaxTerms || ng < 1 || ng > kMaxGiants || !k || !evk || !p || !out) {
+        set_last_error("bsgs_inner: %d baby x %d giant steps out of range [1, %d] x [1, %d]", nb, ng, kMaxTerms, kMaxGiants);
+        return CKKS_ERR_ARG;
+    }
+    BsgsInnerArgs a{};
+    a.raised = raised; a.ct_a = ct_a; a.ct_b = ct_b;
+    a.ext_slot = pl->d_ext_slot; a.evk_row = pl->d_evk_row; a.pmod = pl->d_pmod; a.pmod_s = pl->d_pmod_s;
+    a.l = pl->l; a.alpha = pl->alpha; a.beta = pl->beta; a.ext = pl->ext; a.evk_ext = pl->evk_ext;
+    a.n = pl->n; a.lg = log2u(pl->n);
+    a.nb = nb; a.ng = ng;
+    for (int b = 0; b < nb; ++b) {
+        if (k[b] != 0 && !(k[b] & 1)) { set_last_error("automorphism index must be odd (or 0 for none)"); return CKKS_ERR_ARG; }
+        a.k[b] = k[b] & (2 * pl->n - 1);
+        a.evk[b] = evk[b];
+        if (a.k[b] && !a.evk[b]) { set_last_error("bsgs_inner: rotation %d has no key", b); return CKKS_ERR_ARG; }
+    }
+    for (int g = 0; g < ng; ++g) {
+        a.out[g] = out[g];
+        for (int b = 0; b < nb; ++b) {
+            a.p[g][b] = p[(size_t)g * nb + b] ? p[(size_t)g * nb + b] : zero;
+            if (!a.p[g][b]) { set_last_error("bsgs_inner: absent diagonal (%d, %d) but no zero plaintext given", g, b); return CKKS_ERR_ARG; }
+        }
+    }
+    return bsgs_inner_launch(a, ctx->d_slots, (cudaStream_t)stream);
+}
+
 // Relinearisation (or any key switch) fused with the rescale that follows it: the
 // polynomials the switched pair is added to (d1, d0) are lifted into the Q||P accumulator
 // (times P on the Q rows), and ONE ModDown divides by P * q_{l-1} * ... * q_{l-k}: the

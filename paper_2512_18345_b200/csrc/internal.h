@@ -190,6 +190,29 @@ struct ModDownEpilogueArgs {
     uint32_t n;
     uint32_t galois, lg;        // galois != 0: fold_b is read through X -> X^galois
 };
+// All baby steps of a double-hoisted BSGS linear transform fused with all giant-step inner
+// sums: for every baby step b the Q||P accumulator u_b of the rotation sigma_{k_b} of the
+// ciphertext (inner product of the raised digits with key b, P * sigma(ct_b) lifted in; k_b = 0:
+// the ciphertext itself on the Q rows) is formed in registers and immediately multiplied into
+// out[g] += p[g][b] (.) u_b.  The u_b are never written.
+struct BsgsInnerArgs {
+    const uint32_t* raised;                     // [beta][ext][n]
+    const uint32_t* ct_a;                       // [l][n]
+    const uint32_t* ct_b;                       // [l][n]
+    const int32_t* ext_slot;                    // [ext]
+    const int32_t* evk_row;                     // [ext]
+    const uint32_t* pmod;                       // [l]  P mod q_i
+    const uint32_t* pmod_s;
+    int l, alpha, beta, ext, evk_ext;
+    uint32_t n, lg;
+    int nb, ng;
+    uint32_t k[kMaxTerms];                      // automorphism index of baby step b (0: none)
+    const uint32_t* evk[kMaxTerms];             // its switching key [beta_total][2][evk_ext][n] (unused for k = 0)
+    const uint32_t* p[kMaxGiants][kMaxTerms];   // plaintext diagonal over Q||P, or `zero`
+    uint32_t* out[kMaxGiants];                  // [2][ext][n]
+};
+int bsgs_inner_launch(const BsgsInnerArgs& a, const ModSlot* slots, cudaStream_t st);
+
 int moddown_epilogue_launch(const ModDownEpilogueArgs& a, const ModSlot* slots, cudaStream_t st);
 int lane_reduce_launch(uint32_t* acc0, size_t lane_stride_words, int lanes, const int32_t* ext_slot,
                        const ModSlot* slots, int ext, size_t n, cudaStream_t st,

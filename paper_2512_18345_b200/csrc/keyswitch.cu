@@ -178,6 +178,172 @@ int inner_product_launch(const InnerProductArgs& a, const ModSlot* slots, cudaSt
     return CKKS_OK;
 }
 
+// Fused baby steps + inner sums of a double-hoisted BSGS linear transform (see BsgsInnerArgs).
+// One thread owns two columns of one extended-basis row; per baby step it forms the rotated
+// key-switch accumulator exactly as inner_product_kernel does (same exact modular arithmetic,
+// so results equal the unfused ckks_ks_hoisted_raw + ckks_fused_terms_multi bit for bit) and
+// multiplies it into the NG running sums.  Traffic: every key and every plaintext diagonal
+// once, raised digits through L2; the 2 * nb accumulator limbs per row are never written.
+constexpr int kBsgsStages = 3;
+
+// 8-byte asynchronous copy global -> shared.  No L2 cache hint: with the hint ptxas 12.9 put the
+// policy descriptor of the copies inside the loop into an odd uniform register pair
+// (LDGSTS ... desc[UR1]), which traps as an illegal instruction on sm_100a.
+__device__ __forceinline__ void cp_async8(uint2* dst_smem, const uint32_t* src, uint64_t) {
+    const uint32_t d = (uint32_t)__cvta_generic_to_shared(dst_smem);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" :: "r"(d), "l"(src) : "memory");
+}
+
+template <int NG, int BETA>
+__global__ void __launch_bounds__(256)
+bsgs_inner_kernel(BsgsInnerArgs p, const ModSlot* __restrict__ slots) {
+    const int row = blockIdx.y;
+    const ModSlot m = slots[p.ext_slot[row]];
+    const size_t n = p.n;
+    const size_t i = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) * 2;
+    if (i >= n) return;
+    const size_t erow = (size_t)p.evk_row[row];
+    const bool qrow = row < p.l;
+    const uint32_t pm = qrow ? p.pmod[row] : 0u, pms = qrow ? p.pmod_s[row] : 0u;
+    const uint64_t pol = l2_evict_first_policy();
+    const size_t half = (size_t)p.ext * n;
+    const size_t at = (size_t)row * n + i;
+    pdl_trigger();
+    pdl_wait();
+    uint64_t sa[NG][2], sb[NG][2];
+#pragma unroll
+    for (int g = 0; g < NG; ++g) sa[g][0] = sa[g][1] = sb[g][0] = sb[g][1] = 0;
+    // Software pipeline through shared memory: the 2 BETA key words and NG plaintext words a
+    // thread needs for baby step b + kBsgsStages - 1 are requested with cp.async (8 bytes each,
+    // L2 evict-first) while baby step b is reduced and multiplied.  A thread reads back only what
+    // it requested itself, so cp.async.wait_group is the only synchronisation; consecutive threads
+    // use consecutive 8-byte slots (no bank conflicts).
+    extern __shared__ uint2 s_pipe[];
+    constexpr int ITEMS = 2 * BETA + NG;
+    auto slot = [&](int stage, int item) -> uint2* { return s_pipe + ((size_t)(stage * ITEMS + item) * 256 + threadIdx.x); };
+    auto request = [&](int b) {
+        if (b < p.nb) {
+            const int stage = b % kBsgsStages;
+            const uint32_t* key = p.evk[b];
+            if (p.k[b] != 0) {
+#pragma unroll
+                for (int t = 0; t < BETA; ++t) {
+                    cp_async8(slot(stage, 2 * t), key + (((size_t)t * 2 + 0) * p.evk_ext + erow) * n + i, pol);
+                    cp_async8(slot(stage, 2 * t + 1), key + (((size_t)t * 2 + 1) * p.evk_ext + erow) * n + i, pol);
+                }
+            }
+#pragma unroll
+            for (int g = 0; g < NG; ++g) cp_async8(slot(stage, 2 * BETA + g), p.p[g][b] + at, pol);
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+#pragma unroll
+    for (int b = 0; b < kBsgsStages - 1; ++b) request(b);
+    for (int b = 0; b < p.nb; ++b) {
+        request(b + kBsgsStages - 1);
+        asm volatile("cp.async.wait_group %0;" :: "n"(kBsgsStages - 1) : "memory");
+        const int stage = b % kBsgsStages;
+        uint32_t ra[2], rb[2];
+        const uint32_t k = p.k[b];
+        if (k == 0) {
+            // the unrotated term: the ciphertext on the Q rows (its plaintext carries the factor P)
+            if (qrow) {
+                const uint2 av = *reinterpret_cast<const uint2*>(p.ct_a + at);
+                const uint2 bv = *reinterpret_cast<const uint2*>(p.ct_b + at);
+                ra[0] = av.x; ra[1] = av.y; rb[0] = bv.x; rb[1] = bv.y;
+            } else {
+                ra[0] = ra[1] = rb[0] = rb[1] = 0;
+            }
+        } else {
+            const uint32_t g0 = galois_src((uint32_t)i, k, p.n, p.lg), g1 = galois_src((uint32_t)i + 1, k, p.n, p.lg);
+            uint64_t ta[2] = {0, 0}, tb[2] = {0, 0};
+#pragma unroll
+            for (int t = 0; t < BETA; ++t) {
+                const uint32_t* dsrc = p.raised + ((size_t)t * p.ext + row) * n;
+                const uint32_t d0 = dsrc[g0], d1 = dsrc[g1];
+                const uint2 xa = *slot(stage, 2 * t), xb = *slot(stage, 2 * t + 1);
+                ta[0] = mad64(d0, xa.x, ta[0]); ta[1] = mad64(d1, xa.y, ta[1]);
+                tb[0] = mad64(d0, xb.x, tb[0]); tb[1] = mad64(d1, xb.y, tb[1]);
+            }
+            ra[0] = reduce64(ta[0], m); ra[1] = reduce64(ta[1], m);
+            rb[0] = reduce64(tb[0], m); rb[1] = reduce64(tb[1], m);
+            if (qrow) {
+                const uint32_t* bsrc = p.ct_b + (size_t)row * n;
+                rb[0] = add_mod(rb[0], shoup_mul(bsrc[g0], pm, pms, m.q), m.q);
+                rb[1] = add_mod(rb[1], shoup_mul(bsrc[g1], pm, pms, m.q), m.q);
+            }
+        }
+#pragma unroll
+        for (int g = 0; g < NG; ++g) {
+            const uint2 pv = *slot(stage, 2 * BETA + g);
+            sa[g][0] += (uint64_t)ra[0] * pv.x; sa[g][1] += (uint64_t)ra[1] * pv.y;
+            sb[g][0] += (uint64_t)rb[0] * pv.x; sb[g][1] += (uint64_t)rb[1] * pv.y;
+        }
+        if ((b & 3) == 3) {
+            // four 62-bit products + a carried residue fit 64 bits: fold and carry
+#pragma unroll
+            for (int g = 0; g < NG; ++g) {
+                sa[g][0] = reduce64(sa[g][0], m); sa[g][1] = reduce64(sa[g][1], m);
+                sb[g][0] = reduce64(sb[g][0], m); sb[g][1] = reduce64(sb[g][1], m);
+            }
+        }
+    }
+#pragma unroll
+    for (int g = 0; g < NG; ++g) {
+        uint32_t* o = p.out[g];
+        *reinterpret_cast<uint2*>(o + at) = make_uint2(reduce64(sa[g][0], m), reduce64(sa[g][1], m));
+        *reinterpret_cast<uint2*>(o + half + at) = make_uint2(reduce64(sb[g][0], m), reduce64(sb[g][1], m));
+    }
+}
+
+template <int NG, int BETA>
+static int bsgs_launch_one(const BsgsInnerArgs& a, const ModSlot* slots, dim3 grid, cudaStream_t st) {
+    const size_t sm = sizeof(uint2) * 256 * (size_t)kBsgsStages * (2 * BETA + NG);
+    if (sm > 48 * 1024)
+        CK(cudaFuncSetAttribute(bsgs_inner_kernel<NG, BETA>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    CK(launch_pdl(bsgs_inner_kernel<NG, BETA>, grid, dim3(256), sm, st, a, slots));
+    return CKKS_OK;
+}
+
+template <int NG>
+static int bsgs_dispatch(const BsgsInnerArgs& a, const ModSlot* slots, dim3 grid, cudaStream_t st) {
+    switch (a.beta) {
+        case 1: return bsgs_launch_one<NG, 1>(a, slots, grid, st);
+        case 2: return bsgs_launch_one<NG, 2>(a, slots, grid, st);
+        case 3: return bsgs_launch_one<NG, 3>(a, slots, grid, st);
+        case 4: return bsgs_launch_one<NG, 4>(a, slots, grid, st);
+    }
+    set_last_error("bsgs_inner supports 1..4 digits, got %d", a.beta);
+    return CKKS_ERR_UNSUPPORTED;
+}
+
+int bsgs_inner_launch(const BsgsInnerArgs& a, const ModSlot* slots, cudaStream_t st) {
+    if (a.n % 2 || a.nb < 1 || a.nb > kMaxTerms || a.ng < 1 || a.ng > kMaxGiants) {
+        set_last_error("bsgs_inner needs even n, 1..%d baby steps, 1..%d giant steps", kMaxTerms, kMaxGiants);
+        return CKKS_ERR_UNSUPPORTED;
+    }
+    int keyed = 0;
+    for (int b = 0; b < a.nb; ++b) keyed += a.k[b] ? 1 : 0;
+    // keys + plaintexts + outputs (+ the ciphertext once); raised digits are re-read through L2
+    const double limbs = (double)a.ext * (2.0 * a.beta * keyed + (double)a.nb * a.ng + 2.0 * a.ng) + 2.0 * a.l;
+    ProfScope ps("bsgs_inner", st, 4.0 * a.n * limbs);
+    dim3 grid((unsigned)((a.n / 2 + 255) / 256), a.ext);
+    int rc = CKKS_ERR_UNSUPPORTED;
+    switch (a.ng) {
+        case 1: rc = bsgs_dispatch<1>(a, slots, grid, st); break;
+        case 2: rc = bsgs_dispatch<2>(a, slots, grid, st); break;
+        case 3: rc = bsgs_dispatch<3>(a, slots, grid, st); break;
+        case 4: rc = bsgs_dispatch<4>(a, slots, grid, st); break;
+        case 5: rc = bsgs_dispatch<5>(a, slots, grid, st); break;
+        case 6: rc = bsgs_dispatch<6>(a, slots, grid, st); break;
+        case 7: rc = bsgs_dispatch<7>(a, slots, grid, st); break;
+        case 8: rc = bsgs_dispatch<8>(a, slots, grid, st); break;
+    }
+    if (rc != CKKS_OK) return rc;
+    CK(cudaGetLastError());
+    return CKKS_OK;
+}
+
 template <bool VEC>
 __global__ void __launch_bounds__(256)
 moddown_epilogue_kernel(ModDownEpilogueArgs p, const ModSlot* __restrict__ slots) {

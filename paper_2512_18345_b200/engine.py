@@ -330,6 +330,30 @@ class Engine:
                                                 ct_b.data_ptr(), out.data_ptr(), self.stream()))
         return out
 
+    def _zero_plain(self, rows: int, n: int):
+        key = ("zero_plain", rows, n)
+        zero = self._tables.get(key)
+        if zero is None:
+            zero = self._tables[key] = self.torch.zeros((rows, n), dtype=self.torch.int32, device=self.device)
+        return zero
+
+    def bsgs_inner(self, plan: int, raised, ct_a, ct_b, ks, evks, table, ext: int):
+        """All baby steps (rotation indices `ks`, 0 = none; keys `evks`) and all giant-step inner
+        sums (table[g][b]: plaintext over Q||P or None) of a double-hoisted BSGS transform in one
+        pass; returns the [2, ext, n] Q||P accumulators of the giant steps."""
+        nb, ng = len(ks), len(table)
+        n = ct_a.shape[1]
+        outs = [self.empty(2, ext, n) for _ in range(ng)]
+        kk = (ctypes.c_uint32 * nb)(*ks)
+        ep = (ctypes.c_void_p * nb)(*[None if e is None else e.data_ptr() for e in evks])
+        flat = [None if pt is None else pt.data_ptr() for row in table for pt in row]
+        pp = (ctypes.c_void_p * (nb * ng))(*flat)
+        op = (ctypes.c_void_p * ng)(*[o.data_ptr() for o in outs])
+        zero = self._zero_plain(ext, n).data_ptr() if any(f is None for f in flat) else None
+        _lib.check(self.lib.ckks_bsgs_inner(self.ctx, plan, raised.data_ptr(), ct_a.data_ptr(), ct_b.data_ptr(),
+                                            nb, kk, ep, ng, pp, zero, op, self.stream()))
+        return outs
+
     def ks_relin_rescale(self, ks_plan: int, md_plan: int, d, evk, out_rows: int):
         """d = [3, l, n] tensor product (d0, d1, d2) -> rescaled relinearised ciphertext [2, out_rows, n]."""
         out = self.empty(2, out_rows, d.shape[2])

@@ -140,3 +140,43 @@ def test_ntt_phases_compose_and_invert_at_2_16(env):
     assert torch.equal(back, x)
     half = eng.ntt_stages(fwd, slots, True, 0, 8)
     assert torch.equal(eng.ntt_stages(half, slots, True, 8, 16), x)
+
+
+def test_bsgs_inner_equals_unfused_baby_steps(env):
+    """The fused baby-step + inner-sum kernel against ckks_ks_hoisted_raw followed by
+    ckks_fused_terms_multi on the same keys, digits and plaintexts: exact modular arithmetic, so
+    the Q||P accumulators must agree bit for bit (including an absent diagonal and the
+    unrotated term)."""
+    eng, torch, p = env.eng, env.torch, env.ks48
+    from paper_2512_18345_b200 import ckks
+
+    level = 21                                  # two digits, the second one partial
+    basis = p.q_basis[:level]
+    ext = level + p.alpha
+    ext_basis = basis + p.p_basis
+    rng = np.random.default_rng(31)
+    ct_a = eng.upload(rand_rows(basis, p.n, rng))
+    ct_b = eng.upload(rand_rows(basis, p.n, rng))
+    plan = eng.ks_plan(p.n, basis, p.p_basis, p.alpha, p.l + p.alpha, p.l)
+    beta = -(-level // p.alpha)
+    raised = eng.ks_stage1(plan, ct_a, beta, ext)
+    full_ext = p.ext_basis
+    rots = [0, 1, 2, 5]
+    ks_idx = [0 if r == 0 else ckks.galois_element(r, p.n) for r in rots]
+    evks = [None if r == 0 else eng.upload(rand_rows(full_ext, p.dnum * 2 * p.n, rng).reshape(len(full_ext), p.dnum, 2, p.n)
+                                           .transpose(1, 2, 0, 3).copy()) for r in rots]
+    ng = 3
+    table = [[None if (g, b) == (1, 2) else eng.upload(rand_rows(ext_basis, p.n, rng)) for b in range(len(rots))]
+             for g in range(ng)]
+    fused = eng.bsgs_inner(plan, raised, ct_a, ct_b, ks_idx, evks, table, ext)
+    # unfused composition
+    accs = []
+    for k, evk in zip(ks_idx, evks):
+        if k == 0:
+            x = torch.stack([ct_a, ct_b])
+            accs.append(torch.cat([x, torch.zeros((2, p.alpha, p.n), dtype=x.dtype, device=x.device)], dim=1))
+        else:
+            accs.append(eng.ks_hoisted_raw(plan, raised, k, evk, ct_b, ext))
+    want = eng.fused_terms_multi(accs, table, eng.row_slots(ext_basis))
+    for g in range(ng):
+        assert torch.equal(fused[g], want[g]), g
