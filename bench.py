@@ -44,6 +44,7 @@ ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
 LIMB_BYTES = 65536 * 4
+FP64_TENSOR_TFLOPS = 37.06
 
 METRIC = {
     "bootstrap": "CKKS bootstrap throughput (2^15 slots, N=2^16); ms_per_step = bootstrap latency ms",
@@ -149,9 +150,12 @@ def read_profile(eng):
     buf = ctypes.create_string_buffer(1 << 16)
     eng.lib.ckks_profile_read(buf, len(buf))
     out = {}
+    flops = {}
     for line in buf.value.decode().splitlines():
-        name, cnt, ms, nbytes = line.split()
+        name, cnt, ms, nbytes, nflops = line.split()
         out[name] = (int(cnt), float(ms), float(nbytes))
+        flops[name] = float(nflops)
+    read_profile.flops = flops
     return out
 
 
@@ -490,13 +494,25 @@ def run_b200(args):
     cnt, ms_top, bytes_top = prof[top]
     achieved = bytes_top / (ms_top * 1e-3) / 1e9
     traffic, traffic_src = measured_traffic(wl, top)
+    bound, unit = "hbm", "GB/s"
+    top_flops = getattr(read_profile, "flops", {}).get(top, 0.0)
+    if top_flops > 0:
+        # the dominant kernel runs on the FP64 tensor cores (split-integer base conversion):
+        # roofline against the measured DMMA rate, profiles/microbench/dmma.cu (63.7 FMA/clk/SM x
+        # 148 SMs x 1.965 GHz x 2 = 37.06 TFLOP/s); MEASURED_PEAKS.json has no FP64 figure
+        bound, unit = "tensor", "TFLOP/s"
+        achieved = top_flops / (ms_top * 1e-3) / 1e12
+        peak, peak_src = FP64_TENSOR_TFLOPS, "measured FP64 DMMA rate (profiles/microbench/dmma.cu, mma.sync m8n8k4 f64)"
     roofline = {
-        "bound": "hbm", "kernel": top, "achieved": achieved, "peak": peak, "unit": "GB/s",
+        "bound": bound, "kernel": top, "achieved": achieved, "peak": peak, "unit": unit,
         "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src, "peak_source": peak_src,
         "avg_launch_us": ms_top / cnt * 1e3, "alg_bytes_per_launch": bytes_top / cnt,
         "share_of_step": ms_top / total_prof_ms,
-        "note": "achieved = algorithmic bytes (operand limbs read+written once) / CUDA-event time of the "
-                "launches of this kernel class in an eager pass of the same step",
+        "note": "achieved = algorithmic bytes (operand limbs read+written once; for a tensor-bound kernel: "
+                "FP64 tensor operations of the contraction) / CUDA-event time of the launches of this kernel "
+                "class in an eager pass of the same step",
+        "hbm_kernels_frac": {k: (nb / (ms * 1e-3) / 1e9) / load_peaks()[0]
+                             for k, (c, ms, nb) in prof.items() if k in ("bsgs_inner", "inner_product", "fused_terms")},
         "kernels": {k: {"launches_per_step": c / prof_steps, "us_per_launch": ms / c * 1e3,
                         "share": ms / total_prof_ms, "gbs": (nb / (ms * 1e-3) / 1e9) if nb else None}
                     for k, (c, ms, nb) in sorted(prof.items(), key=lambda kv: -kv[1][1])},

@@ -47,8 +47,9 @@ const char* ckks_last_error(void);
  * counters (instrument.py:11-32).  While enabled, every kernel launch is
  * bracketed by CUDA events on its stream (do not enable during graph
  * capture).  ckks_profile_read synchronises and writes one line
- * "<kernel> <launches> <total_ms> <algorithmic_bytes>" per kernel class into buf
- * (bytes: operand limbs read + written once, tables excluded). */
+ * "<kernel> <launches> <total_ms> <algorithmic_bytes> <tensor_flops>" per kernel class
+ * into buf (bytes: operand limbs read + written once, tables excluded; tensor_flops: FP64
+ * tensor-core operations of the base-conversion contraction, 2 per FMA, 0 for other kernels). */
 int ckks_profile_enable(int on);
 int ckks_profile_read(char* buf, size_t cap);
 

@@ -37,7 +37,7 @@ bool pdl_enabled() {
 }
 
 // ---- optional kernel timing ----------------------------------------------------------
-struct ProfRec { int name; cudaEvent_t a, b; double bytes; };
+struct ProfRec { int name; cudaEvent_t a, b; double bytes, flops; };
 static bool g_prof_on = false;
 static std::vector<ProfRec> g_prof;
 static std::vector<std::string> g_prof_names;
@@ -50,13 +50,13 @@ static cudaEvent_t prof_event() {
     return e;
 }
 
-ProfScope::ProfScope(const char* name, cudaStream_t stream, double alg_bytes) : st(stream), live(g_prof_on) {
+ProfScope::ProfScope(const char* name, cudaStream_t stream, double alg_bytes, double alg_flops) : st(stream), live(g_prof_on) {
     if (!live) return;
     int id = -1;
     for (size_t i = 0; i < g_prof_names.size(); ++i)
         if (g_prof_names[i] == name) id = (int)i;
     if (id < 0) { id = (int)g_prof_names.size(); g_prof_names.push_back(name); }
-    ProfRec r{id, prof_event(), prof_event(), alg_bytes};
+    ProfRec r{id, prof_event(), prof_event(), alg_bytes, alg_flops};
     cudaEventRecord(r.a, st);
     g_prof.push_back(r);
 }
@@ -207,19 +207,20 @@ int ckks_profile_read(char* buf, size_t cap) {
     CK(cudaDeviceSynchronize());
     std::vector<double> total(g_prof_names.size(), 0.0);
     std::vector<int> count(g_prof_names.size(), 0);
-    std::vector<double> bytes(g_prof_names.size(), 0.0);
+    std::vector<double> bytes(g_prof_names.size(), 0.0), flops(g_prof_names.size(), 0.0);
     for (auto& r : g_prof) {
         float ms = 0.f;
         CK(cudaEventElapsedTime(&ms, r.a, r.b));
         total[r.name] += ms;
         count[r.name] += 1;
         bytes[r.name] += r.bytes;
+        flops[r.name] += r.flops;
     }
     size_t at = 0;
     buf[0] = 0;
     for (size_t i = 0; i < g_prof_names.size(); ++i) {
         if (!count[i]) continue;
-        int w = snprintf(buf + at, cap - at, "%s %d %.6f %.0f\n", g_prof_names[i].c_str(), count[i], total[i], bytes[i]);
+        int w = snprintf(buf + at, cap - at, "%s %d %.6f %.0f %.0f\n", g_prof_names[i].c_str(), count[i], total[i], bytes[i], flops[i]);
         if (w < 0 || (size_t)w >= cap - at) break;
         at += (size_t)w;
     }

@@ -332,6 +332,13 @@ bconv_generic(BconvJobs jobs, const ModSlot* __restrict__ slots, size_t cols) {
     }
 }
 
+// FP64 tensor-core work of the split-integer contraction: two halves x l_in x l_out FMAs per column
+static double jobs_flops(const BconvJobs& jobs, size_t cols) {
+    double macs = 0;
+    for (int j = 0; j < jobs.count; ++j) macs += 2.0 * jobs.job[j].tab.l_in * jobs.job[j].tab.l_out;
+    return 2.0 * macs * cols;
+}
+
 static double jobs_bytes(const BconvJobs& jobs, size_t cols) {
     double limbs = 0;
     for (int j = 0; j < jobs.count; ++j) limbs += jobs.job[j].tab.l_in + jobs.job[j].tab.l_out;
@@ -363,7 +370,7 @@ static int launch_dmma(const BconvJobs& jobs, const ModSlot* slots, size_t cols,
     const int chunk = (((l_out_max + z - 1) / z) + 7) & ~7;
     const size_t sm = sizeof(double) * (size_t)chunk * 4 * KS + sizeof(uint4) * ((size_t)chunk + 4 * KS);
     dim3 grid(gx, jobs.count, (l_out_max + chunk - 1) / chunk);
-    ProfScope ps("bconv", st, jobs_bytes(jobs, cols));
+    ProfScope ps("bconv", st, jobs_bytes(jobs, cols), jobs_flops(jobs, cols));
     if (sm > 48 * 1024)
         CK(cudaFuncSetAttribute(bconv_dmma<KS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     CK(launch_pdl(bconv_dmma<KS>, grid, dim3(128), sm, st, jobs, slots, cols, chunk));

@@ -65,7 +65,8 @@ struct ProfScope {
     bool live;
     // alg_bytes: algorithmic bytes of the launch (operand limbs read + written once,
     // tables and twiddles excluded: SURVEY 8d / Appendix A convention)
-    ProfScope(const char* name, cudaStream_t stream, double alg_bytes = 0.0);
+    // alg_flops: floating-point operations of a tensor-core launch (2 per FMA), 0 otherwise
+    ProfScope(const char* name, cudaStream_t stream, double alg_bytes = 0.0, double alg_flops = 0.0);
     ~ProfScope();
 };
 

@@ -101,7 +101,7 @@ eng.lib.ckks_profile_enable(0)
 stages = {}
 for line in cbuf.value.decode().splitlines():
     parts = line.split()
-    if len(parts) == 4:
+    if len(parts) >= 4:
         k, c, ms, nb = parts[0], int(parts[1]), float(parts[2]), float(parts[3])
         stages[k] = {"launches": c / reps, "us_per_launch": round(ms / c * 1e3, 2),
                      "gbs": round(nb / (ms * 1e-3) / 1e9, 0) if ms else None}
