@@ -10,10 +10,11 @@ top = int(sys.argv[2]) if len(sys.argv) > 2 else 40
 hdr = next(r for r in rows if "Kernel Name" in r)
 start = rows.index(hdr)
 ki, mv, gi = hdr.index("Kernel Name"), hdr.index("Metric Value"), hdr.index("Grid Size")
+mn = hdr.index("Metric Name")
 by_kernel = collections.defaultdict(list)
 by_shape = collections.defaultdict(list)
 for r in rows[start + 1:]:
-    if len(r) <= mv:
+    if len(r) <= mv or r[mn] != "gpu__time_duration.sum":
         continue
     try:
         ns = float(r[mv].replace(",", ""))
