@@ -349,27 +349,6 @@ int ckks_modulus_register(ckks_ctx* ctx, uint32_t q, uint32_t n, uint32_t psi, i
         ctx->owned.push_back(d_inv);
         m.fwd = d_fwd;
         m.inv = d_inv;
-        if (n == 65536) {
-            // YZ_s[g][e] = psi^(+-(2^(12-s) brev4(e) + 2^(16-s) brev_s(g))), see ntt.cu
-            std::vector<uint2> yf(240), yi(240);
-            for (uint32_t s = 0; s < 4; ++s)
-                for (uint32_t g = 0; g < (1u << s); ++g)
-                    for (uint32_t e = 0; e < 16; ++e) {
-                        const uint64_t ex = ((uint64_t)h_bitrev(e, 4) << (12 - s)) +
-                                            ((uint64_t)h_bitrev(g, s) << (16 - s));
-                        const uint32_t wf = h_powmod(psi, ex, q), wi = h_powmod(psi_inv, ex, q);
-                        const size_t at = 16 * ((1u << s) - 1) + g * 16 + e;
-                        yf[at] = make_uint2(wf, h_shoup(wf, q));
-                        yi[at] = make_uint2(wi, h_shoup(wi, q));
-                    }
-            uint2 *d_yf, *d_yi;
-            CKS(upload(yf, &d_yf));
-            CKS(upload(yi, &d_yi));
-            ctx->owned.push_back(d_yf);
-            ctx->owned.push_back(d_yi);
-            m.otf_fwd = d_yf;
-            m.otf_inv = d_yi;
-        }
         m.n = n;
         m.n_inv = h_inv(n % q, q);
         m.n_inv_s = h_shoup(m.n_inv, q);

@@ -26,8 +26,6 @@ struct ModSlot {
     uint32_t fast;         // 1 when 2^30 < q < 2^31 (two-subtraction range tricks valid)
     const uint2* fwd;      // [n]
     const uint2* inv;      // [n]
-    const uint2* otf_fwd;  // [240] split twiddles YZ_s[g][e] of the N = 2^16 contiguous phase
-    const uint2* otf_inv;  // [240] (null for other degrees)
 };
 
 // ---- scalar modular arithmetic ------------------------------------------------

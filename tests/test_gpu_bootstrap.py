@@ -102,3 +102,29 @@ def test_sparse_secret_encapsulation(boot_env):
     plain = Bootstrapper(p, dense, BootstrapConfig())
     bad = np.abs(ckks.decrypt_decode(plain.bootstrap(ct), dense, p) - z).max()
     assert bad > 2.0 ** -17 and bad > 8 * err, (bad, err)
+
+
+def test_linear_transform_fused_baby_steps_equal_unfused(boot_env):
+    """A BSGS linear transform with the fused baby-step kernel (bsgs_inner) and with one hoisted
+    key switch per rotation + the multi-output inner sums: the same exact arithmetic, so the two
+    ciphertexts are equal limb for limb; and both match the plaintext diagonal product."""
+    ckks, p, sk, boot = boot_env
+    from paper_2512_18345_b200.bootstrap import LinearTransform, apply_diagonals
+
+    n = p.n // 2
+    rng = np.random.default_rng(12)
+    diags = {d: rng.uniform(-1, 1, n) + 1j * rng.uniform(-1, 1, n) for d in (0, 1, 2, 3, 5, 8, 9, 17, 30, 33)}
+    level = 12
+    z = rng.uniform(-1, 1, n) + 1j * rng.uniform(-1, 1, n)
+    ct = ckks.encrypt(ckks.encode(z, p, level=level, scale=float(1 << 45)), sk, p, seed=31)
+    outs = []
+    for fuse in (True, False):
+        lt = LinearTransform(diags, p, level, n1=4, limbs=2, fuse_baby_steps=fuse)
+        keys = ckks.EvaluationKeys(p, relin=None)
+        for i, r in enumerate(sorted(lt.rotations())):
+            keys.add_rotation(sk, r, seed=400 + i)
+        outs.append(lt.apply(ct, keys))
+    assert np.array_equal(outs[0].a.coeffs, outs[1].a.coeffs) and np.array_equal(outs[0].b.coeffs, outs[1].b.coeffs)
+    assert ckks.level_of(outs[0]) == level - 2
+    got = ckks.decrypt_decode(outs[0], sk, p)
+    assert np.abs(got - apply_diagonals(diags, z)).max() < 2.0 ** -20
