@@ -413,7 +413,7 @@ class Bootstrapper:
         for lt in self.cts:
             ct = lt.apply(ct, self.keys)
         # W holds (y_lo + i*y_hi) / 2 in bit-reversed slot order, scale tag eval_scale / 2
-        conj = ckks.conjugate(ct, self.keys)
+        conj = ckks.conjugate_fused(ct, self.keys)
         lo = ckks.add(ct, conj)        # y_lo   at tag eval_scale
         hi = ckks.sub(ct, conj)        # i*y_hi at tag eval_scale
         lo = ckks.Ciphertext(lo.a, lo.b, self.eval_scale)
@@ -490,7 +490,7 @@ class Bootstrapper:
         e = self._exp_taylor(x, coef)
         for _ in range(self.cfg.squarings):
             e = self._mul(e, e)
-        diff = ckks.sub(e, ckks.conjugate(e, self.keys))
+        diff = ckks.sub(e, ckks.conjugate_fused(e, self.keys))
         lvl = ckks.level_of(diff)
         pt_scale = float(self.params.q_basis[lvl - 1].q)
         # message scale folded so the result carries tag out_scale

@@ -515,6 +515,43 @@ def hrot_hoisted(ct: Ciphertext, rotations, keys: EvaluationKeys) -> dict:
     return out
 
 
+def apply_galois_fused(ct: Ciphertext, k: int, evk: ks.SwitchingKey) -> Ciphertext:
+    """sigma_k followed by its key switch WITHOUT a separate automorphism pass: ModUp of the
+    unrotated a part, the rotation applied as a gather inside the inner product and the ModDown
+    (the single-rotation case of hoisting).  sigma_k commutes with ModUp only up to a multiple
+    of the digit modulus, so the result equals apply_galois up to key-switch noise, not limb
+    for limb: hrot / conjugate keep the reference composition, application circuits use this."""
+    from .engine import get_engine
+
+    eng = get_engine()
+    params = evk.params
+    level, n, basis = level_of(ct), ct.a.n, ct.a.basis
+    if n % 4:
+        return apply_galois(ct, k, evk)
+    plan = eng.ks_plan(n, basis, params.p_basis, params.alpha, params.l + params.alpha, params.l)
+    raised = eng.ks_stage1(plan, ct.a.data, -(-level // params.alpha), level + params.alpha)
+    out = eng.ks_hoisted(plan, raised, k, evk.matrix(), ct.b.data)
+    return ct_from_tensor(out, basis, ct.scale)
+
+
+def hrot_fused(ct: Ciphertext, r: int, keys: EvaluationKeys) -> Ciphertext:
+    """hrot through apply_galois_fused (same message, different noise)."""
+    n = ct.a.n
+    if r % (n // 2) == 0:
+        return ct
+    k = galois_element(r, n)
+    if k not in keys.galois:
+        raise RnsError(f"no Galois key for rotation {r}")
+    return apply_galois_fused(ct, k, keys.galois[k])
+
+
+def conjugate_fused(ct: Ciphertext, keys: EvaluationKeys) -> Ciphertext:
+    k = conjugation_element(ct.a.n)
+    if k not in keys.galois:
+        raise RnsError("no conjugation key")
+    return apply_galois_fused(ct, k, keys.galois[k])
+
+
 def conjugate(ct: Ciphertext, keys: EvaluationKeys) -> Ciphertext:
     k = conjugation_element(ct.a.n)
     if k not in keys.galois:

@@ -117,7 +117,7 @@ class HelrTrainer:
 
     def _rot_sum(self, ct, rotations):
         for r in rotations:
-            ct = ckks.add(ct, ckks.hrot(ct, r, self.keys))
+            ct = ckks.add(ct, ckks.hrot_fused(ct, r, self.keys))
         return ct
 
     def iteration(self, z, w):

@@ -60,7 +60,7 @@ for i, lt in enumerate(boot.cts):
 
 
 def split(x):
-    conj = ckks.conjugate(x, boot.keys)
+    conj = ckks.conjugate_fused(x, boot.keys)
     lo, hi = ckks.add(x, conj), ckks.sub(x, conj)
     return ckks.Ciphertext(lo.a, lo.b, boot.eval_scale), ckks.Ciphertext(hi.a, hi.b, boot.eval_scale)
 
