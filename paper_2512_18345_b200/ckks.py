@@ -435,10 +435,16 @@ def hmult_rescale(x: Ciphertext, y: Ciphertext, rlk: ks.SwitchingKey, k: int = 1
     if tuple(m.q for m in basis) != tuple(m.q for m in params.q_basis[:level]):
         raise StructureError("ciphertext basis is not a prefix of the parameter q-basis")
     rest, dropped = basis[:level - k], basis[level - k:]
-    d = eng.tensor_halves(x.a.data, x.b.data, y.a.data, y.b.data, eng.row_slots(basis))
     ks_plan = eng.ks_plan(n, basis, params.p_basis, params.alpha, params.l + params.alpha, params.l)
     md_plan = eng.moddown_plan(n, rest, dropped + params.p_basis)
-    out = eng.ks_relin_rescale(ks_plan, md_plan, d, rlk.matrix(), level - k)
+    if n == 65536:
+        # no tensor pass: d2 is formed while the first inverse transform loads, d1 / d0 inside the
+        # inner product (same limbs as the two-call route below)
+        out = eng.hmult_relin_rescale(ks_plan, md_plan, x.a.data, x.b.data, y.a.data, y.b.data,
+                                      rlk.matrix(), level - k)
+    else:
+        d = eng.tensor_halves(x.a.data, x.b.data, y.a.data, y.b.data, eng.row_slots(basis))
+        out = eng.ks_relin_rescale(ks_plan, md_plan, d, rlk.matrix(), level - k)
     return Ciphertext(a=Polynomial(rest, out[0], EVALUATION), b=Polynomial(rest, out[1], EVALUATION),
                       scale=x.scale * y.scale / math.prod(m.q for m in dropped))
 

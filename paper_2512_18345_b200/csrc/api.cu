@@ -700,10 +700,11 @@ static int need_full_plan(KsPlan* pl) {
 // carry_copy the digit's own limbs are copied through; the fused pipeline
 // skips that copy and lets stage 2 read them from the input directly.
 static int stage1_core(ckks_ctx* ctx, KsPlan* pl, const uint32_t* a, uint32_t* raised,
-                       bool carry_copy, cudaStream_t st) {
+                       bool carry_copy, cudaStream_t st, const uint32_t* mul_in = nullptr) {
     const size_t n = pl->n;
+    // mul_in: the polynomial to switch is a (.) mul_in, formed while the inverse transform loads
     CKS(ntt_launch(a, pl->ws_coeff, pl->d_q_slot, ctx->d_slots, RowMap{nullptr, nullptr}, pl->l,
-                   pl->n, 1, st));
+                   pl->n, 1, st, nullptr, mul_in));
     for (int t0 = 0; t0 < pl->beta;) {
         BconvJobs jobs;
         jobs.count = 0;
@@ -939,6 +940,38 @@ int ckks_ks_relin_rescale(ckks_ctx* ctx, int32_t ks_plan, int32_t md_plan, const
     ip.pmod_s = pl->d_pmod_s;
     CKS(inner_product_launch(ip, ctx->d_slots, st));
     if (md->alpha > pl->alpha + kMaxMergedDrop) { set_last_error("merged rescale drops more than %d limbs", kMaxMergedDrop); return CKKS_ERR_UNSUPPORTED; }
+    return stage3_core(ctx, md, acc_a, acc_b, acc_a + (size_t)md->l * n, acc_b + (size_t)md->l * n,
+                       nullptr, out_a, out_b, st, 0, nullptr, pl->ws_conv, pl->ws_pc);
+}
+
+// HMult + relinearise + rescale without a tensor pass: d2 = xa * ya is formed while the first
+// inverse transform loads, and the inner product forms the carried rows of d2 and the lifted
+// d1 = xa * yb + ya * xb, d0 = xb * yb from the four operand halves.  Same values as ckks_tensor +
+// ckks_ks_relin_rescale (exact modular arithmetic), five limb transfers per row and one launch less.
+int ckks_hmult_relin_rescale(ckks_ctx* ctx, int32_t ks_plan, int32_t md_plan, const uint32_t* xa,
+                             const uint32_t* xb, const uint32_t* ya, const uint32_t* yb,
+                             const uint32_t* evk, uint32_t* out_a, uint32_t* out_b, void* stream) {
+    KsPlan *pl, *md;
+    CKS(get_plan(ctx, ks_plan, &pl));
+    CKS(need_full_plan(pl));
+    CKS(get_plan(ctx, md_plan, &md));
+    if (md->n != pl->n || md->l + md->alpha != pl->ext || md->l >= pl->l) {
+        set_last_error("ModDown plan (l=%d, alpha=%d) does not tile the key-switch accumulator (l=%d, ext=%d)",
+                       md->l, md->alpha, pl->l, pl->ext);
+        return CKKS_ERR_ARG;
+    }
+    if (pl->n != 65536) { set_last_error("fused HMult needs N = 2^16 (product-on-load transform)"); return CKKS_ERR_UNSUPPORTED; }
+    if (md->alpha > pl->alpha + kMaxMergedDrop) { set_last_error("merged rescale drops more than %d limbs", kMaxMergedDrop); return CKKS_ERR_UNSUPPORTED; }
+    cudaStream_t st = (cudaStream_t)stream;
+    const size_t n = pl->n;
+    CKS(stage1_core(ctx, pl, xa, pl->ws_raised, false, st, ya));
+    uint32_t* acc_a = pl->ws_acc;
+    uint32_t* acc_b = pl->ws_acc + (size_t)pl->ext * n;
+    InnerProductArgs ip = ip_args(pl, nullptr, pl->ws_raised, evk, 0, pl->ext, acc_a, acc_b);
+    ip.tx_a = xa; ip.tx_b = xb; ip.ty_a = ya; ip.ty_b = yb;
+    ip.pmod = pl->d_pmod;
+    ip.pmod_s = pl->d_pmod_s;
+    CKS(inner_product_launch(ip, ctx->d_slots, st));
     return stage3_core(ctx, md, acc_a, acc_b, acc_a + (size_t)md->l * n, acc_b + (size_t)md->l * n,
                        nullptr, out_a, out_b, st, 0, nullptr, pl->ws_conv, pl->ws_pc);
 }

@@ -76,7 +76,8 @@ struct ModDownEpilogueArgs;
 // epilogue to its registers and stores the key-switch result instead of the transform.
 int ntt_launch(const uint32_t* in, uint32_t* out, const int32_t* row_slot, const ModSlot* slots,
                RowMap rm, int rows, uint32_t n, int inverse, cudaStream_t st,
-               const ModDownEpilogueArgs* epi = nullptr);
+               const ModDownEpilogueArgs* epi = nullptr, const uint32_t* mul_in = nullptr);
+// mul_in != null (inverse, N = 2^16 only): the input is in (.) mul_in, multiplied on load.
 bool ntt_can_fuse_moddown(uint32_t n);
 int ntt_stages_launch(const uint32_t* in, uint32_t* out, const int32_t* row_slot,
                       const ModSlot* slots, int rows, uint32_t n, int inverse, uint32_t s_lo,
@@ -169,6 +170,11 @@ struct InnerProductArgs {
     uint32_t n;
     uint32_t galois, lg;        // galois != 0: read digit columns through X -> X^galois (hoisting)
     int accumulate;             // add into acc instead of overwriting it
+    // tensor mode (all four non-null): the operands of an HMult; the kernel forms d2 = xa*ya (the
+    // carried digit rows), d1 = xa*yb + ya*xb and d0 = xb*yb itself and lifts P*d1, P*d0 into
+    // the accumulators, so no tensor pass and no (d0, d1, d2) buffers exist.  carry, lift_a and
+    // lift_b are ignored.
+    const uint32_t *tx_a, *tx_b, *ty_a, *ty_b;
     const uint32_t* lift_a;     // non-null: add (P mod q_i) * lift_a to the Q rows of acc_a (no automorphism)
     const uint32_t* lift_b;     // non-null: add (P mod q_i) * sigma(lift_b) to the Q rows of acc_b, i.e.
     const uint32_t* pmod;       //   fold the rotated ciphertext's b-part into the Q||P accumulator

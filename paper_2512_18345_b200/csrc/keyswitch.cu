@@ -20,7 +20,7 @@ __device__ __forceinline__ uint64_t mad64(uint32_t a, uint32_t b, uint64_t c) {
 // BETA > 0: digit count known at compile time -- the loop is unrolled and all 3 * BETA
 // 16-byte loads of a thread are issued before the first product, which is what keeps
 // enough bytes in flight per SM to stream the key at HBM speed.  BETA = 0: runtime count.
-template <bool VEC, int BETA>
+template <bool VEC, int BETA, bool TENS>
 __global__ void __launch_bounds__(256)
 inner_product_kernel(InnerProductArgs p, const ModSlot* __restrict__ slots) {
     const int row = p.row_lo + blockIdx.y;
@@ -45,6 +45,10 @@ inner_product_kernel(InnerProductArgs p, const ModSlot* __restrict__ slots) {
 #pragma unroll
         for (int w = 0; w < W; ++w) gsrc[w] = galois_src((uint32_t)i + w, p.galois, p.n, p.lg);
     }
+    const bool tens = TENS && row < p.l;
+    uint32_t own[W], la[W], lb[W];
+#pragma unroll
+    for (int w = 0; w < W; ++w) own[w] = la[w] = lb[w] = 0;
     constexpr int CH = BETA > 0 ? BETA : 4;      // digits per 64-bit accumulation chunk (four 62-bit products fit)
     for (int t0 = 0; t0 < beta; t0 += CH) {
         uint32_t d[CH][W], xa[CH][W], xb[CH][W];
@@ -71,10 +75,36 @@ inner_product_kernel(InnerProductArgs p, const ModSlot* __restrict__ slots) {
             }
         }
         if (BETA > 0) pdl_wait();
+        if (tens && t0 == 0) {
+            const size_t at = (size_t)row * n + i;
+            uint32_t XA[W], XB[W], YA[W], YB[W];
+            if (VEC) {
+                const uint4 a1 = *reinterpret_cast<const uint4*>(p.tx_a + at), b1 = *reinterpret_cast<const uint4*>(p.tx_b + at);
+                const uint4 a2 = *reinterpret_cast<const uint4*>(p.ty_a + at), b2 = *reinterpret_cast<const uint4*>(p.ty_b + at);
+                XA[0] = a1.x; XA[W > 1 ? 1 : 0] = a1.y; XA[W > 2 ? 2 : 0] = a1.z; XA[W > 3 ? 3 : 0] = a1.w;
+                XB[0] = b1.x; XB[W > 1 ? 1 : 0] = b1.y; XB[W > 2 ? 2 : 0] = b1.z; XB[W > 3 ? 3 : 0] = b1.w;
+                YA[0] = a2.x; YA[W > 1 ? 1 : 0] = a2.y; YA[W > 2 ? 2 : 0] = a2.z; YA[W > 3 ? 3 : 0] = a2.w;
+                YB[0] = b2.x; YB[W > 1 ? 1 : 0] = b2.y; YB[W > 2 ? 2 : 0] = b2.z; YB[W > 3 ? 3 : 0] = b2.w;
+            } else {
+                XA[0] = p.tx_a[at]; XB[0] = p.tx_b[at]; YA[0] = p.ty_a[at]; YB[0] = p.ty_b[at];
+            }
+#pragma unroll
+            for (int w = 0; w < W; ++w) {
+                own[w] = mul_mod(XA[w], YA[w], m);
+                lb[w] = mul_mod(XB[w], YB[w], m);
+                la[w] = m.fast ? reduce64((uint64_t)XA[w] * YB[w] + (uint64_t)YA[w] * XB[w], m)
+                               : (uint32_t)(((uint64_t)XA[w] * YB[w] % m.q + (uint64_t)YA[w] * XB[w] % m.q) % m.q);
+            }
+        }
 #pragma unroll
         for (int c = 0; c < CH; ++c) {
             const int t = t0 + c;
             if (BETA == 0 && t >= beta) continue;
+            if (tens && t == digit_of_row) {
+#pragma unroll
+                for (int w = 0; w < W; ++w) d[c][w] = own[w];
+                continue;
+            }
             const uint32_t* dsrc = (p.carry && t == digit_of_row)
                                        ? p.carry + (size_t)row * n
                                        : p.raised + ((size_t)t * p.ext + row) * n;
@@ -123,7 +153,15 @@ inner_product_kernel(InnerProductArgs p, const ModSlot* __restrict__ slots) {
     }
     uint32_t* oa = p.acc_a + (size_t)(row - p.row_lo) * n + i;
     uint32_t* ob = p.acc_b + (size_t)(row - p.row_lo) * n + i;
-    if (p.lift_b && row < p.l) {
+    if (tens) {
+        const uint32_t pm = p.pmod[row], pms = p.pmod_s[row];
+#pragma unroll
+        for (int w = 0; w < W; ++w) {
+            ra[w] = add_mod(ra[w], shoup_mul(la[w], pm, pms, m.q), m.q);
+            rb[w] = add_mod(rb[w], shoup_mul(lb[w], pm, pms, m.q), m.q);
+        }
+    }
+    if (!TENS && p.lift_b && row < p.l) {
         const uint32_t pm = p.pmod[row], pms = p.pmod_s[row];
         const uint32_t* bsrc = p.lift_b + (size_t)row * n;
 #pragma unroll
@@ -132,7 +170,7 @@ inner_product_kernel(InnerProductArgs p, const ModSlot* __restrict__ slots) {
             rb[w] = add_mod(rb[w], shoup_mul(bv, pm, pms, m.q), m.q);
         }
     }
-    if (p.lift_a && row < p.l) {
+    if (!TENS && p.lift_a && row < p.l) {
         const uint32_t pm = p.pmod[row], pms = p.pmod_s[row];
         const uint32_t* asrc = p.lift_a + (size_t)row * n;
 #pragma unroll
@@ -156,8 +194,11 @@ inner_product_kernel(InnerProductArgs p, const ModSlot* __restrict__ slots) {
 
 template <int BETA>
 static void inner_product_dispatch(const InnerProductArgs& a, const ModSlot* slots, dim3 grid, bool vec, cudaStream_t st) {
-    if (vec) launch_pdl(inner_product_kernel<true, BETA>, grid, dim3(256), 0, st, a, slots);
-    else launch_pdl(inner_product_kernel<false, BETA>, grid, dim3(256), 0, st, a, slots);
+    const bool tens = a.tx_a != nullptr;
+    if (vec && tens) launch_pdl(inner_product_kernel<true, BETA, true>, grid, dim3(256), 0, st, a, slots);
+    else if (vec) launch_pdl(inner_product_kernel<true, BETA, false>, grid, dim3(256), 0, st, a, slots);
+    else if (tens) launch_pdl(inner_product_kernel<false, BETA, true>, grid, dim3(256), 0, st, a, slots);
+    else launch_pdl(inner_product_kernel<false, BETA, false>, grid, dim3(256), 0, st, a, slots);
 }
 
 int inner_product_launch(const InnerProductArgs& a, const ModSlot* slots, cudaStream_t st) {

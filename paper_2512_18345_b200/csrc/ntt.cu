@@ -324,9 +324,12 @@ ntt16_fwd_contig(const uint32_t* in, uint32_t* out, const int32_t* __restrict__ 
     }
 }
 
+// MUL: the transform's input is the element-wise product in (.) in2 of two evaluation-domain
+// polynomials (the d2 = a1 * a2 term of HMult), formed on load instead of by a tensor pass.
+template <bool MUL>
 __global__ void __launch_bounds__(256)
 ntt16_inv_contig(const uint32_t* in, uint32_t* out, const int32_t* __restrict__ row_slot,
-                 const ModSlot* __restrict__ slots, RowMap rm) {
+                 const ModSlot* __restrict__ slots, RowMap rm, const uint32_t* in2) {
     __shared__ uint32_t tile[16 * 272];
     __shared__ uint2 s_blk[16][16];      // per block: the 15 twiddles of stages 4..7, laid out 8 | 4 | 2 | 1
     const int tid = threadIdx.x;
@@ -353,6 +356,16 @@ ntt16_inv_contig(const uint32_t* in, uint32_t* out, const int32_t* __restrict__ 
         ld256(src + 8 * h, r);
 #pragma unroll
         for (int k = 0; k < 8; ++k) v[8 * h + k] = r[k];
+    }
+    if (MUL) {
+        const uint32_t* src2 = in2 + rm.in_row(blockIdx.y) * kN16 + B * 256 + 16 * e;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            uint32_t r[8];
+            ld256(src2 + 8 * h, r);
+#pragma unroll
+            for (int k = 0; k < 8; ++k) v[8 * h + k] = mul_mod(v[8 * h + k], r[k], m);
+        }
     }
     __syncwarp();
     // global stages 0..3 on elements 16e + k: slot = ((256 + B) * 16 + e) * (8 >> s) + group
@@ -411,8 +424,12 @@ bool ntt_can_fuse_moddown(uint32_t n) { return n == (uint32_t)kN16; }
 
 int ntt_launch(const uint32_t* in, uint32_t* out, const int32_t* row_slot, const ModSlot* slots,
                RowMap rm, int rows, uint32_t n, int inverse, cudaStream_t st,
-               const ModDownEpilogueArgs* epi) {
+               const ModDownEpilogueArgs* epi, const uint32_t* mul_in) {
     if (rows <= 0) return CKKS_OK;
+    if (mul_in && (!inverse || n != (uint32_t)kN16)) {
+        set_last_error("product-on-load needs an inverse N = 2^16 transform");
+        return CKKS_ERR_ARG;
+    }
     if (epi && (inverse || !ntt_can_fuse_moddown(n) || rows != 2 * epi->l)) {
         set_last_error("fused ModDown epilogue needs a forward N = 2^16 transform over 2 l rows");
         return CKKS_ERR_ARG;
@@ -433,8 +450,9 @@ int ntt_launch(const uint32_t* in, uint32_t* out, const int32_t* row_slot, const
                 CK(launch_pdl(ntt16_fwd_contig<false>, g_con, dim3(256), 0, st, out, out, row_slot, slots, rm2, ModDownEpilogueArgs{}));
             }
         } else {
-            { ProfScope ps("ntt16_inv_contig", st, 8.0 * rows * kN16);
-              CK(launch_pdl(ntt16_inv_contig, g_con, dim3(256), 0, st, in, out, row_slot, slots, rm)); }
+            { ProfScope ps("ntt16_inv_contig", st, (mul_in ? 12.0 : 8.0) * rows * kN16);
+              if (mul_in) CK(launch_pdl(ntt16_inv_contig<true>, g_con, dim3(256), 0, st, in, out, row_slot, slots, rm, mul_in));
+              else CK(launch_pdl(ntt16_inv_contig<false>, g_con, dim3(256), 0, st, in, out, row_slot, slots, rm, (const uint32_t*)nullptr)); }
             { ProfScope ps("ntt16_inv_strided", st, 8.0 * rows * kN16);
               CK(launch_pdl(ntt16_inv_strided<COLS>, g_str, dim3(16 * COLS), 0, st, out, out, row_slot, slots, rm2)); }
         }
@@ -460,7 +478,7 @@ int ntt_stages_launch(const uint32_t* in, uint32_t* out, const int32_t* row_slot
         const bool strided = inverse ? (s_lo == 8) : (s_lo == 0);
         if (!inverse && strided) ntt16_fwd_strided<COLS><<<g_str, 16 * COLS, 0, st>>>(in, out, row_slot, slots, rm);
         if (!inverse && !strided) ntt16_fwd_contig<false><<<g_con, 256, 0, st>>>(in, out, row_slot, slots, rm, ModDownEpilogueArgs{});
-        if (inverse && !strided) ntt16_inv_contig<<<g_con, 256, 0, st>>>(in, out, row_slot, slots, rm);
+        if (inverse && !strided) ntt16_inv_contig<false><<<g_con, 256, 0, st>>>(in, out, row_slot, slots, rm, nullptr);
         if (inverse && strided) ntt16_inv_strided<COLS><<<g_str, 16 * COLS, 0, st>>>(in, out, row_slot, slots, rm);
         CK(cudaGetLastError());
         return CKKS_OK;

@@ -362,6 +362,14 @@ class Engine:
                                                   out[0].data_ptr(), out[1].data_ptr(), self.stream()))
         return out
 
+    def hmult_relin_rescale(self, ks_plan: int, md_plan: int, xa, xb, ya, yb, evk, out_rows: int):
+        """HMult + relinearise + rescale from the operand halves in one pipeline (no tensor pass)."""
+        out = self.empty(2, out_rows, xa.shape[1])
+        _lib.check(self.lib.ckks_hmult_relin_rescale(self.ctx, ks_plan, md_plan, xa.data_ptr(), xb.data_ptr(),
+                                                     ya.data_ptr(), yb.data_ptr(), evk.data_ptr(),
+                                                     out[0].data_ptr(), out[1].data_ptr(), self.stream()))
+        return out
+
     def ks_accumulate_rot(self, plan: int, ct_a, ct_b, k: int, evk, first: bool):
         """Stages 1-2 of the key switch of sigma_k(ct) into the current lane's Q||P accumulator,
         the rotation applied as a gather (no automorphism pass), P * sigma_k(ct_b) lifted in."""

@@ -180,3 +180,28 @@ def test_bsgs_inner_equals_unfused_baby_steps(env):
     want = eng.fused_terms_multi(accs, table, eng.row_slots(ext_basis))
     for g in range(ng):
         assert torch.equal(fused[g], want[g]), g
+
+
+@pytest.mark.parametrize("level,k", [(48, 2), (30, 2), (21, 1), (13, 1)])
+def test_fused_hmult_equals_tensor_then_relin_rescale(env, level, k):
+    """ckks_hmult_relin_rescale (d2 formed while the inverse transform loads, d1 / d0 inside the
+    inner product) against ckks_tensor + ckks_ks_relin_rescale on the same operands and key: exact
+    modular arithmetic, equal limb for limb (full and partial last digit, 1- and 2-limb rescale)."""
+    eng, torch, p = env.eng, env.torch, env.ks48
+    basis = p.q_basis[:level]
+    rest, dropped = basis[:level - k], basis[level - k:]
+    rng = np.random.default_rng(100 + level)
+    xa, xb, ya, yb = (eng.upload(rand_rows(basis, p.n, rng)) for _ in range(4))
+    full_ext = p.ext_basis
+    evk = eng.upload(rand_rows(full_ext, p.dnum * 2 * p.n, rng).reshape(len(full_ext), p.dnum, 2, p.n)
+                     .transpose(1, 2, 0, 3).copy())
+    ks_plan = eng.ks_plan(p.n, basis, p.p_basis, p.alpha, p.l + p.alpha, p.l)
+    md_plan = eng.moddown_plan(p.n, rest, dropped + p.p_basis)
+    fused = eng.hmult_relin_rescale(ks_plan, md_plan, xa, xb, ya, yb, evk, level - k)
+    d = eng.tensor_halves(xa, xb, ya, yb, eng.row_slots(basis))
+    want = eng.ks_relin_rescale(ks_plan, md_plan, d, evk, level - k)
+    assert torch.equal(fused, want)
+    # squaring: both operands are the same tensors
+    fused = eng.hmult_relin_rescale(ks_plan, md_plan, xa, xb, xa, xb, evk, level - k)
+    d = eng.tensor_halves(xa, xb, xa, xb, eng.row_slots(basis))
+    assert torch.equal(fused, eng.ks_relin_rescale(ks_plan, md_plan, d, evk, level - k))
