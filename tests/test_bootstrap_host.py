@@ -51,3 +51,28 @@ def test_stage_structure_and_diagonal_counts():
     # r merged stages give at most 2^(r+1) - 1 diagonals
     for g, r in zip(groups, default_groups(10, 3)):
         assert len(g) <= 2 ** (r + 1) - 1
+
+
+def test_exp_polynomial_accuracy_and_parity():
+    """The EvalMod polynomial: degree-13 Chebyshev interpolation of exp(i*y) on the range the
+    squarings leave beats the degree-15 Taylor series, has cos/sin parity, and the x = i*y form is
+    real.  Error on the message after r squarings and the Q0/(2*pi*Delta) factor stays below 2^-24."""
+    import math
+
+    from paper_2512_18345_b200.bootstrap import BootstrapConfig, exp_coefficients
+
+    cfg = BootstrapConfig()
+    bound = 2 * math.pi * cfg.k_bound / (1 << cfg.squarings)
+    ys = np.linspace(-bound, bound, 20001)
+    a, c = exp_coefficients(cfg)
+    assert len(a) == cfg.degree + 1 == 14
+    err = np.abs(np.polyval(a[::-1], ys) - np.exp(1j * ys)).max()
+    ta, _ = exp_coefficients(BootstrapConfig(degree=15, approx="taylor"))
+    terr = np.abs(np.polyval(ta[::-1], ys) - np.exp(1j * ys)).max()
+    assert err < terr / 50
+    amplification = (1 << cfg.squarings) * (2.0 ** 62 / (2 * math.pi * 2.0 ** cfg.log_delta_in))
+    assert err * amplification < 2.0 ** -24
+    for k in range(cfg.degree + 1):
+        assert (a[k].imag == 0.0) if k % 2 == 0 else (a[k].real == 0.0)
+        assert abs(complex(c[k]).imag) < 1e-300
+    assert np.abs(np.polyval(c[::-1], 1j * ys) - np.exp(1j * ys)).max() < 2 * err
