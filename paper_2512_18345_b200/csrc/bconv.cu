@@ -361,8 +361,9 @@ static int launch_dmma(const BconvJobs& jobs, const ModSlot* slots, size_t cols,
     // amortised over them); the output walk is split over blockIdx.z when one conversion is too small
     const size_t tiles = cols / 16;
     const int z_max = (l_out_max + 7) / 8;
+    // fewer tiles per warp before splitting the output walk: a z-split repeats the pre-scale
     int tpw = 4;
-    while (tpw > 1 && ((tiles + 4 * tpw - 1) / (4 * tpw)) * jobs.count * z_max < (size_t)148 * 6) tpw >>= 1;
+    while (tpw > 1 && ((tiles + 4 * tpw - 1) / (4 * tpw)) * jobs.count < (size_t)148 * 6) tpw >>= 1;
     const unsigned gx = (unsigned)((tiles + 4 * tpw - 1) / (4 * tpw));
     const size_t ctas_xy = (size_t)gx * jobs.count;
     int z = (int)(((size_t)148 * 6 + ctas_xy - 1) / ctas_xy);
