@@ -369,7 +369,21 @@ def keyswitch(ct: Ciphertext, evk: SwitchingKey) -> Ciphertext:
 
 
 def keyswitch_batched(cts: list[Ciphertext], evk: SwitchingKey) -> list[Ciphertext]:
-    return [keyswitch(ct, evk) for ct in cts]
+    """Independent key switches under one key (reference keyswitch.py:456-459: a plain loop).
+    As many as fit the L2 together (scheduler.plan_batch) run concurrently, one workspace lane
+    and stream each; every result equals keyswitch(ct, evk) limb for limb."""
+    from .engine import get_engine
+    from .scheduler import concurrent_keyswitches
+
+    eng = get_engine()
+    cts = list(cts)
+    width = concurrent_keyswitches(evk.params, eng.lane_count(), len(cts))
+    if width <= 1:
+        return [keyswitch(ct, evk) for ct in cts]
+    out: list[Ciphertext] = []
+    for lo in range(0, len(cts), width):
+        out += eng.fork([(lambda ct=ct: keyswitch(ct, evk)) for ct in cts[lo:lo + width]])
+    return out
 
 
 def dump_pipeline_vectors(directory, ct: Ciphertext, evk: SwitchingKey) -> list[str]:

@@ -205,3 +205,24 @@ def test_fused_hmult_equals_tensor_then_relin_rescale(env, level, k):
     fused = eng.hmult_relin_rescale(ks_plan, md_plan, xa, xb, xa, xb, evk, level - k)
     d = eng.tensor_halves(xa, xb, xa, xb, eng.row_slots(basis))
     assert torch.equal(fused, eng.ks_relin_rescale(ks_plan, md_plan, d, evk, level - k))
+
+
+def test_keyswitch_batched_concurrent_lanes_equals_loop(env, golden):
+    """keyswitch_batched with several workspace lanes (scheduler.plan_batch decides how many key
+    switches are in flight) returns the limbs of a plain loop of keyswitch()."""
+    from paper_2512_18345_b200 import params
+
+    eng, ks = env.eng, env.ks
+    p = params.ParameterSet.from_dict(golden["params"]["ks12"])
+    s_from, s_to = ks.keygen(p, seed=1), ks.keygen(p, seed=2)
+    evk = ks.switching_keygen(s_from, s_to, p, seed=4)
+    rng = np.random.default_rng(6)
+    cts = [ks.encrypt(rng.integers(1, 9, p.n).astype(np.int64) * p.delta, s_from, p, seed=10 + i) for i in range(5)]
+    want = [ks.keyswitch(ct, evk) for ct in cts]
+    eng.set_lanes(4)
+    try:
+        got = ks.keyswitch_batched(cts, evk)
+    finally:
+        eng.set_lanes(1)
+    for g, w in zip(got, want):
+        assert np.array_equal(g.a.coeffs, w.a.coeffs) and np.array_equal(g.b.coeffs, w.b.coeffs)

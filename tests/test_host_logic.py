@@ -166,3 +166,29 @@ def test_counters_object():
     assert counters.snapshot()["butterflies"] == 3
     counters.reset()
     assert not any(counters.snapshot().values())
+
+
+def test_plan_batch_matches_reference_model(golden):
+    """scheduler.plan_batch reproduces the reference's B* (1/1/1 at ks48,
+    5/3/3 at ks24, 15/7/7 at ks12 on a 98 MB L2) and scales to B200's 126 MB."""
+    from paper_2512_18345_b200.params import ParameterSet
+    from paper_2512_18345_b200.scheduler import B200_L2_BYTES, concurrent_keyswitches, keyswitch_footprint, plan_batch
+
+    want = {"ks48": (1, 1, 1), "ks24": (5, 3, 3), "ks12": (15, 7, 7)}
+    for name, (s1, s3, full) in want.items():
+        p = ParameterSet.from_dict(golden["params"][name])
+        l2 = 98 * 10 ** 6
+        assert (plan_batch(p, "ks_stage1", l2).batch, plan_batch(p, "ks_stage3", l2).batch,
+                plan_batch(p, "ks_full", l2).batch) == (s1, s3, full)
+    p48 = ParameterSet.from_dict(golden["params"]["ks48"])
+    assert keyswitch_footprint(p48, 1) == 4 * 60 * 65536 * 4 and keyswitch_footprint(p48, 3) == 4 * 48 * 65536 * 4
+    plan = plan_batch(p48, "ks_full")
+    assert plan.l2_capacity == B200_L2_BYTES and plan.batch == 2 and not plan.spills
+    assert plan_batch(p48, "ks_full", 10 ** 6).spills
+    p12 = ParameterSet.from_dict(golden["params"]["ks12"])
+    assert concurrent_keyswitches(p12, lanes=4, pending=10) == 4
+    assert concurrent_keyswitches(p48, lanes=8, pending=10) == 2
+    assert concurrent_keyswitches(p48, lanes=1, pending=10) == 1
+    import pytest
+    with pytest.raises(ValueError):
+        plan_batch(p48, "nope")
