@@ -247,10 +247,13 @@ int ckks_ks_accumulate(ckks_ctx* ctx, int32_t plan, const uint32_t* ct_a, const 
                        int first, void* stream);
 /* HMult + relinearise + rescale from the four operand halves (each [l][n]) without a tensor
  * pass or (d0, d1, d2) buffers: values equal ckks_tensor + ckks_ks_relin_rescale bit for bit.
+ * (add_a, add_b), both or neither NULL: a ciphertext over the l - k output limbs added to the
+ * result inside the ModDown epilogue (poly_elementwise "add" without its own pass).
  * N = 2^16 only (CKKS_ERR_UNSUPPORTED otherwise: use the two-call route). */
 int ckks_hmult_relin_rescale(ckks_ctx* ctx, int32_t ks_plan, int32_t md_plan, const uint32_t* xa,
                              const uint32_t* xb, const uint32_t* ya, const uint32_t* yb,
-                             const uint32_t* evk, uint32_t* out_a, uint32_t* out_b, void* stream);
+                             const uint32_t* evk, const uint32_t* add_a, const uint32_t* add_b,
+                             uint32_t* out_a, uint32_t* out_b, void* stream);
 
 /* Baby steps and inner sums of a double-hoisted BSGS linear transform in one pass:
  * out[g] = sum_b p[g * nb + b] (.) u_b, u_b = the ckks_ks_hoisted_raw accumulator of rotation

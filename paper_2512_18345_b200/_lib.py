@@ -91,7 +91,7 @@ def load() -> ctypes.CDLL:
     L.ckks_ks_hoisted.argtypes = [vp, i32, vp, u32, vp, vp, vp, vp, vp]
     L.ckks_ks_hoisted_raw.argtypes = [vp, i32, vp, u32, vp, vp, vp, vp]
     L.ckks_ks_relin_rescale.argtypes = [vp, i32, i32, vp, vp, vp, vp, vp, vp, vp]
-    L.ckks_hmult_relin_rescale.argtypes = [vp, i32, i32, vp, vp, vp, vp, vp, vp, vp, vp]
+    L.ckks_hmult_relin_rescale.argtypes = [vp, i32, i32, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]
     L.ckks_bsgs_inner.argtypes = [vp, i32, vp, vp, vp, ctypes.c_int, vp, vp, ctypes.c_int, vp, vp, vp, vp]
     L.ckks_ks_accumulate.argtypes = [vp, i32, vp, vp, ctypes.c_int, vp]
     L.ckks_ks_accumulate_rot.argtypes = [vp, i32, vp, vp, ctypes.c_uint32, vp, ctypes.c_int, vp]

@@ -457,9 +457,11 @@ class Bootstrapper:
         t = ckks.mod_drop(ckks.Ciphertext(t.a, t.b, target_scale), level)
         return ckks.add_plain(t, self._const(c0, level, target_scale))
 
-    def _mul(self, x, y):
+    def _mul(self, x, y, addend=None):
+        """x * y, relinearised and rescaled by two limbs; `addend` (at the result's level and
+        scale) is added inside the same pipeline."""
         lvl = min(ckks.level_of(x), ckks.level_of(y))
-        return ckks.hmult_rescale(ckks.mod_drop(x, lvl), ckks.mod_drop(y, lvl), self.keys.relin, 2)
+        return ckks.hmult_rescale(ckks.mod_drop(x, lvl), ckks.mod_drop(y, lvl), self.keys.relin, 2, addend=addend)
 
     def _exp_taylor(self, x, coef):
         """sum_k coef[k] x^k by a balanced power tree (depth ceil(log2(degree+1)))."""
@@ -495,14 +497,12 @@ class Bootstrapper:
             xp_d = ckks.mod_drop(xp, lvl_in) if ckks.level_of(xp) > lvl_in else xp
             dropped = math.prod(m.q for m in self.params.q_basis[want_level:lvl_in])
 
-            def high():
-                r = realise(right, want_scale * dropped / xp_d.scale, lvl_in)
-                prod = self._mul(r, xp_d)
-                return ckks.Ciphertext(prod.a, prod.b, want_scale)
-
-            # the two halves are independent: spread them over the lanes this branch owns
-            prod, low = eng.fork([high, lambda: realise(left, want_scale, want_level)])
-            return ckks.add(prod, low)
+            # the two halves are independent: spread them over the lanes this branch owns; the low
+            # half then rides in the ModDown epilogue of the product (no separate add)
+            r, low = eng.fork([lambda: realise(right, want_scale * dropped / xp_d.scale, lvl_in),
+                               lambda: realise(left, want_scale, want_level)])
+            prod = self._mul(r, xp_d, addend=low)
+            return ckks.Ciphertext(prod.a, prod.b, want_scale)
 
         tree = build(0, 1 << depth)
         out_level = ckks.level_of(x) - 2 * depth

@@ -418,7 +418,8 @@ def hmult(x: Ciphertext, y: Ciphertext, rlk: ks.SwitchingKey) -> Ciphertext:
     return relinearize(d0, d1, d2, rlk, x.scale * y.scale)
 
 
-def hmult_rescale(x: Ciphertext, y: Ciphertext, rlk: ks.SwitchingKey, k: int = 1) -> Ciphertext:
+def hmult_rescale(x: Ciphertext, y: Ciphertext, rlk: ks.SwitchingKey, k: int = 1,
+                  addend: Ciphertext | None = None) -> Ciphertext:
     """rescale(hmult(x, y), k) with the relinearisation ModDown and the rescale merged into
     one division by P * (the k dropped limbs): one base conversion and one NTT fewer per
     multiplication.  Same value as the two-step route up to the rounding of the division."""
@@ -429,6 +430,11 @@ def hmult_rescale(x: Ciphertext, y: Ciphertext, rlk: ks.SwitchingKey, k: int = 1
     params = rlk.params
     level = level_of(x)
     n = x.a.n
+    if addend is not None and (n != 65536 or level <= k):
+        # `addend` (a ciphertext at the output level, same scale up to the caller) rides in the
+        # ModDown epilogue of the fused pipeline only; elsewhere it is a separate add
+        out = hmult_rescale(x, y, rlk, k)
+        return add(Ciphertext(a=out.a, b=out.b, scale=addend.scale), addend)
     if n % 4 or level <= k:
         return rescale(hmult(x, y, rlk), k)
     basis = x.a.basis
@@ -440,8 +446,12 @@ def hmult_rescale(x: Ciphertext, y: Ciphertext, rlk: ks.SwitchingKey, k: int = 1
     if n == 65536:
         # no tensor pass: d2 is formed while the first inverse transform loads, d1 / d0 inside the
         # inner product (same limbs as the two-call route below)
+        if addend is not None and level_of(addend) != level - k:
+            raise RnsError("addend must live at the output level of hmult_rescale")
         out = eng.hmult_relin_rescale(ks_plan, md_plan, x.a.data, x.b.data, y.a.data, y.b.data,
-                                      rlk.matrix(), level - k)
+                                      rlk.matrix(), level - k,
+                                      None if addend is None else addend.a.data,
+                                      None if addend is None else addend.b.data)
     else:
         d = eng.tensor_halves(x.a.data, x.b.data, y.a.data, y.b.data, eng.row_slots(basis))
         out = eng.ks_relin_rescale(ks_plan, md_plan, d, rlk.matrix(), level - k)

@@ -950,7 +950,8 @@ int ckks_ks_relin_rescale(ckks_ctx* ctx, int32_t ks_plan, int32_t md_plan, const
 // ckks_ks_relin_rescale (exact modular arithmetic), five limb transfers per row and one launch less.
 int ckks_hmult_relin_rescale(ckks_ctx* ctx, int32_t ks_plan, int32_t md_plan, const uint32_t* xa,
                              const uint32_t* xb, const uint32_t* ya, const uint32_t* yb,
-                             const uint32_t* evk, uint32_t* out_a, uint32_t* out_b, void* stream) {
+                             const uint32_t* evk, const uint32_t* add_a, const uint32_t* add_b,
+                             uint32_t* out_a, uint32_t* out_b, void* stream) {
     KsPlan *pl, *md;
     CKS(get_plan(ctx, ks_plan, &pl));
     CKS(need_full_plan(pl));
@@ -972,8 +973,9 @@ int ckks_hmult_relin_rescale(ckks_ctx* ctx, int32_t ks_plan, int32_t md_plan, co
     ip.pmod = pl->d_pmod;
     ip.pmod_s = pl->d_pmod_s;
     CKS(inner_product_launch(ip, ctx->d_slots, st));
+    // (add_a, add_b): a ciphertext at the output level added inside the ModDown epilogue
     return stage3_core(ctx, md, acc_a, acc_b, acc_a + (size_t)md->l * n, acc_b + (size_t)md->l * n,
-                       nullptr, out_a, out_b, st, 0, nullptr, pl->ws_conv, pl->ws_pc);
+                       add_b, out_a, out_b, st, 0, add_a, pl->ws_conv, pl->ws_pc);
 }
 
 // ---- giant steps sharing one ModDown ---------------------------------------------------

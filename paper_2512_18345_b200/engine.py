@@ -362,11 +362,15 @@ class Engine:
                                                   out[0].data_ptr(), out[1].data_ptr(), self.stream()))
         return out
 
-    def hmult_relin_rescale(self, ks_plan: int, md_plan: int, xa, xb, ya, yb, evk, out_rows: int):
-        """HMult + relinearise + rescale from the operand halves in one pipeline (no tensor pass)."""
+    def hmult_relin_rescale(self, ks_plan: int, md_plan: int, xa, xb, ya, yb, evk, out_rows: int,
+                            add_a=None, add_b=None):
+        """HMult + relinearise + rescale from the operand halves in one pipeline (no tensor pass);
+        (add_a, add_b): a ciphertext at the output level added inside the last kernel."""
         out = self.empty(2, out_rows, xa.shape[1])
         _lib.check(self.lib.ckks_hmult_relin_rescale(self.ctx, ks_plan, md_plan, xa.data_ptr(), xb.data_ptr(),
                                                      ya.data_ptr(), yb.data_ptr(), evk.data_ptr(),
+                                                     None if add_a is None else add_a.data_ptr(),
+                                                     None if add_b is None else add_b.data_ptr(),
                                                      out[0].data_ptr(), out[1].data_ptr(), self.stream()))
         return out
 
