@@ -128,3 +128,30 @@ def test_linear_transform_fused_baby_steps_equal_unfused(boot_env):
     assert ckks.level_of(outs[0]) == level - 2
     got = ckks.decrypt_decode(outs[0], sk, p)
     assert np.abs(got - apply_diagonals(diags, z)).max() < 2.0 ** -20
+
+
+def test_captured_multi_lane_graph_equals_eager_single_lane(boot_env):
+    """Race check: the whole bootstrap captured as one CUDA graph over 4 stream lanes (nested
+    forks, per-lane workspaces, shared ModDowns) and replayed three times gives exactly the limbs
+    of the eager single-lane run -- all arithmetic is exact, so any ordering hazard would show."""
+    import torch
+
+    ckks, p, sk, boot = boot_env
+    from paper_2512_18345_b200.engine import get_engine
+
+    eng = get_engine()
+    rng = np.random.default_rng(77)
+    n = p.n // 2
+    z = rng.uniform(-1, 1, n) + 1j * rng.uniform(-1, 1, n)
+    ct = ckks.encrypt(ckks.encode(z, p, level=2, scale=boot.delta_in), sk, p, seed=15)
+    ref = boot.bootstrap(ct)
+    ref_t = torch.stack([ref.a.data, ref.b.data]).clone()
+    eng.set_lanes(4)
+    try:
+        replay = boot.capture(ct)
+        for _ in range(3):
+            out = replay(ct)
+            assert torch.equal(torch.stack([out.a.data, out.b.data]), ref_t)
+    finally:
+        torch.cuda.synchronize()
+        eng.set_lanes(1)
