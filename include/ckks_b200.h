@@ -266,6 +266,13 @@ int ckks_bsgs_inner(ckks_ctx* ctx, int32_t plan, const uint32_t* raised, const u
                     const uint32_t* ct_b, int nb, const uint32_t* k, const uint32_t* const* evk, int ng,
                     const uint32_t* const* p, const uint32_t* zero, uint32_t* const* out, void* stream);
 
+/* ckks_ks_stage3 (ModDown) of `count` <= 4 accumulators in one set of launches: qp is
+ * [count][2][l + alpha][n] (Q rows then P rows per half), out [count][2][l][n]; element g uses the
+ * workspace of lane (current + g), so count lanes from the current one must exist and be idle.
+ * Same limbs as count calls of ckks_ks_stage3.  N = 2^16 only. */
+int ckks_ks_stage3_batch(ckks_ctx* ctx, int32_t plan, int count, const uint32_t* qp, uint32_t* out,
+                         void* stream);
+
 /* ckks_ks_accumulate for the rotation sigma_k of (ct_a, ct_b) without materialising it: the
  * automorphism is a gather inside the inner product and P * sigma_k(ct_b) is lifted into the b
  * accumulator (no separate automorphism pass, no separate sum of the b parts). */

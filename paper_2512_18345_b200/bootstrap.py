@@ -216,8 +216,11 @@ class LinearTransform:
                     raise RnsError(f"no Galois key for rotation {b * self.step}")
                 ks_idx.append(k)
                 evks.append(keys.galois[k].matrix())
-            for g0 in range(0, len(giants), 8):
-                chunk = giants[g0:g0 + 8]
+            # the unrotated giant step first, the moving ones after it in one allocation (so that a
+            # batched ModDown can take them as one [count, 2, ext, n] slice)
+            order = [g for g in giants if g == 0] + [g for g in giants if g != 0]
+            for g0 in range(0, len(order), 8):
+                chunk = order[g0:g0 + 8]
                 table = [[self.table[g][b].poly.data if b in self.table[g] else None for b in babies] for g in chunk]
                 qps.update(zip(chunk, eng.bsgs_inner(plan, raised, ct.a.data, b_half, ks_idx, evks, table, ext)))
         else:
@@ -238,6 +241,31 @@ class LinearTransform:
             return eng.ks_stage3(plan, qp[0, :level], qp[1, :level], qp[0, level:], qp[1, level:])
 
         inner_sum.raw = qps          # the Q||P accumulators themselves (giant step 0 needs no ModDown)
+
+        def inner_sums(gs):
+            """ModDown of several giant steps' inner sums; one set of launches per run of up to
+            four accumulators that are adjacent in memory, over that many of the caller's lanes."""
+            out = {}
+            width = min(4, eng.lane_count())
+            i = 0
+            while i < len(gs):
+                run = [gs[i]]
+                while (len(run) < width and i + len(run) < len(gs) and n_ring == 65536 and
+                       qps[gs[i + len(run)]].data_ptr() == qps[run[-1]].data_ptr() + 2 * ext * n_ring * 4):
+                    run.append(gs[i + len(run)])
+                if len(run) == 1:
+                    out[run[0]] = inner_sum(run[0])
+                else:
+                    first = qps[run[0]]
+                    base = first._base if first._base is not None else first
+                    at = (first.data_ptr() - base.data_ptr()) // (2 * ext * n_ring * 4)
+                    res = eng.ks_stage3_batch(plan, base[at:at + len(run)], level)
+                    for j, g in enumerate(run):
+                        out[g] = res[j]
+                i += len(run)
+            return out
+
+        inner_sum.many = inner_sums
         return inner_sum
 
     def rotations(self) -> set[int]:
@@ -269,7 +297,10 @@ class LinearTransform:
         # it is: no ModDown of its own
         base_raw = getattr(inner_sum, "raw", {}).get(0) if moving and p_ok(self) else None
         todo = [g for g in self.giants if not (g == 0 and base_raw is not None)]
-        inners = dict(zip(todo, eng.fork([(lambda g=g: inner_sum(g)) for g in todo])))
+        if hasattr(inner_sum, "many"):
+            inners = inner_sum.many(todo)              # batched ModDowns (adjacent accumulators)
+        else:
+            inners = dict(zip(todo, eng.fork([(lambda g=g: inner_sum(g)) for g in todo])))
         base = inners.get(0)
         scale = ct.scale * self.pt_scale
         if not moving:

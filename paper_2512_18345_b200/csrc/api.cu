@@ -150,6 +150,9 @@ struct KsPlan {
     uint32_t *ws_coeff = nullptr, *ws_raised = nullptr, *ws_acc = nullptr, *ws_conv = nullptr,
              *ws_pc = nullptr;
     bool moddown_only = false;
+    // row maps of batched ModDowns (ckks_ks_stage3_batch), by batch size; built on first use
+    struct BatchMaps { int32_t *in_row, *pc_row, *p_slot, *conv_row, *q_slot; size_t lane_words; };
+    std::map<int, BatchMaps> s3_batch;
 };
 
 }  // namespace ckks
@@ -976,6 +979,80 @@ int ckks_hmult_relin_rescale(ckks_ctx* ctx, int32_t ks_plan, int32_t md_plan, co
     // (add_a, add_b): a ciphertext at the output level added inside the ModDown epilogue
     return stage3_core(ctx, md, acc_a, acc_b, acc_a + (size_t)md->l * n, acc_b + (size_t)md->l * n,
                        add_b, out_a, out_b, st, 0, add_a, pl->ws_conv, pl->ws_pc);
+}
+
+// ModDown of `count` Q||P accumulators at once (the inner sums of the moving giant steps of a
+// BSGS transform): the same five kernels as ckks_ks_stage3, each over count times the rows, instead
+// of count chains of five small launches.  Element g works in the arena of lane (current + g); qp
+// is [count][2][l + alpha][n], out [count][2][l][n].  N = 2^16, count <= 4.
+int ckks_ks_stage3_batch(ckks_ctx* ctx, int32_t plan, int count, const uint32_t* qp, uint32_t* out,
+                         void* stream) {
+    KsPlan* pl;
+    CKS(get_plan(ctx, plan, &pl));
+    if (count < 1 || 2 * count > kMaxBconvJobs || ctx->lane + count > ctx->lanes) {
+        set_last_error("batched ModDown of %d accumulators needs that many lanes from the current one and at most %d",
+                       count, kMaxBconvJobs / 2);
+        return CKKS_ERR_ARG;
+    }
+    if (!ntt_can_fuse_moddown(pl->n) || ctx->ws_words % pl->n) { set_last_error("batched ModDown needs N = 2^16"); return CKKS_ERR_UNSUPPORTED; }
+    cudaStream_t st = (cudaStream_t)stream;
+    const size_t n = pl->n;
+    const int l = pl->l, alpha = pl->alpha, ext = pl->ext;
+    auto it = pl->s3_batch.find(count);
+    if (it == pl->s3_batch.end() || it->second.lane_words != ctx->ws_words) {
+        // rows of element g: accumulator at g * 2 ext (+ ext for the b half), workspace at g lanes
+        const int32_t lane_rows = (int32_t)(ctx->ws_words / n);
+        std::vector<int32_t> in_row, pc_row, p_slot, conv_row, q_slot;
+        std::vector<int32_t> ps(2 * alpha), qs(2 * l);
+        CK(cudaMemcpy(ps.data(), pl->d_s3_p_slot, sizeof(int32_t) * 2 * alpha, cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(qs.data(), pl->d_s3_q_slot, sizeof(int32_t) * 2 * l, cudaMemcpyDeviceToHost));
+        for (int g = 0; g < count; ++g)
+            for (int h = 0; h < 2; ++h) {
+                for (int j = 0; j < alpha; ++j) {
+                    in_row.push_back(g * 2 * ext + h * ext + l + j);
+                    pc_row.push_back(g * lane_rows + h * alpha + j);
+                    p_slot.push_back(ps[h * alpha + j]);
+                }
+                for (int i = 0; i < l; ++i) {
+                    conv_row.push_back(g * lane_rows + h * l + i);
+                    q_slot.push_back(qs[h * l + i]);
+                }
+            }
+        KsPlan::BatchMaps m{};
+        CKS(upload(in_row, &m.in_row));
+        CKS(upload(pc_row, &m.pc_row));
+        CKS(upload(p_slot, &m.p_slot));
+        CKS(upload(conv_row, &m.conv_row));
+        CKS(upload(q_slot, &m.q_slot));
+        m.lane_words = ctx->ws_words;
+        for (void* ptr : {(void*)m.in_row, (void*)m.pc_row, (void*)m.p_slot, (void*)m.conv_row, (void*)m.q_slot})
+            ctx->owned.push_back(ptr);
+        it = pl->s3_batch.insert_or_assign(count, m).first;
+    }
+    const KsPlan::BatchMaps& m = it->second;
+    CKS(ntt_launch(qp, pl->ws_pc, m.p_slot, ctx->d_slots, RowMap{m.in_row, m.pc_row}, count * 2 * alpha, pl->n, 1, st));
+    BconvJobs jobs;
+    jobs.count = 2 * count;
+    for (int g = 0; g < count; ++g)
+        for (int h = 0; h < 2; ++h) {
+            BconvJob& j = jobs.job[2 * g + h];
+            j.tab = ctx->tables[pl->moddown_table]->dev;
+            j.in = pl->ws_pc + (size_t)g * ctx->ws_words + (size_t)h * alpha * n;
+            j.in_stride = n;
+            j.out = pl->ws_conv + (size_t)g * ctx->ws_words + (size_t)h * l * n;
+            j.out_stride = n;
+            j.out_row = nullptr;
+        }
+    CKS(bconv_launch_jobs(jobs, ctx->d_slots, n, st));
+    ModDownEpilogueArgs e{};
+    e.xq_a = qp; e.xq_b = qp + (size_t)ext * n; e.conv = pl->ws_conv; e.fold_a = nullptr; e.fold_b = nullptr;
+    e.out_a = out; e.out_b = out + (size_t)l * n;
+    e.q_slot = pl->d_q_slot; e.pinv = pl->d_pinv; e.pinv_s = pl->d_pinv_s;
+    e.l = l; e.n = pl->n; e.galois = 0; e.lg = log2u(pl->n);
+    e.xq_stride = (size_t)2 * ext * n;
+    e.out_stride = (size_t)2 * l * n;
+    return ntt_launch(pl->ws_conv, pl->ws_conv, m.q_slot, ctx->d_slots, RowMap{m.conv_row, m.conv_row},
+                      count * 2 * l, pl->n, 0, st, &e);
 }
 
 // ---- giant steps sharing one ModDown ---------------------------------------------------

@@ -196,6 +196,9 @@ struct ModDownEpilogueArgs {
     int l;
     uint32_t n;
     uint32_t galois, lg;        // galois != 0: fold_b is read through X -> X^galois
+    // batched ModDown (several accumulators in one launch, rows = batch * 2 l): element g reads
+    // xq_* + g * xq_stride and writes out_* + g * out_stride (words); 0 for a single ModDown
+    size_t xq_stride, out_stride;
 };
 // All baby steps of a double-hoisted BSGS linear transform fused with all giant-step inner
 // sums: for every baby step b the Q||P accumulator u_b of the rotation sigma_{k_b} of the

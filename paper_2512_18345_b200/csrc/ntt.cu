@@ -254,13 +254,14 @@ ntt16_fwd_contig(const uint32_t* in, uint32_t* out, const int32_t* __restrict__ 
     const ModSlot& m = slots[row_slot[blockIdx.y]];
     const uint32_t q = m.q;
     const uint32_t B = blockIdx.x * 16 + blk;          // 256-element block index within the limb
-    const int ep_row = EPI ? blockIdx.y % ep.l : 0, ep_half = EPI ? blockIdx.y / ep.l : 0;
+    const int ep_row = EPI ? blockIdx.y % ep.l : 0, ep_half = EPI ? (blockIdx.y / ep.l) & 1 : 0;
+    const size_t ep_g = EPI ? blockIdx.y / (2 * ep.l) : 0;         // element of a batched ModDown
     const size_t ep_at = (size_t)ep_row * kN16 + B * 256 + 16 * e;
     pdl_trigger();
     if (EPI) {
         // x_Q (and the folded polynomial) are needed only after the last stage: pull their
         // lines into L2 now
-        asm volatile("prefetch.global.L2 [%0];" :: "l"((ep_half ? ep.xq_b : ep.xq_a) + ep_at));
+        asm volatile("prefetch.global.L2 [%0];" :: "l"((ep_half ? ep.xq_b : ep.xq_a) + ep_g * ep.xq_stride + ep_at));
         const uint32_t* f = ep_half ? ep.fold_b : ep.fold_a;
         if (f && !ep.galois) asm volatile("prefetch.global.L2 [%0];" :: "l"(f + ep_at));
     }
@@ -290,9 +291,9 @@ ntt16_fwd_contig(const uint32_t* in, uint32_t* out, const int32_t* __restrict__ 
     ct16(v, q, TW_MUL(s == 0 ? tw.t1 : (s == 1 ? tw.t2[gi & 1] : (s == 2 ? tw.t4[gi & 3] : tw.t8[gi & 7]))));
     if (EPI) {
         const uint32_t pinv = ep.pinv[ep_row], pinv_s = ep.pinv_s[ep_row];
-        const uint32_t* x = (ep_half ? ep.xq_b : ep.xq_a) + ep_at;
+        const uint32_t* x = (ep_half ? ep.xq_b : ep.xq_a) + ep_g * ep.xq_stride + ep_at;
         const uint32_t* fsrc = ep_half ? ep.fold_b : ep.fold_a;
-        uint32_t* o = (ep_half ? ep.out_b : ep.out_a) + ep_at;
+        uint32_t* o = (ep_half ? ep.out_b : ep.out_a) + ep_g * ep.out_stride + ep_at;
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
             uint32_t xv[8], r[8];
@@ -430,8 +431,9 @@ int ntt_launch(const uint32_t* in, uint32_t* out, const int32_t* row_slot, const
         set_last_error("product-on-load needs an inverse N = 2^16 transform");
         return CKKS_ERR_ARG;
     }
-    if (epi && (inverse || !ntt_can_fuse_moddown(n) || rows != 2 * epi->l)) {
-        set_last_error("fused ModDown epilogue needs a forward N = 2^16 transform over 2 l rows");
+    if (epi && (inverse || !ntt_can_fuse_moddown(n) || rows % (2 * epi->l) != 0 ||
+                (rows != 2 * epi->l && (epi->fold_a || epi->fold_b)))) {
+        set_last_error("fused ModDown epilogue needs a forward N = 2^16 transform over (a multiple of) 2 l rows");
         return CKKS_ERR_ARG;
     }
     if (n == (uint32_t)kN16) {

@@ -315,6 +315,14 @@ class Engine:
                                            out[1].data_ptr(), self.stream()))
         return out
 
+    def ks_stage3_batch(self, plan: int, qps, l: int):
+        """ModDown of qps = [count, 2, ext, n] accumulators in one set of launches -> [count, 2, l, n].
+        Element g works in the arena of lane (current + g): the caller owns those lanes."""
+        count, n = qps.shape[0], qps.shape[3]
+        out = self.empty(count, 2, l, n)
+        _lib.check(self.lib.ckks_ks_stage3_batch(self.ctx, plan, count, qps.data_ptr(), out.data_ptr(), self.stream()))
+        return out
+
     def ks_hoisted(self, plan: int, raised, k: int, evk, ct_b):
         """Key switch of the ciphertext rotated by X -> X^k from pre-raised digits."""
         out = self.empty(2, ct_b.shape[0], ct_b.shape[1])
@@ -343,7 +351,8 @@ class Engine:
         pass; returns the [2, ext, n] Q||P accumulators of the giant steps."""
         nb, ng = len(ks), len(table)
         n = ct_a.shape[1]
-        outs = [self.empty(2, ext, n) for _ in range(ng)]
+        big = self.empty(ng, 2, ext, n)          # one allocation: a batched ModDown can take a slice of it
+        outs = [big[g] for g in range(ng)]
         kk = (ctypes.c_uint32 * nb)(*ks)
         ep = (ctypes.c_void_p * nb)(*[None if e is None else e.data_ptr() for e in evks])
         flat = [None if pt is None else pt.data_ptr() for row in table for pt in row]

@@ -226,3 +226,25 @@ def test_keyswitch_batched_concurrent_lanes_equals_loop(env, golden):
         eng.set_lanes(1)
     for g, w in zip(got, want):
         assert np.array_equal(g.a.coeffs, w.a.coeffs) and np.array_equal(g.b.coeffs, w.b.coeffs)
+
+
+def test_batched_moddown_equals_separate_moddowns(env):
+    """ckks_ks_stage3_batch over three accumulators (one set of launches, element g in the arena
+    of lane g) against three ckks_ks_stage3 calls: equal limb for limb."""
+    eng, torch, p = env.eng, env.torch, env.ks48
+    level = 30
+    basis = p.q_basis[:level]
+    ext = level + p.alpha
+    rng = np.random.default_rng(41)
+    plan = eng.ks_plan(p.n, basis, p.p_basis, p.alpha, p.l + p.alpha, p.l)
+    qps = torch.stack([torch.stack([eng.upload(rand_rows(basis + p.p_basis, p.n, rng)) for _ in range(2)])
+                       for _ in range(3)])
+    want = [eng.ks_stage3(plan, q[0, :level], q[1, :level], q[0, level:], q[1, level:]) for q in qps]
+    eng.set_lanes(3)
+    try:
+        got = eng.ks_stage3_batch(plan, qps, level)
+        torch.cuda.synchronize()
+    finally:
+        eng.set_lanes(1)
+    for g in range(3):
+        assert torch.equal(got[g], want[g]), g
