@@ -328,7 +328,7 @@ ntt16_fwd_contig(const uint32_t* in, uint32_t* out, const int32_t* __restrict__ 
 // MUL: the transform's input is the element-wise product in (.) in2 of two evaluation-domain
 // polynomials (the d2 = a1 * a2 term of HMult), formed on load instead of by a tensor pass.
 template <bool MUL>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, MUL ? 3 : 6)
 ntt16_inv_contig(const uint32_t* in, uint32_t* out, const int32_t* __restrict__ row_slot,
                  const ModSlot* __restrict__ slots, RowMap rm, const uint32_t* in2) {
     __shared__ uint32_t tile[16 * 272];
