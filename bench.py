@@ -562,6 +562,7 @@ def main():
     if args.impl == "reference":
         run_reference(args)
     else:
+        args.warmup = max(args.warmup, 3)      # timing rule: at least three untimed warm-up steps
         run_b200(args)
 
 
