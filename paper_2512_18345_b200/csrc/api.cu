@@ -709,12 +709,12 @@ static int stage1_core(ckks_ctx* ctx, KsPlan* pl, const uint32_t* a, uint32_t* r
     CKS(ntt_launch(a, pl->ws_coeff, pl->d_q_slot, ctx->d_slots, RowMap{nullptr, nullptr}, pl->l,
                    pl->n, 1, st, nullptr, mul_in));
     for (int t0 = 0; t0 < pl->beta;) {
+        // all digits in one launch, the partial last digit included (bconv_launch_jobs splits
+        // unequal sizes itself when the kernel in use cannot stack them)
         BconvJobs jobs;
         jobs.count = 0;
-        const int l_in0 = pl->digit_hi[t0] - pl->digit_lo[t0];
         int t = t0;
         for (; t < pl->beta && jobs.count < kMaxBconvJobs; ++t) {
-            if (pl->digit_hi[t] - pl->digit_lo[t] != l_in0) break;
             BconvJob& j = jobs.job[jobs.count++];
             j.tab = ctx->tables[pl->raise_table[t]]->dev;
             j.in = pl->ws_coeff + (size_t)pl->digit_lo[t] * n;

@@ -246,16 +246,22 @@ bconv_dmma(BconvJobs jobs, const ModSlot* __restrict__ slots, size_t cols, int c
     uint4* s_om = sm4 + ((size_t)((chunk + 7) & ~7) * KP * sizeof(double)) / sizeof(uint4);   // {q, qinv, out row, 2^48 mod q}
     uint4* s_in = s_om + ((chunk + 7) & ~7);                               // {q, inv_qhat, shoup(inv_qhat), -}
     {
-        const uint4* src = reinterpret_cast<const uint4*>(job.tab.t_f64 + (size_t)i_lo * KP);
-        uint4* dst = reinterpret_cast<uint4*>(s_t);
-        for (int idx = threadIdx.x; idx < rows_pad * KP / 2; idx += blockDim.x) dst[idx] = src[idx];
+        // a conversion with fewer input limbs than the launch's KP (the partial last digit stacked
+        // with the full ones) has a narrower table: zero-fill the extra columns
+        const int kpj = job.tab.kp;
+        const double* src = job.tab.t_f64 + (size_t)i_lo * kpj;
+        for (int idx = threadIdx.x; idx < rows_pad * KP; idx += blockDim.x) {
+            const int i = idx / KP, k = idx - i * KP;
+            s_t[idx] = k < kpj ? src[(size_t)i * kpj + k] : 0.0;
+        }
     }
     for (int r = threadIdx.x; r < rows_pad; r += blockDim.x) {
         uint4 om = job.tab.om[i_lo + r];
         if (job.out_row && i_lo + r < i_hi) om.z = (uint32_t)job.out_row[i_lo + r];
         s_om[r] = om;
     }
-    for (int k = threadIdx.x; k < KP; k += blockDim.x) s_in[k] = job.tab.inc[k];
+    for (int k = threadIdx.x; k < KP; k += blockDim.x)
+        s_in[k] = k < job.tab.kp ? job.tab.inc[k] : make_uint4(3u, 0u, 0u, 0u);
     pdl_wait();                                 // tables are static; the residues are not
     if (tile < tiles) fetch(tile);
     __syncthreads();
@@ -417,15 +423,13 @@ static int launch_fast(const BconvJobs& jobs, const ModSlot* slots, size_t cols,
 
 int bconv_launch_jobs(const BconvJobs& jobs, const ModSlot* slots, size_t cols, cudaStream_t st) {
     if (jobs.count <= 0 || cols == 0) return CKKS_OK;
-    const int l_in = jobs.job[0].tab.l_in;
+    int l_in = jobs.job[0].tab.l_in;
     int l_out_max = 0;
-    bool fast = true, pairs = cols % 2 == 0;
+    bool fast = true, pairs = cols % 2 == 0, mixed = false;
     for (int j = 0; j < jobs.count; ++j) {
         const BconvJob& jb = jobs.job[j];
-        if (jb.tab.l_in != l_in) {
-            set_last_error("stacked conversions must share l_in");
-            return CKKS_ERR_ARG;
-        }
+        if (jb.tab.l_in != jobs.job[0].tab.l_in) mixed = true;     // only the tensor-core kernel stacks these
+        if (jb.tab.l_in > l_in) l_in = jb.tab.l_in;
         if (jb.tab.l_out > l_out_max) l_out_max = jb.tab.l_out;
         fast = fast && jb.tab.all31;
         pairs = pairs && (((uintptr_t)jb.in | (uintptr_t)jb.out) % 8 == 0) &&
@@ -443,6 +447,18 @@ int bconv_launch_jobs(const BconvJobs& jobs, const ModSlot* slots, size_t cols, 
                 default: return launch_dmma<4>(jobs, slots, cols, l_out_max, st);
             }
         }
+    }
+    if (mixed) {
+        // the other kernels are specialised on one l_in: run equal-sized groups one after the other
+        for (int j0 = 0; j0 < jobs.count;) {
+            BconvJobs part;
+            part.count = 0;
+            int j = j0;
+            for (; j < jobs.count && jobs.job[j].tab.l_in == jobs.job[j0].tab.l_in; ++j) part.job[part.count++] = jobs.job[j];
+            CKS(bconv_launch_jobs(part, slots, cols, st));
+            j0 = j;
+        }
+        return CKKS_OK;
     }
     if (fast && l_in <= 16) {
         switch (l_in) {
