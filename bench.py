@@ -192,16 +192,16 @@ def oracle_step(workload):
 
 # key switches of one bootstrap by number of active limbs (CoeffToSlot at 48/46/44, EvalMod
 # 42..24, SlotToCoeff 21..19), from the circuit in paper_2512_18345_b200/bootstrap.py:
-# 3 x 14 rotations per linear transform side, 2 branches x 15 relinearisations + 3 conjugations.
+# 3 x 14 rotations per linear transform side, 2 branches x 11 relinearisations + 3 conjugations.
 def bootstrap_keyswitch_levels():
     levels = []
     for lvl in (48, 46, 44):
         levels += [lvl] * 14
     levels += [42]                                 # conjugation after CoeffToSlot
     for _branch in range(2):
-        levels += [42, 40, 38]                     # x^2, x^4, x^8
-        levels += [40, 40, 40, 38, 38, 36]         # power-tree products of the degree-13 polynomial
-        levels += [34, 32, 30, 28, 26, 24]         # squarings
+        levels += [42, 40, 40, 38, 36]             # x^2, x^3, x^4, x^8, x^12
+        levels += [34]                             # one relinearisation for q_1 x^4 + q_2 x^8 + q_3 x^12
+        levels += [32, 30, 28, 26, 24]             # squarings
         levels += [22]                             # conjugation for the sine
     for lvl in (21, 20, 19):
         levels += [lvl] * 14

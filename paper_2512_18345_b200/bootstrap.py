@@ -342,13 +342,20 @@ class LinearTransform:
 # ---------------------------------------------------------------------------
 @dataclass
 class BootstrapConfig:
-    squarings: int = 6            # r: exp(i*theta / 2^r) is squared r times
-    degree: int = 13              # degree of the polynomial for exp on |x| <= 2*pi*K / 2^r
-    approx: str = "chebyshev"     # "chebyshev": interpolation at Chebyshev nodes of that interval
-                                  # (near-minimax: degree 13 errs 2^-27 on the message where the degree-15
-                                  # Taylor series errs 2^-20, for one HMult and one PMult pair less per
-                                  # branch); "taylor": the truncated series
-    k_bound: int = 16             # |I| <= K
+    scheme: str = "ps"            # polynomial evaluation: "ps" (Paterson-Stockmeyer, degree <= 15, five
+                                  # limb pairs deep, lazy relinearisation: six key switches) or "tree"
+                                  # (balanced power tree, depth ceil(log2(degree+1)), one key switch per
+                                  # product: nine for degree 13)
+    squarings: int = 5            # r: exp(i*theta / 2^r) is squared r times
+    degree: int = 15              # degree of the polynomial for exp on |x| <= 2*pi*K / 2^r
+    approx: str = "chebyshev"     # "chebyshev": interpolation at the Chebyshev nodes of that interval
+                                  # (near-minimax); "taylor": the truncated series.  The approximation
+                                  # error is a deterministic function of I, so SlotToCoeff adds it up
+                                  # coherently (x sqrt(slots)): it has to sit ~8 bits below the target
+                                  # precision.  Degree 15 on K = 12 errs 2^-28 on the message.
+    k_bound: int = 12             # |I| <= K for the polynomial's interval.  I is a sum of h + 1 terms
+                                  # uniform in [-1/2, 1/2): standard deviation 1.66 at h = 32, K = 12 is
+                                  # 7.2 sigma (6e-14 per coefficient); the absolute bound is (h + 1) / 2
     log_delta_in: int = 52        # input scale 2^log_delta_in at two limbs (Q0 ~ 2^62)
     groups: int = 3               # stage groups per linear transform
     n1: int | None = None         # baby-step count (default ~ sqrt of the diagonal span)
@@ -401,7 +408,7 @@ class Bootstrapper:
         # ---- level plan -----------------------------------------------------------
         self.lvl_cts = L                                   # CoeffToSlot: two limbs per group (its error
         self.lvl_evalmod = L - 2 * cfg.groups              # is amplified by Q0*2^r/(2*pi*Delta) ~ 2^13)
-        depth = math.ceil(math.log2(cfg.degree + 1))       # Taylor polynomial depth
+        depth = 5 if cfg.scheme == "ps" else math.ceil(math.log2(cfg.degree + 1))   # polynomial depth
         self.lvl_after_evalmod = self.lvl_evalmod - 2 * (depth + cfg.squarings) - 1
         self.lvl_stc = self.lvl_after_evalmod
         self.out_level = self.lvl_stc - cfg.groups
@@ -494,8 +501,68 @@ class Bootstrapper:
         lvl = min(ckks.level_of(x), ckks.level_of(y))
         return ckks.hmult_rescale(ckks.mod_drop(x, lvl), ckks.mod_drop(y, lvl), self.keys.relin, 2, addend=addend)
 
+    def _exp_ps(self, x, coef):
+        """sum_k coef[k] x^k, degree <= 15, Paterson-Stockmeyer with baby powers x, x^2, x^3 and
+        giant powers x^4, x^8, x^12:  p = q_0 + q_1 x^4 + q_2 x^8 + q_3 x^12,  q_j = sum_{i<4}
+        coef[4j+i] x^i.  Each q_j is ONE fused plaintext pass over (x, x^2, x^3) + one rescale; the
+        three products are tensor products summed before a single relinearisation.  Five limb pairs
+        deep (one more than the balanced tree), six key switches instead of nine to ten."""
+        from .engine import get_engine
+
+        eng = get_engine()
+        d = len(coef) - 1
+        if d > 15:
+            raise RnsError("Paterson-Stockmeyer evaluation here covers degree <= 15")
+        c = list(coef) + [0.0] * (16 - len(coef))
+        q = self.params.q_basis
+        dd = lambda lvl: float(q[lvl - 1].q) * float(q[lvl - 2].q)      # the two limbs a rescale at `lvl` drops
+        L0 = ckks.level_of(x)
+        x2 = self._mul(x, x)                           # L0 - 2
+        x3, x4 = eng.fork([lambda: self._mul(x2, x), lambda: self._mul(x2, x2)])      # L0 - 4
+        x8 = self._mul(x4, x4)                         # L0 - 6
+        x12 = self._mul(x8, x4)                        # L0 - 8
+        lq = L0 - 4                                    # level the baby polynomials are formed at
+        lt = L0 - 8                                    # level of the three products
+        out_level = lt - 2
+        s_f = self.eval_scale_at(out_level)
+        sigma = s_f * dd(lt)                           # scale of every tensor product
+        xs = [ckks.mod_drop(x, lq), ckks.mod_drop(x2, lq), x3]
+        giants = {1: ckks.mod_drop(x4, lt), 2: ckks.mod_drop(x8, lt), 3: x12}
+        slots = eng.row_slots(xs[0].a.basis)
+
+        def baby(j):
+            """q_j at level lq - 2 with the exact scale that makes q_j * x^(4j) land on sigma
+            (q_0: directly on s_f)."""
+            want = s_f if j == 0 else sigma / giants[j].scale
+            pre = want * dd(lq)                        # scale before the rescale
+            terms, pts = [], []
+            for i in (1, 2, 3):
+                ck = c[4 * j + i]
+                if ck == 0:
+                    continue
+                terms.append(ckks.ct_tensor(xs[i - 1]))
+                pts.append(self._const(ck, lq, pre / xs[i - 1].scale).poly.data)
+            if not terms:
+                raise RnsError("degenerate baby polynomial")
+            acc = eng.fused_terms(terms, pts, slots)
+            t = ckks.ct_from_tensor(acc, xs[0].a.basis, pre)
+            if c[4 * j] != 0:
+                t = ckks.add_plain(t, self._const(c[4 * j], lq, pre))
+            r = ckks.rescale(t, 2)
+            return ckks.Ciphertext(r.a, r.b, want)
+
+        top = max(j for j in range(4) if any(c[4 * j + i] != 0 for i in range(4)))
+        qs = eng.fork([(lambda j=j: baby(j)) for j in range(top + 1)])
+        pairs = [(ckks.mod_drop(qs[j], lt), giants[j]) for j in range(1, top + 1)]
+        prod = ckks.hmult_sum_rescale(pairs, self.keys.relin, 2)
+        prod = ckks.Ciphertext(prod.a, prod.b, s_f)
+        return ckks.add(prod, ckks.mod_drop(qs[0], out_level))
+
     def _exp_taylor(self, x, coef):
-        """sum_k coef[k] x^k by a balanced power tree (depth ceil(log2(degree+1)))."""
+        """sum_k coef[k] x^k by a balanced power tree (depth ceil(log2(degree+1))), or by
+        Paterson-Stockmeyer when the configuration asks for it."""
+        if self.cfg.scheme == "ps":
+            return self._exp_ps(x, coef)
         from .engine import get_engine
 
         eng = get_engine()

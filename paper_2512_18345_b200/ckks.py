@@ -459,6 +459,42 @@ def hmult_rescale(x: Ciphertext, y: Ciphertext, rlk: ks.SwitchingKey, k: int = 1
                       scale=x.scale * y.scale / math.prod(m.q for m in dropped))
 
 
+def hmult_sum_rescale(pairs, rlk: ks.SwitchingKey, k: int = 1) -> Ciphertext:
+    """rescale(relinearize(sum_i x_i * y_i), k) with ONE key switch for the whole sum (lazy
+    relinearisation): the tensor products (d0, d1, d2) of the pairs are added limb-wise before
+    the relinearisation.  All operands at one level, all products at one scale."""
+    from .engine import get_engine
+
+    eng = get_engine()
+    params = rlk.params
+    x0, y0 = pairs[0]
+    level, n, basis = level_of(x0), x0.a.n, x0.a.basis
+    scale = x0.scale * y0.scale
+    for x, y in pairs:
+        _same_level(x.a, x0.a)
+        _same_level(y.a, x0.a)
+        if not _close(x.scale * y.scale, scale):
+            raise RnsError(f"scale mismatch in hmult_sum_rescale: {x.scale * y.scale} vs {scale}")
+    if n % 4 or level <= k:
+        raise RnsError("hmult_sum_rescale needs n % 4 == 0 and more than k limbs")
+    if tuple(m.q for m in basis) != tuple(m.q for m in params.q_basis[:level]):
+        raise StructureError("ciphertext basis is not a prefix of the parameter q-basis")
+    slots3 = eng.row_slots(basis, repeat=3)
+    d = None
+    for x, y in pairs:
+        t = eng.tensor_halves(x.a.data, x.b.data, y.a.data, y.b.data, eng.row_slots(basis))
+        if d is None:
+            d = t
+        else:
+            eng.elementwise(d.view(3 * level, n), t.view(3 * level, n), slots3, 0, out=d.view(3 * level, n))
+    rest, dropped = basis[:level - k], basis[level - k:]
+    ks_plan = eng.ks_plan(n, basis, params.p_basis, params.alpha, params.l + params.alpha, params.l)
+    md_plan = eng.moddown_plan(n, rest, dropped + params.p_basis)
+    out = eng.ks_relin_rescale(ks_plan, md_plan, d, rlk.matrix(), level - k)
+    return Ciphertext(a=Polynomial(rest, out[0], EVALUATION), b=Polynomial(rest, out[1], EVALUATION),
+                      scale=scale / math.prod(m.q for m in dropped))
+
+
 def rescale(ct: Ciphertext, k: int = 1) -> Ciphertext:
     """Drop the last k limbs, dividing message and scale by their product P: one ModDown
     pass with P = the dropped limbs, (x_rest - NTT(BConv_{P -> rest}(INTT(x_P)))) * P^-1.
