@@ -226,6 +226,7 @@ int inner_product_launch(const InnerProductArgs& a, const ModSlot* slots, cudaSt
 // multiplies it into the NG running sums.  Traffic: every key and every plaintext diagonal
 // once, raised digits through L2; the 2 * nb accumulator limbs per row are never written.
 constexpr int kBsgsStages = 3;
+constexpr int kBsgsThreads = 128;
 
 // 8-byte asynchronous copy global -> shared.  No L2 cache hint: with the hint ptxas 12.9 put the
 // policy descriptor of the copies inside the loop into an odd uniform register pair
@@ -236,7 +237,7 @@ __device__ __forceinline__ void cp_async8(uint2* dst_smem, const uint32_t* src, 
 }
 
 template <int NG, int BETA>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(kBsgsThreads)
 bsgs_inner_kernel(BsgsInnerArgs p, const ModSlot* __restrict__ slots) {
     const int row = blockIdx.y;
     const ModSlot m = slots[p.ext_slot[row]];
@@ -261,7 +262,7 @@ bsgs_inner_kernel(BsgsInnerArgs p, const ModSlot* __restrict__ slots) {
     // use consecutive 8-byte slots (no bank conflicts).
     extern __shared__ uint2 s_pipe[];
     constexpr int ITEMS = 2 * BETA + NG;
-    auto slot = [&](int stage, int item) -> uint2* { return s_pipe + ((size_t)(stage * ITEMS + item) * 256 + threadIdx.x); };
+    auto slot = [&](int stage, int item) -> uint2* { return s_pipe + ((size_t)(stage * ITEMS + item) * kBsgsThreads + threadIdx.x); };
     auto request = [&](int b) {
         if (b < p.nb) {
             const int stage = b % kBsgsStages;
@@ -339,10 +340,10 @@ bsgs_inner_kernel(BsgsInnerArgs p, const ModSlot* __restrict__ slots) {
 
 template <int NG, int BETA>
 static int bsgs_launch_one(const BsgsInnerArgs& a, const ModSlot* slots, dim3 grid, cudaStream_t st) {
-    const size_t sm = sizeof(uint2) * 256 * (size_t)kBsgsStages * (2 * BETA + NG);
+    const size_t sm = sizeof(uint2) * kBsgsThreads * (size_t)kBsgsStages * (2 * BETA + NG);
     if (sm > 48 * 1024)
         CK(cudaFuncSetAttribute(bsgs_inner_kernel<NG, BETA>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    CK(launch_pdl(bsgs_inner_kernel<NG, BETA>, grid, dim3(256), sm, st, a, slots));
+    CK(launch_pdl(bsgs_inner_kernel<NG, BETA>, grid, dim3(kBsgsThreads), sm, st, a, slots));
     return CKKS_OK;
 }
 
@@ -368,7 +369,7 @@ int bsgs_inner_launch(const BsgsInnerArgs& a, const ModSlot* slots, cudaStream_t
     // keys + plaintexts + outputs (+ the ciphertext once); raised digits are re-read through L2
     const double limbs = (double)a.ext * (2.0 * a.beta * keyed + (double)a.nb * a.ng + 2.0 * a.ng) + 2.0 * a.l;
     ProfScope ps("bsgs_inner", st, 4.0 * a.n * limbs);
-    dim3 grid((unsigned)((a.n / 2 + 255) / 256), a.ext);
+    dim3 grid((unsigned)((a.n / 2 + kBsgsThreads - 1) / kBsgsThreads), a.ext);
     int rc = CKKS_ERR_UNSUPPORTED;
     switch (a.ng) {
         case 1: rc = bsgs_dispatch<1>(a, slots, grid, st); break;
