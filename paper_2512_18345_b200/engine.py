@@ -106,6 +106,44 @@ class Engine:
             main.wait_stream(self.lane_streams[lane])
         return out
 
+    def pipeline(self, items, first, second):
+        """Two-stage software pipeline over two lanes: `first(item)` runs on the caller's lane,
+        `second(item, first_result)` on the next lane of the caller's group as soon as that
+        item's first stage is done, so stage one of item i + 1 overlaps stage two of item i
+        (the reference models this co-scheduling of a cache-bound with a DRAM-bound kernel group
+        in costmodel.py:508-541; here the two groups really run on two streams).  Intermediates
+        stay referenced until the join, so no buffer is recycled under a reader on the other
+        stream.  Results of `second`, in order."""
+        torch = self.torch
+        outer = getattr(self, "_lane_group", None)
+        group = outer if outer is not None else list(range(getattr(self, "lanes", 1)))
+        if len(group) < 2:
+            return [second(item, first(item)) for item in items]
+        home, lane = group[0], group[1]
+        main = torch.cuda.current_stream(self.device)
+        side = self.lane_streams[lane]
+        side.wait_stream(main)
+        keep, out = [], []
+        try:
+            for item in items:
+                self._lane_group = [home]
+                _lib.check(self.lib.ckks_select_lane(self.ctx, home))
+                mid = first(item)
+                done = torch.cuda.Event()
+                done.record(main)
+                keep.append(mid)
+                self._lane_group = [lane]
+                _lib.check(self.lib.ckks_select_lane(self.ctx, lane))
+                side.wait_event(done)
+                with torch.cuda.stream(side):
+                    out.append(second(item, mid))
+        finally:
+            self._lane_group = outer
+            _lib.check(self.lib.ckks_select_lane(self.ctx, home))
+        main.wait_stream(side)
+        del keep
+        return out
+
     def lane_count(self) -> int:
         """Lanes the caller may fork over right now (all of them outside a fork)."""
         group = getattr(self, "_lane_group", None)

@@ -386,6 +386,29 @@ def keyswitch_batched(cts: list[Ciphertext], evk: SwitchingKey) -> list[Cipherte
     return out
 
 
+def keyswitch_pipelined(cts: list[Ciphertext], evk: SwitchingKey) -> list[Ciphertext]:
+    """Independent key switches under one key as a two-lane software pipeline: the ModUp of
+    ciphertext i + 1 (transforms and base conversion, cache- and integer-bound) runs while the
+    inner product of ciphertext i streams the key from HBM and its ModDown follows (the
+    complementary pipelining the reference models in costmodel.py:508-541, with the stage-2
+    split of keyswitch.py:358-366: the P half first, so the ModDown's inverse transform can start
+    under the Q half).  Every result equals keyswitch(ct, evk) limb for limb."""
+    from .engine import get_engine
+    from .rns import poly_elementwise
+
+    params = evk.params
+
+    def mod_up(ct):
+        return keyswitch_stage1(ct.a, params)
+
+    def rest(ct, raised):
+        p_part, q_part = keyswitch_stage2_split(raised, evk)
+        delta = keyswitch_stage3(q_part, p_part, params)
+        return Ciphertext(a=delta.a, b=poly_elementwise(delta.b, ct.b, "add"), scale=ct.scale)
+
+    return get_engine().pipeline(list(cts), mod_up, rest)
+
+
 def dump_pipeline_vectors(directory, ct: Ciphertext, evk: SwitchingKey) -> list[str]:
     """Write every stage's polynomials as RNSV files, names as the reference's."""
     from pathlib import Path

@@ -4,16 +4,27 @@ model: costmodel.py:320-332 keyswitch_footprint, :407-420 plan_batch; SURVEY 8f 
 `plan_batch` answers the reference's question -- how many independent key-switching sequences
 fit the L2 together -- with the reference's own footprint rule and B200's 126 MB L2, and
 `keyswitch.keyswitch_batched` uses the answer: that many key switches of the batch are in flight
-at once (one workspace lane and stream each), the rest follow in waves.  At ks48 one sequence
-already fills the cache (B* = 1 or 2): key switches run one after the other and each kernel has
-the L2 to itself; at ks12 (B* = 15 / 7) a wave of 7 shares it."""
+at once (one workspace lane and stream each), the rest follow in waves: B* = 2 at ks48, 5 at ks24,
+10 at ks12.  Measured against a plain loop and against the two-lane stage pipeline
+(`keyswitch.keyswitch_pipelined`) in profiles/r1s_ks_schedules.json."""
 from __future__ import annotations
 
+import json
 from dataclasses import dataclass
+from importlib import resources
 
 from .params import ParameterSet
 
 B200_L2_BYTES = 126 * (1 << 20)          # B300_MICROARCH guide: ~126 MB total over both dies
+
+
+def machine_profile(name: str = "b200") -> dict:
+    """Measured machine profile in the reference's schema (data/profiles/*.json, read by
+    costmodel.MachineModel.from_dict, costmodel.py:95-103): lets `rnscope plan / analyze` predict
+    this engine's kernels from B200's measured L2 / HBM / integer-pipe peaks.
+    The extra "measured" object says where each number comes from; the reference ignores it."""
+    text = resources.files(__package__).joinpath(f"data/profiles/{name}.json").read_text()
+    return json.loads(text)
 
 
 @dataclass(frozen=True)

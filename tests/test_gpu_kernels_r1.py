@@ -228,6 +228,30 @@ def test_keyswitch_batched_concurrent_lanes_equals_loop(env, golden):
         assert np.array_equal(g.a.coeffs, w.a.coeffs) and np.array_equal(g.b.coeffs, w.b.coeffs)
 
 
+def test_keyswitch_pipelined_equals_loop(env, golden):
+    """keyswitch_pipelined (ModUp of ciphertext i + 1 on one lane under the inner product and
+    ModDown of ciphertext i on another, stage-2 split) returns the limbs of keyswitch(); also with
+    a single lane, where it degenerates to the staged sequence."""
+    from paper_2512_18345_b200 import params
+
+    eng, ks = env.eng, env.ks
+    p = params.ParameterSet.from_dict(golden["params"]["ks12"])
+    s_from, s_to = ks.keygen(p, seed=1), ks.keygen(p, seed=2)
+    evk = ks.switching_keygen(s_from, s_to, p, seed=4)
+    rng = np.random.default_rng(6)
+    cts = [ks.encrypt(rng.integers(1, 9, p.n).astype(np.int64) * p.delta, s_from, p, seed=10 + i) for i in range(5)]
+    want = [ks.keyswitch(ct, evk) for ct in cts]
+    for lanes in (1, 2, 4):
+        eng.set_lanes(lanes)
+        try:
+            got = ks.keyswitch_pipelined(cts, evk)
+            env.torch.cuda.synchronize()
+        finally:
+            eng.set_lanes(1)
+        for g, w in zip(got, want):
+            assert np.array_equal(g.a.coeffs, w.a.coeffs) and np.array_equal(g.b.coeffs, w.b.coeffs)
+
+
 def test_batched_moddown_equals_separate_moddowns(env):
     """ckks_ks_stage3_batch over three accumulators (one set of launches, element g in the arena
     of lane g) against three ckks_ks_stage3 calls: equal limb for limb."""

@@ -192,3 +192,18 @@ def test_plan_batch_matches_reference_model(golden):
     import pytest
     with pytest.raises(ValueError):
         plan_batch(p48, "nope")
+
+
+def test_machine_profile_follows_the_reference_schema():
+    """data/profiles/b200.json carries every field the reference's MachineModel.from_dict reads
+    (costmodel.py:95-103) and satisfies its constructor checks (:73-79)."""
+    from paper_2512_18345_b200.scheduler import B200_L2_BYTES, machine_profile
+
+    prof = machine_profile()
+    for key in ("name", "l2_capacity", "l2_read_bw", "l2_write_bw", "dram_bw", "fma_tput", "alu_tput",
+                "launch_overhead", "saturation_limbs"):
+        assert prof[key] == prof[key] and (isinstance(prof[key], str) or prof[key] > 0)
+    assert prof["schema_version"] == 1
+    assert prof["l2_write_bw"] <= prof["l2_read_bw"]
+    assert prof["dram_bw"] < prof["l2_write_bw"]
+    assert int(prof["l2_capacity"]) == B200_L2_BYTES
