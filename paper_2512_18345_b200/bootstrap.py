@@ -529,6 +529,7 @@ class Bootstrapper:
         xs = [ckks.mod_drop(x, lq), ckks.mod_drop(x2, lq), x3]
         giants = {1: ckks.mod_drop(x4, lt), 2: ckks.mod_drop(x8, lt), 3: x12}
         slots = eng.row_slots(xs[0].a.basis)
+        xts = [ckks.ct_tensor(v) for v in xs]          # gathered once, read by every baby polynomial
 
         def baby(j):
             """q_j at level lq - 2 with the exact scale that makes q_j * x^(4j) land on sigma
@@ -540,7 +541,7 @@ class Bootstrapper:
                 ck = c[4 * j + i]
                 if ck == 0:
                     continue
-                terms.append(ckks.ct_tensor(xs[i - 1]))
+                terms.append(xts[i - 1])
                 pts.append(self._const(ck, lq, pre / xs[i - 1].scale).poly.data)
             if not terms:
                 raise RnsError("degenerate baby polynomial")
