@@ -42,6 +42,25 @@ def test_bootstrap_precision_and_level(boot_env):
     assert np.array_equal(again.a.coeffs, out.a.coeffs) and np.array_equal(again.b.coeffs, out.b.coeffs)
 
 
+@pytest.mark.parametrize("groups", [2, 4])
+def test_bootstrap_stage_groups_trade_levels_for_diagonals(boot_env, groups):
+    """BootstrapConfig.groups: more (fewer) stage groups per linear transform end three limbs lower
+    (higher) per group and refresh the same message to the same precision class."""
+    from paper_2512_18345_b200.bootstrap import BootstrapConfig, Bootstrapper
+
+    ckks, p, sk, base = boot_env
+    boot = Bootstrapper(p, sk, BootstrapConfig(groups=groups))
+    assert boot.out_level == base.out_level - 3 * (groups - 3)
+    assert len(boot.cts) == len(boot.stc) == groups
+    rng = np.random.default_rng(2)
+    z = rng.uniform(-1, 1, p.n // 2) + 1j * rng.uniform(-1, 1, p.n // 2)
+    ct = ckks.encrypt(ckks.encode(z, p, level=2, scale=boot.delta_in), sk, p, seed=6)
+    out = boot.bootstrap(ct)
+    assert ckks.level_of(out) == boot.out_level
+    err = np.abs(ckks.decrypt_decode(out, sk, p) - z).max()
+    assert err < 2.0 ** -19, f"bootstrap precision 2^{math.log2(err):.1f} with {groups} groups"
+
+
 def test_mod_raise_is_exact_centred_lift(boot_env):
     ckks, p, sk, boot = boot_env
     from paper_2512_18345_b200.transform import ntt_polynomial
