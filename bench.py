@@ -217,6 +217,9 @@ def helr_keyswitch_levels():
 def time_oracle(workload, steps, warmup):
     """(throughput, ms per unit, sample description) of the CPU port."""
     base = "keyswitch" if workload in ("bootstrap", "helr") else workload
+    from oracle import oracle as _oracle
+
+    _oracle.set_threads(host_threads())          # torchrun exports OMP_NUM_THREADS=1 to its ranks
     step = oracle_step(base)
     for _ in range(warmup):
         step()
@@ -269,10 +272,18 @@ def run_b200(args):
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # one rank per GPU; a box with fewer GPUs than ranks (only when the N > 1 path is rehearsed on a
+    # single-GPU machine) shares devices and rendezvous over gloo, and says so in the JSON line
+    oversubscribed = world > torch.cuda.device_count()
+    if oversubscribed:
+        local %= torch.cuda.device_count()
     torch.cuda.set_device(local)
     if world > 1:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if oversubscribed:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     from paper_2512_18345_b200 import ckks, keyswitch as ks, transform
     from paper_2512_18345_b200.engine import get_engine
@@ -540,6 +551,8 @@ def run_b200(args):
             line["paper_rtx5090_latency_ms"] = 15.2
         if precision_bits is not None:
             line["precision_log2_max_err"] = precision_bits
+        if oversubscribed:
+            line["oversubscribed"] = f"{world} ranks on {torch.cuda.device_count()} GPU(s): rehearsal of the N > 1 path, not a scaling number"
         print(json.dumps(line))
     if world > 1:
         dist.destroy_process_group()

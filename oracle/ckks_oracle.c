@@ -22,6 +22,19 @@
 
 typedef unsigned __int128 u128;
 
+/* Worker threads of the parallel loops below.  Launchers such as torchrun export
+ * OMP_NUM_THREADS=1 to every rank; the CPU baseline is meant to use every host thread it is
+ * given, so bench.py sets the count explicitly.  Returns the count in effect (1 without OpenMP). */
+#ifdef _OPENMP
+#include <omp.h>
+int orc_set_threads(int n) {
+    if (n > 0) omp_set_num_threads(n);
+    return omp_get_max_threads();
+}
+#else
+int orc_set_threads(int n) { (void)n; return 1; }
+#endif
+
 typedef struct {
     uint32_t q;
     uint32_t n_inv;
