@@ -862,6 +862,7 @@ int ckks_ks_hoisted(ckks_ctx* ctx, int32_t plan, const uint32_t* raised, uint32_
     uint32_t* acc_b = pl->ws_acc + (size_t)pl->ext * n;
     InnerProductArgs ip = ip_args(pl, nullptr, raised, evk, 0, pl->ext, acc_a, acc_b);
     ip.galois = k & (2 * pl->n - 1);
+    if (ip.galois == 1) ip.galois = 0;           // X -> X: the plain inner product, no gather
     CKS(inner_product_launch(ip, ctx->d_slots, st));
     return stage3_core(ctx, pl, acc_a, acc_b, acc_a + (size_t)pl->l * n, acc_b + (size_t)pl->l * n,
                        ct_b, out_a, out_b, st, ip.galois);

@@ -388,25 +388,30 @@ def keyswitch_batched(cts: list[Ciphertext], evk: SwitchingKey) -> list[Cipherte
 
 def keyswitch_pipelined(cts: list[Ciphertext], evk: SwitchingKey) -> list[Ciphertext]:
     """Independent key switches under one key as a two-lane software pipeline: the ModUp of
-    ciphertext i + 1 (transforms and base conversion, cache- and integer-bound) runs while the
-    inner product of ciphertext i streams the key from HBM and its ModDown follows (the
-    complementary pipelining the reference models in costmodel.py:508-541, with the stage-2
-    split of keyswitch.py:358-366: the P half first, so the ModDown's inverse transform can start
-    under the Q half).  Every result equals keyswitch(ct, evk) limb for limb."""
+    ciphertext i + 1 (transforms and base conversion, cache- and integer-bound) runs on one lane
+    while the inner product of ciphertext i streams the key from HBM and its ModDown follows on
+    the other -- the complementary pipelining the reference models in costmodel.py:508-541, built
+    from the same launches as the fused key switch.  Every result equals keyswitch(ct, evk) limb
+    for limb."""
     from .engine import get_engine
-    from .rns import poly_elementwise
 
     params = evk.params
+    eng = get_engine()
+    tabs = _tables(params)
+    plan, ext, key = tabs.plan(), len(tabs.ext_basis), evk.matrix()
+    for ct in cts:
+        if not _same_basis(ct.a, params.q_basis):
+            raise StructureError("stage 1 input basis must match the parameter q-basis")
 
     def mod_up(ct):
-        return keyswitch_stage1(ct.a, params)
+        return eng.ks_stage1(plan, ct.a.data, params.beta, ext)
 
     def rest(ct, raised):
-        p_part, q_part = keyswitch_stage2_split(raised, evk)
-        delta = keyswitch_stage3(q_part, p_part, params)
-        return Ciphertext(a=delta.a, b=poly_elementwise(delta.b, ct.b, "add"), scale=ct.scale)
+        out = eng.ks_hoisted(plan, raised, 1, key, ct.b.data)        # k = 1: no rotation
+        return Ciphertext(a=Polynomial(params.q_basis, out[0], EVALUATION),
+                          b=Polynomial(params.q_basis, out[1], EVALUATION), scale=ct.scale)
 
-    return get_engine().pipeline(list(cts), mod_up, rest)
+    return eng.pipeline(list(cts), mod_up, rest)
 
 
 def dump_pipeline_vectors(directory, ct: Ciphertext, evk: SwitchingKey) -> list[str]:
