@@ -333,7 +333,11 @@ typedef struct {
 static uint32_t mod_q(const orc_ctx *c, int idx) { return c->mod[idx].q; }
 
 /* keyswitch.py:256-315 keyswitch_stage1 / _raise_group with B = beta.
- * a: [l][n] evaluation domain. raised: [dnum][l+alpha][n]. */
+ * a: [l][n] evaluation domain. raised: [dnum][l+alpha][n].
+ * Generalised to levels that are not a multiple of alpha (the reference enforces
+ * L = dnum * alpha, params.py:40): digit t covers rows [t*alpha, min(l, (t+1)*alpha)), so
+ * the last digit may be partial; dnum = ceil(l / alpha).  At l = dnum * alpha this is the
+ * reference's routine verbatim (pinned at l in {12, 24, 36, 48}, tests/golden). */
 void orc_ks_stage1(const orc_ctx *c, int l, int alpha, int dnum, const int32_t *q_idx,
                    const int32_t *p_idx, const uint32_t *a, uint32_t *raised) {
     const uint32_t n = c->n;
@@ -342,25 +346,26 @@ void orc_ks_stage1(const orc_ctx *c, int l, int alpha, int dnum, const int32_t *
     uint32_t *coeff = (uint32_t *)malloc(sizeof(uint32_t) * (size_t)l * n);
     memcpy(coeff, a, sizeof(uint32_t) * (size_t)l * n);
     orc_ntt(c, coeff, q_idx, l, 1);
-    uint32_t *conv = (uint32_t *)malloc(sizeof(uint32_t) * (size_t)l * n);
+    uint32_t *conv = (uint32_t *)malloc(sizeof(uint32_t) * (size_t)ext * n);
     uint32_t *qs = (uint32_t *)malloc(sizeof(uint32_t) * (size_t)alpha);
-    uint32_t *ps = (uint32_t *)malloc(sizeof(uint32_t) * (size_t)l);
-    int32_t *target = (int32_t *)malloc(sizeof(int32_t) * (size_t)l);
+    uint32_t *ps = (uint32_t *)malloc(sizeof(uint32_t) * (size_t)ext);
+    int32_t *target = (int32_t *)malloc(sizeof(int32_t) * (size_t)ext);
     for (int t = 0; t < dnum; ++t) {
+        const int lo = t * alpha, hi = (lo + alpha < l) ? lo + alpha : l;
         /* :196-201 raise target = complementary Q limbs then P limbs */
         int cnt = 0;
         for (int i = 0; i < l; ++i)
-            if (i / alpha != t) target[cnt++] = q_idx[i];
+            if (i < lo || i >= hi) target[cnt++] = q_idx[i];
         for (int i = 0; i < alpha; ++i) target[cnt++] = p_idx[i];
-        for (int i = 0; i < alpha; ++i) qs[i] = mod_q(c, q_idx[t * alpha + i]);
+        for (int i = lo; i < hi; ++i) qs[i - lo] = mod_q(c, q_idx[i]);
         for (int i = 0; i < cnt; ++i) ps[i] = mod_q(c, target[i]);
-        orc_bconv(qs, alpha, ps, cnt, coeff + (size_t)t * alpha * n, conv, n);   /* :276 */
+        orc_bconv(qs, hi - lo, ps, cnt, coeff + (size_t)lo * n, conv, n);        /* :276 */
         orc_ntt(c, conv, target, cnt, 0);                                        /* :278 */
         /* :283-293 assemble: carried digit rows from the input, rest from conv */
         uint32_t *out = raised + (size_t)t * ext * n;
         int src = 0;
         for (int row = 0; row < ext; ++row) {
-            if (row < l && row / alpha == t)
+            if (row >= lo && row < hi)
                 memcpy(out + (size_t)row * n, a + (size_t)row * n, sizeof(uint32_t) * n);
             else
                 memcpy(out + (size_t)row * n, conv + (size_t)(src++) * n, sizeof(uint32_t) * n);
@@ -449,4 +454,149 @@ void orc_keyswitch(const orc_ctx *c, int l, int alpha, int dnum, const int32_t *
     orc_elementwise(c, out_b, ct_b, out_b, q_idx, l, 0);   /* :452 fold ct.b */
     if (!raised_out) free(raised);
     if (!acc_out) free(acc);
+}
+
+/* ---- extensions for circuits above the reference's entry points -------------------------
+ * The reference stops at keyswitch() (keyswitch.py:444-453); HRot, HMult + relinearise,
+ * rescale, hoisting and bootstrapping are compositions of its primitives.  The
+ * routines below restate the composed steps the CUDA engine fuses, each as plain loops over
+ * the same "(a op b) % q" arithmetic, so that whole circuits can be replayed on the CPU. */
+
+/* Register one more modulus after orc_create (tables as in orc_create).  Returns its index. */
+int orc_add_modulus(orc_ctx *c, uint64_t q, uint64_t psi, uint64_t mod_n) {
+    const uint32_t n = c->n;
+    c->mod = (orc_modulus *)realloc(c->mod, sizeof(orc_modulus) * (size_t)(c->n_mod + 1));
+    orc_modulus *m = &c->mod[c->n_mod];
+    m->q = (uint32_t)q;
+    m->fwd = (uint32_t *)calloc(n, sizeof(uint32_t));
+    m->inv = (uint32_t *)calloc(n, sizeof(uint32_t));
+    m->n_inv = 0;
+    if (n >= 2 && psi != 0 && (m->q - 1) % (2ull * n) == 0) {
+        uint32_t root = (uint32_t)psi;
+        uint64_t order = 2 * mod_n;
+        while (order > 2ull * n) { root = mulmod(root, root, m->q); order >>= 1; }
+        uint32_t root_inv = powmod(root, (uint64_t)m->q - 2, m->q);
+        uint32_t *pw = (uint32_t *)malloc(sizeof(uint32_t) * n);
+        uint32_t *pwi = (uint32_t *)malloc(sizeof(uint32_t) * n);
+        uint32_t acc = 1 % m->q, acci = 1 % m->q;
+        for (uint32_t k = 0; k < n; ++k) {
+            pw[k] = acc; pwi[k] = acci;
+            acc = mulmod(acc, root, m->q);
+            acci = mulmod(acci, root_inv, m->q);
+        }
+        for (uint32_t t = 0; t < n; ++t) {
+            uint32_t r = bitrev(t, c->lg);
+            m->fwd[t] = pw[r];
+            m->inv[t] = pwi[r];
+        }
+        free(pw); free(pwi);
+        m->n_inv = powmod(n % m->q, (uint64_t)m->q - 2, m->q);
+    }
+    return c->n_mod++;
+}
+
+/* transform.py:203-250 _run_stages on an explicit stage range (ntt_two_phase's halves). */
+void orc_ntt_stages(const orc_ctx *c, uint32_t *data, const int32_t *row_mod, int rows,
+                    int inverse, uint32_t s_lo, uint32_t s_hi) {
+#pragma omp parallel for schedule(dynamic, 1)
+    for (int r = 0; r < rows; ++r)
+        run_stages(data + (size_t)r * c->n, &c->mod[row_mod[r]], c->n, c->lg, inverse, s_lo, s_hi);
+}
+
+/* keyswitch.py:318-332 _stage2_accumulate, generalised the way the engine uses it:
+ *  - the ciphertext may live at l <= L limbs while the key is the full-level one: active
+ *    extended-basis row r reads key row evk_row[r] of a key with evk_ext rows per polynomial;
+ *  - perm != NULL: the digits are read through the evaluation-domain automorphism
+ *    (rns.py:313-320 out[:, t] = in[:, perm[t]]): hoisted rotation;
+ *  - lift_a / lift_b != NULL: (P mod q_i) * lift is added on the Q rows (lift_b through perm),
+ *    i.e. a polynomial that takes no key switch joins the Q||P accumulator;
+ *  - accumulate: add into acc instead of overwriting it.
+ * raised: [beta][ext][n]; evk: [beta_total][2][evk_ext][n]; acc_a, acc_b: [ext][n]. */
+void orc_inner_product(const orc_ctx *c, int l, int beta, int ext, const int32_t *ext_idx,
+                       const uint32_t *raised, const uint32_t *evk, int evk_ext,
+                       const int32_t *evk_row, const int32_t *perm, const uint32_t *lift_a,
+                       const uint32_t *lift_b, const uint32_t *pmod, int accumulate,
+                       uint32_t *acc_a, uint32_t *acc_b) {
+    const uint32_t n = c->n;
+#pragma omp parallel for schedule(static)
+    for (int row = 0; row < ext; ++row) {
+        const uint64_t q = mod_q(c, ext_idx[row]);
+        const size_t er = (size_t)evk_row[row];
+        uint32_t *oa = acc_a + (size_t)row * n, *ob = acc_b + (size_t)row * n;
+        for (uint32_t j = 0; j < n; ++j) {
+            const uint32_t src = perm ? (uint32_t)perm[j] : j;
+            uint64_t sa = 0, sb = 0;
+            for (int t = 0; t < beta; ++t) {
+                uint64_t d = raised[((size_t)t * ext + row) * n + src];
+                uint64_t ka = evk[(((size_t)t * 2 + 0) * evk_ext + er) * n + j];
+                uint64_t kb = evk[(((size_t)t * 2 + 1) * evk_ext + er) * n + j];
+                sa = (sa + d * ka % q) % q;
+                sb = (sb + d * kb % q) % q;
+            }
+            if (row < l && lift_a) sa = (sa + (uint64_t)lift_a[(size_t)row * n + j] * pmod[row] % q) % q;
+            if (row < l && lift_b) sb = (sb + (uint64_t)lift_b[(size_t)row * n + src] * pmod[row] % q) % q;
+            if (accumulate) { sa = (sa + oa[j]) % q; sb = (sb + ob[j]) % q; }
+            oa[j] = (uint32_t)sa;
+            ob[j] = (uint32_t)sb;
+        }
+    }
+}
+
+/* acc (+)= x (.) p on both halves of a ciphertext: x, acc [2][rows][n], p [rows][n]
+ * (chains of rns.py:243-258 poly_elementwise mul / add). */
+void orc_pmult_acc(const orc_ctx *c, const uint32_t *x, const uint32_t *p, uint32_t *acc,
+                   const int32_t *row_mod, int rows, int first) {
+    const uint32_t n = c->n;
+#pragma omp parallel for schedule(static)
+    for (int r = 0; r < 2 * rows; ++r) {
+        const int row = r % rows;
+        const uint64_t q = mod_q(c, row_mod[row]);
+        const uint32_t *xs = x + (size_t)r * n, *ps = p + (size_t)row * n;
+        uint32_t *o = acc + (size_t)r * n;
+        for (uint32_t j = 0; j < n; ++j) {
+            uint64_t v = (uint64_t)xs[j] * ps[j] % q;
+            if (!first) v = (v + o[j]) % q;
+            o[j] = (uint32_t)v;
+        }
+    }
+}
+
+/* ModRaise: the value v in (-q0 q1 / 2, q0 q1 / 2] with v = in[0] mod q0 = in[1] mod q1
+ * (Garner lift of two coefficient-domain limbs, centred), reduced modulo every target row. */
+void orc_lift2_centered(const orc_ctx *c, const uint32_t *in, int mod0, int mod1, uint32_t *out,
+                        const int32_t *row_mod, int rows) {
+    const uint32_t n = c->n;
+    const uint64_t q0 = mod_q(c, mod0), q1 = mod_q(c, mod1);
+    const uint64_t q0_inv = powmod((uint32_t)(q0 % q1), q1 - 2, (uint32_t)q1);
+    const u128 big = (u128)q0 * q1;
+#pragma omp parallel for schedule(static)
+    for (uint32_t j = 0; j < n; ++j) {
+        const uint64_t r0 = in[j], r1 = in[(size_t)n + j];
+        const uint64_t d = (r1 + q1 - r0 % q1) % q1;
+        const u128 v = (u128)r0 + (u128)q0 * (d * q0_inv % q1);
+        const int neg = v > big / 2;
+        const u128 mag = neg ? big - v : v;
+        for (int i = 0; i < rows; ++i) {
+            const uint64_t q = mod_q(c, row_mod[i]);
+            uint64_t r = (uint64_t)(mag % q);
+            if (neg && r) r = q - r;
+            out[(size_t)i * n + j] = (uint32_t)r;
+        }
+    }
+}
+
+/* out = in + (P mod q_i) * lift on rows < l (rows >= l copied): a polynomial over Q joins a
+ * Q||P accumulator.  in may alias out. */
+void orc_add_lifted(const orc_ctx *c, const uint32_t *in, const uint32_t *lift,
+                    const uint32_t *pmod, const int32_t *ext_idx, int l, int ext, uint32_t *out) {
+    const uint32_t n = c->n;
+#pragma omp parallel for schedule(static)
+    for (int row = 0; row < ext; ++row) {
+        const uint64_t q = mod_q(c, ext_idx[row]);
+        for (uint32_t j = 0; j < n; ++j) {
+            uint64_t v = in[(size_t)row * n + j];
+            if (row < l) v = (v + (uint64_t)lift[(size_t)row * n + j] * pmod[row] % q) % q;
+            out[(size_t)row * n + j] = (uint32_t)v;
+        }
+    }
 }

@@ -469,3 +469,18 @@ def get_engine() -> Engine:
     if _engine is None:
         _engine = Engine()
     return _engine
+
+
+def use_backend(backend):
+    """Install `backend` as the object get_engine() returns and hand back the previous one
+    (None: the CUDA engine is created again on next use).
+
+    Checker hook, never called by the package itself: tests/ and the CPU reference arm of
+    bench.py pass an object with Engine's methods that is backed by the CPU oracle
+    (oracle/engine_oracle.py) to replay the host orchestration of a circuit -- same circuit,
+    reference primitives -- and compare limbs with the CUDA path.  There is no automatic
+    selection: without this explicit call every device operation needs the CUDA library and a
+    GPU and fails loudly otherwise."""
+    global _engine
+    previous, _engine = _engine, backend
+    return previous

@@ -298,7 +298,12 @@ def _as_word_tensor(t):
     if t.dtype != torch.int32:
         raise StructureError(f"device limb matrix must hold 32-bit words, got {t.dtype}")
     if not t.is_cuda:
-        raise StructureError("device limb matrix must live on a CUDA device")
+        from . import engine
+
+        # CPU word tensors are adopted only while a checker backend that works on host tensors
+        # is installed (engine.use_backend); the CUDA engine takes device tensors only
+        if not getattr(engine._engine, "host_tensors", False):
+            raise StructureError("device limb matrix must live on a CUDA device")
     return t if t.is_contiguous() else t.contiguous()
 
 

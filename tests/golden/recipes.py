@@ -58,3 +58,22 @@ KS_CASES = {
 }
 
 AUTOMORPHISM_KS = (3, 5, 25, -1)
+
+
+# ---- level-l key switching on the ks48 moduli (tests/golden/make_golden_level.py) -------------
+# A ciphertext at level l lives over the first l limbs of ks48's Q basis and is switched with
+# the rows of a FULL-level key that belong to active limbs.  The reference enforces
+# L = dnum * alpha (params.py:40), so l in LEVEL_FULL_DIGITS is pinned by its own keyswitch() on
+# a ParameterSet cut to those limbs; other levels (partial last digit), hoisted rotations and the
+# ModDown merged with a rescale are pinned by compositions of its public primitives.
+LEVEL_FULL_DIGITS = (12, 24, 36, 48)
+LEVEL_PARTIAL = (42, 21)
+LEVEL_EVK_SEED = 100          # key polynomial (digit t, half h): rand_rows(ext48, n, 100 + 2 t + h)
+LEVEL_CT_SEEDS = (200, 201)   # ciphertext halves (a, b) over the first l limbs
+HOIST_CASES = ((24, 5), (42, 25), (21, -1))          # (level, automorphism index k)
+MERGED_MODDOWN_CASES = ((48, 2), (30, 2), (19, 1))   # (level l, dropped limbs k): Q_{l-k} <- Q_l || P
+MERGED_SEEDS = (300, 301)     # the two [l + alpha] accumulator halves
+
+
+def level_key_rows(ext_qs, n: int, t: int, h: int) -> np.ndarray:
+    return rand_rows(ext_qs, n, LEVEL_EVK_SEED + 2 * t + h)
