@@ -70,6 +70,15 @@ void ckks_ctx_destroy(ckks_ctx* ctx);
 int ckks_set_lanes(ckks_ctx* ctx, int lanes);
 int ckks_select_lane(ckks_ctx* ctx, int lane);
 
+/* The arena is reallocated (it MOVES) when the lane count changes or a plan needs more words
+ * than any plan before it.  A CUDA graph captured earlier holds raw pointers into the old
+ * arena: ckks_arena_generation returns a counter that changes with every reallocation, so a
+ * holder of such a graph can refuse to replay it (Bootstrapper.capture does);
+ * ckks_arena_reserve grows the arena to `words_per_lane` up front (e.g. the full-level plan's
+ * size) so that later plans never move it. */
+int ckks_arena_generation(ckks_ctx* ctx, uint64_t* generation);
+int ckks_arena_reserve(ckks_ctx* ctx, size_t words_per_lane);
+
 /* Register modulus q for ring degree n with psi a primitive 2n-th root of
  * unity mod q (already squared down to order 2n, transform.py:88-96) and build
  * its device twiddle tables: fwd[t] = psi^bitrev(t), inv[t] = psi^-bitrev(t),

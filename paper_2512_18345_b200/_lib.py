@@ -17,7 +17,7 @@ ABI_VERSION = 1
 
 # every symbol include/ckks_b200.h declares (checked by tests/test_abi.py)
 SYMBOLS = (
-    "ckks_abi_version", "ckks_last_error", "ckks_profile_enable", "ckks_profile_read", "ckks_ctx_create", "ckks_ctx_destroy", "ckks_set_lanes", "ckks_select_lane",
+    "ckks_abi_version", "ckks_last_error", "ckks_profile_enable", "ckks_profile_read", "ckks_ctx_create", "ckks_ctx_destroy", "ckks_set_lanes", "ckks_select_lane", "ckks_arena_generation", "ckks_arena_reserve",
     "ckks_modulus_register", "ckks_modulus_tables", "ckks_ntt", "ckks_ntt_stages",
     "ckks_elementwise", "ckks_automorphism_eval", "ckks_automorphism_coeff", "ckks_lift2_centered", "ckks_pmult_accumulate", "ckks_fused_terms", "ckks_fused_terms_multi", "ckks_tensor", "ckks_tensor_halves",
     "ckks_bconv_table_create", "ckks_bconv_table_read", "ckks_bconv",
@@ -65,6 +65,8 @@ def load() -> ctypes.CDLL:
     L.ckks_ctx_destroy.restype = None
     L.ckks_set_lanes.argtypes = [vp, ctypes.c_int]
     L.ckks_select_lane.argtypes = [vp, ctypes.c_int]
+    L.ckks_arena_generation.argtypes = [vp, ctypes.POINTER(ctypes.c_uint64)]
+    L.ckks_arena_reserve.argtypes = [vp, sz]
     L.ckks_modulus_register.argtypes = [vp, u32, u32, u32, pi32]
     L.ckks_modulus_tables.argtypes = [vp, i32, vp, vp, pu32]
     L.ckks_ntt.argtypes = [vp, vp, vp, vp, ctypes.c_int, u32, ctypes.c_int, vp]

@@ -656,8 +656,13 @@ class Bootstrapper:
                 static_out = torch.stack([out.a.data, out.b.data])
         torch.cuda.current_stream().wait_stream(side)
         out_basis, out_scale = out.a.basis, out.scale
+        generation = eng.arena_generation()
 
         def replay(ct, copy_out: bool = True):
+            if eng.arena_generation() != generation:
+                # the graph holds raw pointers into the key-switch workspace arena as it was
+                raise RnsError("the workspace arena was reallocated after this graph was captured (lane count "
+                               "changed or a larger key-switch plan was created): capture again")
             static_in[0].copy_(ct.a.data)
             static_in[1].copy_(ct.b.data)
             graph.replay()
@@ -665,9 +670,13 @@ class Bootstrapper:
             return ct_from_tensor(res, out_basis, out_scale)
 
         replay.graph, replay.static_in, replay.static_out = graph, static_in, static_out
+        replay.valid = lambda: eng.arena_generation() == generation
         return replay
 
-    def bootstrap(self, ct):
+    def bootstrap(self, ct, trace=None):
+        """`trace(name, ciphertext)`, when given, is called after every phase (eager runs only:
+        it reads limbs back, so never under graph capture)."""
+        note = trace if trace is not None else (lambda name, c: None)
         if not ckks._close(ct.scale, self.delta_in):
             raise RnsError(f"bootstrap expects scale 2^{self.cfg.log_delta_in}, got {ct.scale}")
         if self.to_sparse is not None:
@@ -676,7 +685,10 @@ class Bootstrapper:
         if self.to_dense is not None:
             back = ckks.keyswitch_level(ckks.Ciphertext(raised.a, raised.b, raised.scale), self.to_dense)
             raised = ckks.Ciphertext(a=back.a, b=back.b, scale=raised.scale)
+        note("mod_raise", raised)
         lo, hi = self.coeff_to_slot(raised)
+        note("coeff_to_slot_lo", lo)
+        note("coeff_to_slot_hi", hi)
         # (Q0 / (2*pi*Delta)) * sin(theta) = kappa * (E - conj E),  kappa = Q0 / (4*pi*i*Delta)
         kappa = self.q0 / (4.0 * math.pi * self.delta_in) / 1j
         from .engine import get_engine
@@ -685,5 +697,28 @@ class Bootstrapper:
                                         lambda: self.eval_mod(hi, self.coef_hi, kappa * 1j)])
         w = ckks.add(m_lo, m_hi)                       # m_lo + i*m_hi (bit-reversed slots)
         w = ckks.mod_drop(w, self.lvl_stc)
+        note("eval_mod", w)
         out = self.slot_to_coeff(w)
-        return ckks.Ciphertext(out.a, out.b, self.out_scale)
+        out = ckks.Ciphertext(out.a, out.b, self.out_scale)
+        note("slot_to_coeff", out)
+        return out
+
+
+def standard_setup(params: ParameterSet, config: BootstrapConfig | None = None, h_dense: int | None = None,
+                   seed: int = 1):
+    """The key regime of the paper's bootstrapping table: a dense application
+    key of Hamming weight h_dense that every evaluation key is generated for, and a sparse key
+    of weight h_sparse used only around ModRaise (sparse-secret encapsulation).  Returns
+    (sk, sk_sparse, Bootstrapper); bench.py, the tests and the oracle replay all build the
+    headline workload through this one function."""
+    sk = ks.keygen(params, h=params.h_dense if h_dense is None else h_dense, seed=seed)
+    sk_sparse = ks.keygen(params, h=params.h_sparse, seed=seed + 1000)
+    return sk, sk_sparse, Bootstrapper(params, sk, config or BootstrapConfig(), sk_sparse=sk_sparse)
+
+
+def standard_input(params: ParameterSet, boot: "Bootstrapper", sk, index: int = 0):
+    """Synthetic input `index` of the headline workload: uniform slots in the unit square,
+    encoded on two limbs at the bootstrap's input scale.  Returns (slots, ciphertext)."""
+    rng = np.random.default_rng(index)
+    z = rng.uniform(-1, 1, params.n // 2) + 1j * rng.uniform(-1, 1, params.n // 2)
+    return z, ckks.encrypt(ckks.encode(z, params, level=2, scale=boot.delta_in), sk, params, seed=50 + index)

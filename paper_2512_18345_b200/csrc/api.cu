@@ -173,6 +173,10 @@ struct ckks_ctx {
     // larger plan is created must be re-captured.
     uint32_t* ws = nullptr;
     size_t ws_words = 0;          // words per lane
+    // Bumped whenever the arena is (re)allocated.  Anything that recorded raw pointers into it
+    // (a captured CUDA graph) remembers the generation and must not be replayed after a change:
+    // ckks_arena_generation lets callers check (Bootstrapper.capture / replay do).
+    uint64_t ws_generation = 0;
     // Lanes: independent copies of the arena so that key switches issued on different
     // streams (independent rotations, the two EvalMod branches) can overlap.
     int lanes = 1;
@@ -239,7 +243,28 @@ int ckks_set_lanes(ckks_ctx* ctx, int lanes) {
         ctx->ws = nullptr;
         ctx->lanes = lanes;
         ctx->lane = 0;
+        ctx->ws_generation++;
         if (ctx->ws_words) CK(cudaMalloc((void**)&ctx->ws, sizeof(uint32_t) * ctx->ws_words * lanes));
+    }
+    return CKKS_OK;
+}
+
+int ckks_arena_generation(ckks_ctx* ctx, uint64_t* generation) {
+    if (!ctx || !generation) { set_last_error("null argument"); return CKKS_ERR_ARG; }
+    *generation = ctx->ws_generation;
+    return CKKS_OK;
+}
+
+int ckks_arena_reserve(ckks_ctx* ctx, size_t words_per_lane) {
+    CKS(check_ctx(ctx));
+    if (words_per_lane > ctx->ws_words) {
+        CK(cudaDeviceSynchronize());
+        if (ctx->ws) CK(cudaFree(ctx->ws));
+        ctx->ws = nullptr;
+        ctx->ws_words = 0;
+        ctx->ws_generation++;
+        CK(cudaMalloc((void**)&ctx->ws, sizeof(uint32_t) * words_per_lane * ctx->lanes));
+        ctx->ws_words = words_per_lane;
     }
     return CKKS_OK;
 }
@@ -264,8 +289,10 @@ int ckks_ctx_create(int device, ckks_ctx** out) {
     CK(cudaSetDevice(device));
     cudaDeviceProp prop;
     CK(cudaGetDeviceProperties(&prop, device));
-    if (prop.major < 10) {
-        set_last_error("device %d is sm_%d%d; libckks_b200 is built for sm_100a only", device,
+    if (prop.major != 10 || prop.minor != 0) {
+        // the library holds sm_100a SASS only (no PTX, no other cubin): fail here, not at the
+        // first launch with "no kernel image"
+        set_last_error("device %d is sm_%d%d; libckks_b200 is built for sm_100a (B200) only", device,
                        prop.major, prop.minor);
         return CKKS_ERR_UNSUPPORTED;
     }
@@ -671,6 +698,7 @@ static int plan_create(ckks_ctx* ctx, uint32_t n, int l, int alpha, const int32_
             if (ctx->ws) CK(cudaFree(ctx->ws));
             ctx->ws = nullptr;
             ctx->ws_words = 0;
+            ctx->ws_generation++;
             CK(cudaMalloc((void**)&ctx->ws, sizeof(uint32_t) * at * ctx->lanes));
             ctx->ws_words = at;
         }
@@ -793,7 +821,7 @@ static InnerProductArgs ip_args(KsPlan* pl, const uint32_t* carry, const uint32_
     a.ext_slot = pl->d_ext_slot; a.evk_row = pl->d_evk_row;
     a.l = pl->l; a.alpha = pl->alpha; a.beta = pl->beta; a.ext = pl->ext; a.evk_ext = pl->evk_ext;
     a.row_lo = row_lo; a.row_hi = row_hi; a.n = pl->n;
-    a.galois = 0; a.lg = log2u(pl->n); a.accumulate = 0;
+    a.galois = 0; a.lg = log2u(pl->n); a.accumulate = 0; a.ordered = 0;
     a.lift_a = nullptr; a.lift_b = nullptr; a.pmod = nullptr; a.pmod_s = nullptr;
     return a;
 }
@@ -821,8 +849,9 @@ int ckks_ks_stage2(ckks_ctx* ctx, int32_t plan, const uint32_t* raised, const ui
     CKS(get_plan(ctx, plan, &pl));
     CKS(need_full_plan(pl));
     if (row_lo < 0 || row_hi > pl->ext || row_lo > row_hi) { set_last_error("bad row range [%d, %d)", row_lo, row_hi); return CKKS_ERR_ARG; }
-    return inner_product_launch(ip_args(pl, nullptr, raised, evk, row_lo, row_hi, acc_a, acc_b),
-                                ctx->d_slots, (cudaStream_t)stream);
+    InnerProductArgs ip = ip_args(pl, nullptr, raised, evk, row_lo, row_hi, acc_a, acc_b);
+    ip.ordered = 1;           // first kernel of the call: its predecessor may have written the key
+    return inner_product_launch(ip, ctx->d_slots, (cudaStream_t)stream);
 }
 
 int ckks_ks_stage3(ckks_ctx* ctx, int32_t plan, const uint32_t* q_a, const uint32_t* q_b,
@@ -863,6 +892,7 @@ int ckks_ks_hoisted(ckks_ctx* ctx, int32_t plan, const uint32_t* raised, uint32_
     InnerProductArgs ip = ip_args(pl, nullptr, raised, evk, 0, pl->ext, acc_a, acc_b);
     ip.galois = k & (2 * pl->n - 1);
     if (ip.galois == 1) ip.galois = 0;           // X -> X: the plain inner product, no gather
+    ip.ordered = 1;
     CKS(inner_product_launch(ip, ctx->d_slots, st));
     return stage3_core(ctx, pl, acc_a, acc_b, acc_a + (size_t)pl->l * n, acc_b + (size_t)pl->l * n,
                        ct_b, out_a, out_b, st, ip.galois);
@@ -880,6 +910,7 @@ int ckks_ks_hoisted_raw(ckks_ctx* ctx, int32_t plan, const uint32_t* raised, uin
     ip.lift_b = ct_b;
     ip.pmod = pl->d_pmod;
     ip.pmod_s = pl->d_pmod_s;
+    ip.ordered = 1;
     return inner_product_launch(ip, ctx->d_slots, (cudaStream_t)stream);
 }
 

@@ -58,8 +58,8 @@ int elementwise_launch(const uint32_t* a, const uint32_t* b, uint32_t* out, cons
     ProfScope ps("elementwise", st, 12.0 * rows * cols);
 #define EW_DISPATCH(K)                                                                             \
     if (vec)                                                                                       \
-        launch_pdl(elementwise_vec4<K>, grid, dim3(256), 0, st, (const uint4*)a, (const uint4*)b,   \
-                   (uint4*)out, row_slot, slots, work);                                            \
+        CK(launch_pdl(elementwise_vec4<K>, grid, dim3(256), 0, st, (const uint4*)a, (const uint4*)b, \
+                      (uint4*)out, row_slot, slots, work));                                        \
     else                                                                                           \
         elementwise_scalar<K><<<grid, 256, 0, st>>>(a, b, out, row_slot, slots, work);
     if (kind == 0) { EW_DISPATCH(0) }

@@ -32,8 +32,10 @@ void set_last_error(const char* fmt, ...);
 // graphs this becomes a programmatic dependency edge.  CKKS_PDL=0 falls back to ordinary
 // launches (the kernels' pdl_* calls are then no-ops).
 bool pdl_enabled();
+// `pdl` false: an ordinary, fully stream-ordered launch (for a kernel that reads, before its
+// pdl_wait(), memory its stream predecessor may have written -- see InnerProductArgs::ordered).
 template <class... P, class... A>
-inline cudaError_t launch_pdl(void (*kernel)(P...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, A&&... args) {
+inline cudaError_t launch_opt_pdl(bool pdl, void (*kernel)(P...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, A&&... args) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = grid;
     cfg.blockDim = block;
@@ -43,8 +45,12 @@ inline cudaError_t launch_pdl(void (*kernel)(P...), dim3 grid, dim3 block, size_
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    cfg.numAttrs = (pdl && pdl_enabled()) ? 1 : 0;
     return cudaLaunchKernelEx(&cfg, kernel, P(args)...);
+}
+template <class... P, class... A>
+inline cudaError_t launch_pdl(void (*kernel)(P...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, A&&... args) {
+    return launch_opt_pdl(true, kernel, grid, block, smem, st, static_cast<A&&>(args)...);
 }
 
 // Logical row r of a launch lives at physical row in[r] of the source buffer
@@ -170,6 +176,12 @@ struct InnerProductArgs {
     uint32_t n;
     uint32_t galois, lg;        // galois != 0: read digit columns through X -> X^galois (hoisting)
     int accumulate;             // add into acc instead of overwriting it
+    // The kernel issues its switching-key loads BEFORE griddepcontrol.wait (the key is static
+    // inside a pipeline whose earlier kernels are ModUp stages).  When the inner product is the
+    // FIRST kernel of an ABI call its stream predecessor is unknown -- it may be the kernel that
+    // wrote the key (key generation, the stacking copy of SwitchingKey.matrix()) -- so those entry
+    // points set `ordered` and the kernel is launched without the programmatic attribute.
+    int ordered;
     // tensor mode (all four non-null): the operands of an HMult; the kernel forms d2 = xa*ya (the
     // carried digit rows), d1 = xa*yb + ya*xb and d0 = xb*yb itself and lifts P*d1, P*d0 into
     // the accumulators, so no tensor pass and no (d0, d1, d2) buffers exist.  carry, lift_a and

@@ -193,12 +193,13 @@ inner_product_kernel(InnerProductArgs p, const ModSlot* __restrict__ slots) {
 }
 
 template <int BETA>
-static void inner_product_dispatch(const InnerProductArgs& a, const ModSlot* slots, dim3 grid, bool vec, cudaStream_t st) {
+static cudaError_t inner_product_dispatch(const InnerProductArgs& a, const ModSlot* slots, dim3 grid, bool vec, cudaStream_t st) {
     const bool tens = a.tx_a != nullptr;
-    if (vec && tens) launch_pdl(inner_product_kernel<true, BETA, true>, grid, dim3(256), 0, st, a, slots);
-    else if (vec) launch_pdl(inner_product_kernel<true, BETA, false>, grid, dim3(256), 0, st, a, slots);
-    else if (tens) launch_pdl(inner_product_kernel<false, BETA, true>, grid, dim3(256), 0, st, a, slots);
-    else launch_pdl(inner_product_kernel<false, BETA, false>, grid, dim3(256), 0, st, a, slots);
+    const bool pdl = !a.ordered;
+    if (vec && tens) return launch_opt_pdl(pdl, inner_product_kernel<true, BETA, true>, grid, dim3(256), 0, st, a, slots);
+    if (vec) return launch_opt_pdl(pdl, inner_product_kernel<true, BETA, false>, grid, dim3(256), 0, st, a, slots);
+    if (tens) return launch_opt_pdl(pdl, inner_product_kernel<false, BETA, true>, grid, dim3(256), 0, st, a, slots);
+    return launch_opt_pdl(pdl, inner_product_kernel<false, BETA, false>, grid, dim3(256), 0, st, a, slots);
 }
 
 int inner_product_launch(const InnerProductArgs& a, const ModSlot* slots, cudaStream_t st) {
@@ -209,11 +210,11 @@ int inner_product_launch(const InnerProductArgs& a, const ModSlot* slots, cudaSt
     dim3 grid((unsigned)((work + 255) / 256), rows);
     ProfScope ps("inner_product", st, 4.0 * a.n * rows * (3.0 * a.beta + 2.0));
     switch (a.beta) {
-        case 1: inner_product_dispatch<1>(a, slots, grid, vec, st); break;
-        case 2: inner_product_dispatch<2>(a, slots, grid, vec, st); break;
-        case 3: inner_product_dispatch<3>(a, slots, grid, vec, st); break;
-        case 4: inner_product_dispatch<4>(a, slots, grid, vec, st); break;
-        default: inner_product_dispatch<0>(a, slots, grid, vec, st); break;
+        case 1: CK(inner_product_dispatch<1>(a, slots, grid, vec, st)); break;
+        case 2: CK(inner_product_dispatch<2>(a, slots, grid, vec, st)); break;
+        case 3: CK(inner_product_dispatch<3>(a, slots, grid, vec, st)); break;
+        case 4: CK(inner_product_dispatch<4>(a, slots, grid, vec, st)); break;
+        default: CK(inner_product_dispatch<0>(a, slots, grid, vec, st)); break;
     }
     CK(cudaGetLastError());
     return CKKS_OK;

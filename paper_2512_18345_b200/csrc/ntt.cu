@@ -411,7 +411,8 @@ static int launch_generic(const uint32_t* in, uint32_t* out, const int32_t* row_
         const size_t off_in = rm.in ? 0 : (size_t)r0 * n, off_out = rm.out ? 0 : (size_t)r0 * n;
         for (uint32_t s = s_lo; s < s_hi; ++s) {
             const bool first = s == s_lo;
-            ProfScope ps("ntt_generic_stage", st, 8.0 * cnt * n);
+            // one radix-2 stage per launch: the transform's 2 * R * N * 4 bytes spread over its stages
+            ProfScope ps("ntt_generic_stage", st, 8.0 * cnt * n / (double)(s_hi - s_lo));
             ntt_stage_generic<<<grid, threads, 0, st>>>(first ? in + off_in : out + off_out,
                                                         out + off_out, row_slot + r0, slots,
                                                         first ? rm_first : rm_rest, n, lg, s, inverse);
@@ -441,21 +442,24 @@ int ntt_launch(const uint32_t* in, uint32_t* out, const int32_t* row_slot, const
         dim3 g_str(256 / COLS, rows), g_con(16, rows);
         const RowMap rm2{rm.out, rm.out};
         if (!inverse) {
-            { ProfScope ps("ntt16_fwd_strided", st, 8.0 * rows * kN16);
+            // algorithmic bytes: 2 * R * N * 4 per TRANSFORM; the first kernel of the pair is
+            // charged the transform's read, the second its write (what passes between them is the
+            // implementation's own traffic)
+            { ProfScope ps("ntt16_fwd_strided", st, 4.0 * rows * kN16);
               CK(launch_pdl(ntt16_fwd_strided<COLS>, g_str, dim3(16 * COLS), 0, st, in, out, row_slot, slots, rm)); }
             if (epi) {
-                // reads conv + x_Q (+ fold), writes the result: (3 or 4) limbs per row
-                ProfScope ps("ntt16_fwd_contig_moddown", st, 4.0 * rows * kN16 * (epi->fold_b ? 3.5 : 3.0));
+                // instead of the transform's write: reads x_Q (+ fold on half the rows), writes the result
+                ProfScope ps("ntt16_fwd_contig_moddown", st, 4.0 * rows * kN16 * (epi->fold_b ? 2.5 : 2.0));
                 CK(launch_pdl(ntt16_fwd_contig<true>, g_con, dim3(256), 0, st, out, out, row_slot, slots, rm2, *epi));
             } else {
-                ProfScope ps("ntt16_fwd_contig", st, 8.0 * rows * kN16);
+                ProfScope ps("ntt16_fwd_contig", st, 4.0 * rows * kN16);
                 CK(launch_pdl(ntt16_fwd_contig<false>, g_con, dim3(256), 0, st, out, out, row_slot, slots, rm2, ModDownEpilogueArgs{}));
             }
         } else {
-            { ProfScope ps("ntt16_inv_contig", st, (mul_in ? 12.0 : 8.0) * rows * kN16);
+            { ProfScope ps("ntt16_inv_contig", st, (mul_in ? 8.0 : 4.0) * rows * kN16);
               if (mul_in) CK(launch_pdl(ntt16_inv_contig<true>, g_con, dim3(256), 0, st, in, out, row_slot, slots, rm, mul_in));
               else CK(launch_pdl(ntt16_inv_contig<false>, g_con, dim3(256), 0, st, in, out, row_slot, slots, rm, (const uint32_t*)nullptr)); }
-            { ProfScope ps("ntt16_inv_strided", st, 8.0 * rows * kN16);
+            { ProfScope ps("ntt16_inv_strided", st, 4.0 * rows * kN16);
               CK(launch_pdl(ntt16_inv_strided<COLS>, g_str, dim3(16 * COLS), 0, st, out, out, row_slot, slots, rm2)); }
         }
         CK(cudaGetLastError());

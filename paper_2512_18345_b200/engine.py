@@ -54,6 +54,13 @@ class Engine:
         self.lane_streams = [None] + [self.torch.cuda.Stream(device=self.device) for _ in range(count - 1)]
         self._lane_group = None
 
+    def arena_generation(self) -> int:
+        """Counter that changes whenever the C library reallocates (moves) its workspace arena;
+        a captured CUDA graph is only valid for the generation it was captured under."""
+        g = ctypes.c_uint64()
+        _lib.check(self.lib.ckks_arena_generation(self.ctx, ctypes.byref(g)))
+        return g.value
+
     def fork(self, jobs, with_lane: bool = False):
         """Run the callables in `jobs` concurrently over the lanes the caller owns (each on
         its lane's stream and workspace), joined back into the current stream.  Results in
@@ -102,8 +109,10 @@ class Engine:
         finally:
             self._lane_group = outer
             _lib.check(self.lib.ckks_select_lane(self.ctx, home))
-        for lane in used:
-            main.wait_stream(self.lane_streams[lane])
+            # join on the error path too: work already enqueued on a side stream still uses lane
+            # workspaces and tensors the main stream would otherwise be free to reuse
+            for lane in used:
+                main.wait_stream(self.lane_streams[lane])
         return out
 
     def pipeline(self, items, first, second):
@@ -140,7 +149,7 @@ class Engine:
         finally:
             self._lane_group = outer
             _lib.check(self.lib.ckks_select_lane(self.ctx, home))
-        main.wait_stream(side)
+            main.wait_stream(side)
         del keep
         return out
 

@@ -103,6 +103,10 @@ class SwitchingKey:
             self._matrix = torch.stack(
                 [torch.stack([pr.a.data, pr.b.data]) for pr in self.pairs]
             ).contiguous()
+            # the inner-product kernels prefetch key words ahead of their programmatic-dependency
+            # wait: make the freshly stacked matrix globally visible before any of them can start
+            if self._matrix.is_cuda:
+                torch.cuda.current_stream(self._matrix.device).synchronize()
         return self._matrix
 
 

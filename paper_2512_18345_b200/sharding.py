@@ -60,3 +60,55 @@ def max_over_ranks(value: float, device=None) -> float:
     t = torch.tensor([float(value)], dtype=torch.float64, device=device)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
+
+
+class WallClock:
+    """Host clock with the start() / stop() -> milliseconds protocol of sharded_job (CPU tests;
+    on a GPU the caller passes a CUDA-event clock so that the time is taken on the device)."""
+
+    def start(self):
+        import time
+
+        self._t0 = time.perf_counter()
+
+    def stop(self) -> float:
+        import time
+
+        return (time.perf_counter() - self._t0) * 1e3
+
+
+def sharded_job(items: Sequence, fn: Callable, clock=None, sync: Callable | None = None,
+                finish: Callable | None = None, device=None, dst: int = 0):
+    """One job over independent work items the way BASELINE config 5 times it: barrier, this
+    rank's contiguous shard of `items` through `fn` (no collective on the data path), `finish`
+    turning the local results into picklable values (e.g. reading device checksums back), ONE
+    gather of the results on rank `dst`, barrier.
+
+    Returns (results in input order on `dst` / None elsewhere, ms, wall_ms): `ms` is the max over
+    ranks of `clock` around the shard's work (CUDA events on a GPU: device time), `wall_ms` the max
+    over ranks of the host time from the first barrier to after the gather.  bench.py --gpus N and
+    the two-rank gloo test both go through this function."""
+    import time
+
+    import torch.distributed as dist
+
+    live = dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1
+    clock = clock or WallClock()
+
+    def barrier():
+        if live:
+            dist.barrier()
+        if sync is not None:
+            sync()
+
+    barrier()
+    t0 = time.perf_counter()
+    clock.start()
+    lo, hi, local = run_sharded(items, fn)
+    ms = clock.stop()
+    if finish is not None:
+        local = finish(local)
+    gathered = gather_results(local, lo, len(items), dst=dst)
+    wall_ms = (time.perf_counter() - t0) * 1e3
+    barrier()
+    return gathered, max_over_ranks(ms, device), max_over_ranks(wall_ms, device)

@@ -1,0 +1,86 @@
+"""The headline circuit against the composed CPU oracle.
+
+The reference has no bootstrapping; its oracle is the package's own
+circuit (bootstrap.py) replayed on the C restatement of the reference primitives
+(oracle/engine_oracle.py; building blocks pinned to the reference by golden.json and
+golden_level.json).  tests/golden/golden_bootstrap.json holds that oracle's limb digests after
+every phase (tests/golden/make_golden_bootstrap.py).
+
+ * CPU (not gpu): the oracle bootstrap at N = 2^11 reproduces the committed digests and
+   refreshes the message to 2^-20.
+ * gpu: the CUDA bootstrap -- eager, and as the 8-lane CUDA graph bench.py times -- at
+   N = 2^11 and at the headline configuration (ks48: N = 2^16, 2^15 slots, dense key with
+   sparse-secret encapsulation) equals the oracle replayed on the same box phase by phase and
+   limb for limb, and equals the committed digests.
+
+The circuit's plaintexts (DFT diagonals) are encoded on the host in floating point.  Live
+comparisons share them; the committed digests are compared only when this machine encodes the
+same plaintext limbs as the machine that generated them ("plaintexts" digest), otherwise that
+part is reported as skipped rather than failed."""
+import json
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+import make_golden_bootstrap as G
+
+GOLD = json.loads((Path(__file__).resolve().parent / "golden" / "golden_bootstrap.json").read_text())["cases"]
+
+
+def with_oracle(fn):
+    from oracle.engine_oracle import OracleEngine
+    from paper_2512_18345_b200 import engine
+
+    previous = engine.use_backend(OracleEngine())
+    try:
+        return fn()
+    finally:
+        engine.use_backend(previous)
+
+
+def check_against_committed(name, rec):
+    g = GOLD[name]
+    if rec["plaintexts"] != g["plaintexts"]:
+        pytest.skip("this host encodes the DFT diagonals with different floating-point rounding than the "
+                    "golden generator's; live oracle comparison above still applies")
+    assert rec["input"] == g["input"]
+    assert rec["phases"] == g["phases"]
+    assert rec["out_level"] == g["out_level"]
+
+
+def test_oracle_bootstrap_n2048_matches_committed_digests():
+    rec, _ = with_oracle(lambda: G.run_case("n2048"))
+    assert rec["precision_log2"] < -20.0, rec["precision_log2"]
+    assert set(rec["phases"]) == {"mod_raise", "coeff_to_slot_lo", "coeff_to_slot_hi", "eval_mod", "slot_to_coeff"}
+    check_against_committed("n2048", rec)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name,bar", [("n2048", -20.0), ("ks48", -18.57)])
+def test_cuda_bootstrap_equals_oracle(name, bar):
+    """bar: 2^-20 at N = 2^11; at N = 2^16 the paper's reported precision."""
+    import torch
+
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    from paper_2512_18345_b200 import ckks
+    from paper_2512_18345_b200.engine import get_engine
+
+    eng = get_engine()
+    eng.set_lanes(1)
+    rec, (p, sk, boot, z, ct) = G.run_case(name)                      # CUDA, eager, one lane
+    assert rec["precision_log2"] < bar, rec["precision_log2"]
+    # the graph bench.py replays: 8 stream lanes, nested forks, programmatic dependent launches
+    eng.set_lanes(8)
+    replay = boot.capture(ct)
+    out = replay(ct)
+    torch.cuda.synchronize()
+    assert G.ct_digest(out) == rec["phases"]["slot_to_coeff"], "8-lane graph differs from the eager bootstrap"
+    eng.set_lanes(1)
+    # the oracle on the same keys, plaintexts and input (pulled to the host per operation)
+    phases = {}
+    o_out = with_oracle(lambda: boot.bootstrap(ct, trace=lambda nm, c: phases.__setitem__(nm, G.ct_digest(c))))
+    for nm in ("mod_raise", "coeff_to_slot_lo", "coeff_to_slot_hi", "eval_mod", "slot_to_coeff"):
+        assert phases[nm] == rec["phases"][nm], f"CUDA and oracle limbs differ after {nm}"
+    assert ckks.level_of(o_out) == rec["out_level"]
+    check_against_committed(name, rec)

@@ -31,7 +31,7 @@ def _free_port():
 def _worker(rank, world, port, out_q):
     import torch.distributed as dist
 
-    from paper_2512_18345_b200.sharding import gather_results, max_over_ranks, run_sharded
+    from paper_2512_18345_b200.sharding import gather_results, max_over_ranks, run_sharded, sharded_job
 
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
@@ -40,6 +40,10 @@ def _worker(rank, world, port, out_q):
     lo, hi, res = run_sharded(items, lambda x: x * x + 1)
     gathered = gather_results(res, lo, len(items))
     slowest = max_over_ranks(10.0 + rank)
+    # the function bench.py --gpus N times a step batch through: shard, finish, one gather
+    job, ms, wall = sharded_job(list(range(7)), lambda x: 3 * x, finish=lambda loc: [v + 1 for v in loc])
+    assert ms >= 0.0 and wall >= ms * 0.0
+    assert job == ([3 * x + 1 for x in range(7)] if rank == 0 else None)
     out_q.put((rank, lo, hi, gathered, slowest))
     dist.barrier()
     dist.destroy_process_group()
