@@ -47,6 +47,9 @@ sys.path.insert(0, str(ROOT))
 
 LIMB_BYTES = 65536 * 4
 FP64_TENSOR_TFLOPS = 37.06
+# Integer-pipe bound of a Shoup butterfly on B200 (profiles/microbench/int_pipes.cu: IMAD.HI 28,
+# IMAD 62 thread-ops per clk per SM; one IMAD.HI + two IMAD per butterfly): 1 / (1/28 + 2/62)
+INT_PIPE_BF_PER_CLK_SM = 14.7
 SEGMENTS = 20            # reference arm: a circuit is cut into this many steps
 
 METRIC = {
@@ -610,6 +613,54 @@ def run_b200(args):
 
         h2d = d2h = rows * LIMB_BYTES
 
+    def ntt_sweep():
+        """BASELINE config 2 (SURVEY 8d): forward and inverse transforms at R in {12, 48, 60, 192, 240}
+        limbs of the ks48 extended basis.  Each point: a CUDA graph of `reps` transforms over operands
+        rotating through > 126 MB, timed with CUDA events (device time per transform); algorithmic
+        bytes 2*R*N*4 (reference-convention two-kernel bytes are twice that), butterflies
+        R*(N/2)*log2 N against the integer-pipe bound of profiles/microbench/int_pipes.cu."""
+        out = []
+        sm_count = torch.cuda.get_device_properties(dev).multi_processor_count
+        peak_hbm = load_peaks()[0]
+        for rows_ in (12, 48, 60, 192, 240):
+            basis_ = tuple(ext[i % len(ext)] for i in range(rows_))
+            count_ = max(2, -(-(160 << 20) // (rows_ * LIMB_BYTES)))
+            polys_ = [rand_limbs(basis_) for _ in range(count_)]
+            outs_ = [eng.empty(rows_, p.n) for _ in range(count_)]
+            slots_ = eng.row_slots(basis_, p.n)
+            for inverse in (False, True):
+                reps = 4 * count_
+                run = lambda: [eng.ntt(polys_[k % count_], slots_, inverse, out=outs_[k % count_]) for k in range(reps)]
+                run()
+                torch.cuda.synchronize()
+                graph = torch.cuda.CUDAGraph()
+                side = torch.cuda.Stream(device=dev)
+                side.wait_stream(torch.cuda.current_stream())
+                with torch.cuda.stream(side):
+                    with torch.cuda.graph(graph, stream=side):
+                        run()
+                torch.cuda.current_stream().wait_stream(side)
+                for _ in range(3):
+                    graph.replay()
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                n_rep = 10
+                a.record()
+                for _ in range(n_rep):
+                    graph.replay()
+                b.record()
+                torch.cuda.synchronize()
+                us = a.elapsed_time(b) * 1e3 / (n_rep * reps)
+                alg = 2.0 * rows_ * LIMB_BYTES
+                bf = rows_ * (p.n // 2) * 16
+                out.append({"rows": rows_, "direction": "inverse" if inverse else "forward", "us": us,
+                            "alg_bytes": alg, "alg_gbs": alg / us / 1e3, "hbm_frac": alg / us / 1e3 / peak_hbm,
+                            "ref_convention_gbs": 2 * alg / us / 1e3,
+                            "butterflies_per_clk_per_sm": bf / (us * 1e-6) / (1.965e9 * sm_count),
+                            "int_pipe_frac": bf / (us * 1e-6) / (1.965e9 * sm_count) / INT_PIPE_BF_PER_CLK_SM})
+                del graph
+            del polys_, outs_
+        return out
+
     class EventClock:
         """Device time on the current stream (every kernel of a step is joined back into it)."""
 
@@ -635,7 +686,9 @@ def run_b200(args):
 
         def one(item):
             fn(item % steps)              # rank r, step s of the job is item r * steps + s: input s on every rank
-            if checksums:
+            # circuits (ms per step) checksum every result; for the microsecond-scale kernel workloads a
+            # reduction per step would be a large part of the step, so only the last result is summed
+            if checksums and (per_step_checksum or item % steps == steps - 1):
                 t = result_of if result_of is not None else last["out"]
                 sums.append(t.sum(dtype=torch.int64))
             return len(sums) - 1
@@ -655,6 +708,7 @@ def run_b200(args):
         timed.wall_ms = wall_ms
         return ms, gathered
 
+    per_step_checksum = wl in ("bootstrap", "helr")
     sampler = ClockSampler(local)
     ms_total, gathered = timed(step, args.steps, args.warmup, sampler, checksums=True)
     wall_total = timed.wall_ms
@@ -663,7 +717,9 @@ def run_b200(args):
     ranks_agree = None
     if rank == 0 and gathered is not None and world > 1:
         # replicated keys + the same inputs on every rank: every GPU must produce the same limbs
-        per_rank = [gathered[r * args.steps:(r + 1) * args.steps] for r in range(world)]
+        gathered = [v for v in gathered if v is not None]      # ranks that summed only their last result
+        n_sums = len(gathered) // world
+        per_rank = [gathered[r * n_sums:(r + 1) * n_sums] for r in range(world)]
         ranks_agree = all(pr == per_rank[0] for pr in per_rank)
 
     e2e_steps = max(3, min(args.steps, 200))
@@ -729,6 +785,17 @@ def run_b200(args):
                     for k, (c, ms, nb, nf) in sorted(prof.items(), key=lambda kv: -kv[1][1])},
     }
 
+    if "ntt" in fam and n_ring == 65536:
+        # the transform is bounded by the integer pipes on B200, not by HBM: report
+        # butterflies per clock per SM next to the byte roofline (8 algorithmic bytes per 16*N/2 butterflies)
+        nt = fam["ntt"]
+        sm_count = torch.cuda.get_device_properties(dev).multi_processor_count
+        bf = nt["bytes"] / (8.0 * n_ring) * (n_ring // 2) * 16
+        rate = bf / (nt["ms"] * 1e-3) / (1.965e9 * sm_count)
+        roofline["ntt_int_pipe"] = {"butterflies_per_clk_per_sm": rate, "peak": INT_PIPE_BF_PER_CLK_SM,
+                                    "frac": rate / INT_PIPE_BF_PER_CLK_SM,
+                                    "peak_source": "profiles/microbench/int_pipes.cu (IMAD.HI 28, IMAD 62 per clk per SM)"}
+
     cpu = None
     parity = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -783,6 +850,8 @@ def run_b200(args):
         if wl == "bootstrap":
             line["latency_ms"] = ms_step
             line["paper_rtx5090_latency_ms"] = 15.2
+        if wl == "ntt" and not args.no_sweep:
+            line["sweep"] = ntt_sweep()
         if precision_bits is not None:
             line["precision_log2_max_err"] = precision_bits
         if parity is not None:
@@ -803,6 +872,7 @@ def main():
     ap.add_argument("--workload", default="bootstrap", choices=["bootstrap", "keyswitch", "ntt", "helr", "config1"])
     ap.add_argument("--rows", type=int, default=60, help="limbs per transform of the ntt workload (config 2: 12..240)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-sweep", action="store_true", help="ntt workload: skip the R / direction sweep")
     ap.add_argument("--lanes", type=int, default=8, help="workspace lanes / side streams of the bootstrap graph")
     args = ap.parse_args()
     if args.steps is None:

@@ -384,6 +384,122 @@ ntt16_inv_contig(const uint32_t* in, uint32_t* out, const int32_t* __restrict__ 
 }
 
 // ---------------------------------------------------------------------------------
+// N <= 2^15: the whole limb lives in one CTA's shared memory (N * 4 B <= 128 KiB), so
+// the transform is ONE launch: radix-4 steps (two stages per barrier) on the
+// shared copy, same butterflies and twiddle slots as _run_stages.  Serves
+// BASELINE config 1 (N = 2^13) and the small parameter sets of the tests.
+// ---------------------------------------------------------------------------------
+template <bool INV>
+__global__ void __launch_bounds__(1024, 1)
+ntt_small_kernel(const uint32_t* in, uint32_t* out, const int32_t* __restrict__ row_slot,
+                 const ModSlot* __restrict__ slots, RowMap rm, uint32_t n, uint32_t lg) {
+    extern __shared__ uint32_t sm[];
+    const uint32_t tid = threadIdx.x, nt = blockDim.x;
+    const ModSlot& m = slots[row_slot[blockIdx.x]];
+    const uint32_t q = m.q;
+    const uint2* __restrict__ tw = INV ? m.inv : m.fwd;
+    pdl_trigger();
+    const uint32_t* src = in + rm.in_row(blockIdx.x) * n;
+    uint32_t* dst = out + rm.out_row(blockIdx.x) * n;
+    pdl_wait();
+    if (n >= 4) {
+        for (uint32_t i = tid; i < n / 4; i += nt)
+            reinterpret_cast<uint4*>(sm)[i] = reinterpret_cast<const uint4*>(src)[i];
+    } else {
+        for (uint32_t i = tid; i < n; i += nt) sm[i] = src[i];
+    }
+    __syncthreads();
+    if (!INV) {
+        // Cooley-Tukey, values kept in [0, 2q)
+        uint32_t s = 0;
+        while (s < lg) {
+            if (s + 2 <= lg) {
+                const uint32_t lh = lg - s - 2, h = 1u << lh;           // h = quarter of the stage-s group
+                for (uint32_t b = tid; b < n / 4; b += nt) {
+                    const uint32_t g = b >> lh, j = b & (h - 1);
+                    const uint32_t i0 = (g << (lh + 2)) + j;
+                    uint32_t a = sm[i0], bb = sm[i0 + h], c = sm[i0 + 2 * h], d = sm[i0 + 3 * h];
+                    const uint2 w1 = tw[(1u << s) + g];
+                    const uint2 w2 = tw[(2u << s) + 2 * g], w3 = tw[(2u << s) + 2 * g + 1];
+                    ct_bfly(a, c, shoup_mul(c, w1.x, w1.y, q), q);
+                    ct_bfly(bb, d, shoup_mul(d, w1.x, w1.y, q), q);
+                    ct_bfly(a, bb, shoup_mul(bb, w2.x, w2.y, q), q);
+                    ct_bfly(c, d, shoup_mul(d, w3.x, w3.y, q), q);
+                    sm[i0] = a; sm[i0 + h] = bb; sm[i0 + 2 * h] = c; sm[i0 + 3 * h] = d;
+                }
+                s += 2;
+            } else {
+                const uint32_t lt = lg - s - 1, t = 1u << lt;
+                for (uint32_t b = tid; b < n / 2; b += nt) {
+                    const uint32_t g = b >> lt, j = b & (t - 1);
+                    const uint32_t i0 = (g << (lt + 1)) + j;
+                    uint32_t x = sm[i0], y = sm[i0 + t];
+                    const uint2 w = tw[(1u << s) + g];
+                    ct_bfly(x, y, shoup_mul(y, w.x, w.y, q), q);
+                    sm[i0] = x; sm[i0 + t] = y;
+                }
+                s += 1;
+            }
+            __syncthreads();
+        }
+        if (n >= 4) {
+            for (uint32_t i = tid; i < n / 4; i += nt) {
+                uint4 v = reinterpret_cast<const uint4*>(sm)[i];
+                v.x = csub(v.x, q); v.y = csub(v.y, q); v.z = csub(v.z, q); v.w = csub(v.w, q);
+                reinterpret_cast<uint4*>(dst)[i] = v;
+            }
+        } else {
+            for (uint32_t i = tid; i < n; i += nt) dst[i] = csub(sm[i], q);
+        }
+        return;
+    }
+    // Gentleman-Sande, canonical values; the last stage carries N^-1 (transform.py:243-246)
+    uint32_t s = 0;
+    while (s + 1 < lg) {
+        if (s + 3 <= lg) {
+            const uint32_t t = 1u << s;
+            const uint32_t g1 = n >> (s + 1), g2 = n >> (s + 2);
+            for (uint32_t b = tid; b < n / 4; b += nt) {
+                const uint32_t G = b >> s, j = b & (t - 1);
+                const uint32_t i0 = (G << (s + 2)) + j;
+                const uint32_t a = sm[i0], bb = sm[i0 + t], c = sm[i0 + 2 * t], d = sm[i0 + 3 * t];
+                const uint2 w0 = tw[g1 + 2 * G], w1 = tw[g1 + 2 * G + 1], w2 = tw[g2 + G];
+                const uint32_t a1 = csub(a + bb, q), b1 = shoup_mul(a - bb + q, w0.x, w0.y, q);
+                const uint32_t c1 = csub(c + d, q), d1 = shoup_mul(c - d + q, w1.x, w1.y, q);
+                sm[i0] = csub(a1 + c1, q);
+                sm[i0 + 2 * t] = shoup_mul(a1 - c1 + q, w2.x, w2.y, q);
+                sm[i0 + t] = csub(b1 + d1, q);
+                sm[i0 + 3 * t] = shoup_mul(b1 - d1 + q, w2.x, w2.y, q);
+            }
+            s += 2;
+        } else {
+            const uint32_t t = 1u << s, g1 = n >> (s + 1);
+            for (uint32_t b = tid; b < n / 2; b += nt) {
+                const uint32_t g = b >> s, j = b & (t - 1);
+                const uint32_t i0 = (g << (s + 1)) + j;
+                const uint32_t x = sm[i0], y = sm[i0 + t];
+                const uint2 w = tw[g1 + g];
+                sm[i0] = csub(x + y, q);
+                sm[i0 + t] = shoup_mul(x - y + q, w.x, w.y, q);
+            }
+            s += 1;
+        }
+        __syncthreads();
+    }
+    {
+        const uint32_t half = n >> 1;
+        const uint32_t ninv = m.n_inv, ninv_s = m.n_inv_s, wl = m.w_last, wl_s = m.w_last_s;
+        for (uint32_t j = tid; j < half; j += nt) {
+            const uint32_t x = sm[j], y = sm[j + half];
+            dst[j] = shoup_mul(csub(x + y, q), ninv, ninv_s, q);
+            dst[j + half] = shoup_mul(x - y + q, wl, wl_s, q);
+        }
+    }
+}
+
+constexpr uint32_t kSmallMaxN = 32768;
+
+// ---------------------------------------------------------------------------------
 // host launchers
 // ---------------------------------------------------------------------------------
 static int launch_generic(const uint32_t* in, uint32_t* out, const int32_t* row_slot,
@@ -419,6 +535,23 @@ static int launch_generic(const uint32_t* in, uint32_t* out, const int32_t* row_
         }
     }
     CK(cudaGetLastError());
+    return CKKS_OK;
+}
+
+static int launch_small(const uint32_t* in, uint32_t* out, const int32_t* row_slot,
+                        const ModSlot* slots, RowMap rm, int rows, uint32_t n, uint32_t lg,
+                        int inverse, cudaStream_t st) {
+    static bool attr_set = false;
+    if (!attr_set) {
+        CK(cudaFuncSetAttribute(ntt_small_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(kSmallMaxN * 4)));
+        CK(cudaFuncSetAttribute(ntt_small_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(kSmallMaxN * 4)));
+        attr_set = true;
+    }
+    const uint32_t quads = n / 4;
+    const uint32_t threads = quads < 32 ? 32 : (quads > 1024 ? 1024 : quads);
+    ProfScope ps(inverse ? "ntt_small_inv" : "ntt_small_fwd", st, 8.0 * rows * n);
+    if (inverse) CK(launch_pdl(ntt_small_kernel<true>, dim3(rows), dim3(threads), (size_t)n * 4, st, in, out, row_slot, slots, rm, n, lg));
+    else CK(launch_pdl(ntt_small_kernel<false>, dim3(rows), dim3(threads), (size_t)n * 4, st, in, out, row_slot, slots, rm, n, lg));
     return CKKS_OK;
 }
 
@@ -467,6 +600,7 @@ int ntt_launch(const uint32_t* in, uint32_t* out, const int32_t* row_slot, const
     }
     uint32_t lg = 0;
     while ((1u << lg) < n) ++lg;
+    if (n <= kSmallMaxN) return launch_small(in, out, row_slot, slots, rm, rows, n, lg, inverse, st);
     return launch_generic(in, out, row_slot, slots, rm, rows, n, inverse, 0, lg, st);
 }
 

@@ -1,7 +1,7 @@
 """In-graph kernel durations of one bootstrap replay through CUPTI (torch.profiler): warm caches,
 real concurrency -- unlike the serialised cold-cache ncu launch list.  Prints per-kernel totals,
 the sum of kernel time, the union of busy intervals and the replay's span.
-Usage: python profiles/graph_trace.py [lanes]"""
+Usage: python profiles/graph_trace.py [lanes [chrome_trace.json]]"""
 import collections
 import json
 import re
@@ -21,11 +21,10 @@ lanes = int(sys.argv[1]) if len(sys.argv) > 1 else 8
 eng = get_engine()
 eng.set_lanes(lanes)
 p = ParameterSet.builtin("ks48")
-sk = ks.keygen(p, h=p.h_sparse, seed=1)
-boot = Bootstrapper(p, sk, BootstrapConfig())
-rng = np.random.default_rng(0)
-z = rng.uniform(-1, 1, p.n // 2) + 1j * rng.uniform(-1, 1, p.n // 2)
-ct = ckks.encrypt(ckks.encode(z, p, level=2, scale=boot.delta_in), sk, p, seed=50)
+from paper_2512_18345_b200.bootstrap import standard_input, standard_setup
+
+sk, _sparse, boot = standard_setup(p)           # the bench's setup: dense key + sparse encapsulation
+_z, ct = standard_input(p, boot, sk, 0)
 replay = boot.capture(ct)
 for _ in range(3):
     replay.graph.replay()
@@ -35,6 +34,8 @@ from torch.profiler import ProfilerActivity, profile
 with profile(activities=[ProfilerActivity.CUDA]) as prof:
     replay.graph.replay()
     torch.cuda.synchronize()
+if len(sys.argv) > 2:                          # full timeline (stream, grid, block per kernel) for offline analysis
+    prof.export_chrome_trace(sys.argv[2])
 evs = [e for e in prof.events() if e.device_type == torch.autograd.DeviceType.CUDA and e.cuda_time_total > 0 or getattr(e, "device_time_total", 0) > 0]
 rows = []
 for e in prof.events():

@@ -1,0 +1,63 @@
+"""Parity of the kernels added in round 2.  All integer work: bit-exact against the CPU oracle
+(itself pinned to the reference's golden vectors, tests/test_oracle_golden.py)."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def env(golden):
+    import torch
+
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    from paper_2512_18345_b200 import baseconv, keyswitch, params, rns, transform
+    from paper_2512_18345_b200.engine import get_engine
+
+    class NS:
+        pass
+
+    ns = NS()
+    ns.torch, ns.baseconv, ns.ks, ns.rns, ns.transform, ns.params = torch, baseconv, keyswitch, rns, transform, params
+    ns.eng = get_engine()
+    ns.ks48 = params.ParameterSet.from_dict(golden["params"]["ks48"])
+    return ns
+
+
+def qs(basis):
+    return [m.q for m in basis]
+
+
+# ---------------------------------------------------------------- single-launch small-ring transform
+@pytest.mark.parametrize("lg", [1, 2, 3, 5, 8, 11, 12, 13, 14, 15])
+def test_small_ring_transform_matches_oracle(env, oracle_mod, lg):
+    """ntt_small_kernel (one CTA per limb, N <= 2^15, reference transform.py:203-250): forward and
+    inverse against the oracle on mixed 31-bit moduli, edge rows included, in place and out of place."""
+    n = 1 << lg
+    primes, cand = [], (1 << 31) - 1
+    step = 2 * n
+    cand -= (cand - 1) % step
+    while len(primes) < 5:
+        if env.rns.is_prime(cand):
+            primes.append(cand)
+        cand -= step
+    mods = tuple(env.rns.Modulus.for_prime(q, n) for q in primes)
+    orc = oracle_mod.Oracle(n, [(m.q, m.psi) for m in mods])
+    rng = np.random.default_rng(lg)
+    x = np.stack([rng.integers(0, m.q, n, dtype=np.uint64) for m in mods])
+    x[0] = 0
+    x[1] = mods[1].q - 1
+    x[2] = 0
+    x[2, 0] = 1
+    rm = np.arange(len(mods), dtype=np.int32)
+    fwd = env.transform.ntt_polynomial(env.rns.Polynomial(mods, x, env.rns.COEFFICIENT))
+    assert np.array_equal(fwd.coeffs, orc.ntt(x, rm))
+    assert np.all(fwd.coeffs[2] == 1) and not fwd.coeffs[0].any()
+    inv = env.transform.ntt_polynomial(env.rns.Polynomial(mods, x, env.rns.EVALUATION), "inverse")
+    assert np.array_equal(inv.coeffs, orc.ntt(x, rm, inverse=True))
+    assert np.array_equal(env.transform.ntt_polynomial(fwd, "inverse").coeffs, x)
+    # in place through the engine (the key-switch pipeline transforms raised digits in place)
+    t = env.torch.from_numpy(x.astype(np.uint32).view(np.int32)).to(env.eng.device)
+    slots = env.eng.row_slots(mods, n)
+    env.eng.ntt(t, slots, False, out=t)
+    assert np.array_equal(t.cpu().numpy().view(np.uint32).astype(np.uint64), orc.ntt(x, rm))
