@@ -333,6 +333,30 @@ def oracle_kernel_step(workload, args):
     return lambda: orc.keyswitch(op, a, b, evk)
 
 
+def numpy_reference_timing(workload, args):
+    """The REAL reference (NumPy package, travelling copy under baseline/_ref) timed on the host
+    cores by baseline/time_reference.py in a subprocess: single-process latency and a process pool
+    over independent inputs (SURVEY 8d "CPU baseline").  None for the circuits (the reference has
+    no bootstrap / HELR entry point) or when the copy is absent."""
+    import subprocess
+
+    if workload not in ("ntt", "keyswitch", "config1"):
+        return None
+    script = ROOT / "baseline" / "time_reference.py"
+    if not (ROOT / "baseline" / "_ref" / "rnscope").is_dir():
+        return {"unavailable": "no travelling copy of the reference (baseline/_ref/rnscope); run __graft_entry__.build() "
+                               "where /root/reference exists"}
+    env = dict(os.environ)
+    env["OMP_NUM_THREADS"] = "1"
+    try:
+        res = subprocess.run([sys.executable, str(script), workload, "--rows", str(args.rows)], capture_output=True,
+                             text=True, timeout=600, env=env)
+        lines = [ln for ln in res.stdout.splitlines() if ln.startswith("{")]
+        return json.loads(lines[-1]) if lines else {"unavailable": (res.stderr or "no output").strip()[-300:]}
+    except Exception as exc:                      # a baseline, never a reason to lose the bench line
+        return {"unavailable": repr(exc)[:300]}
+
+
 def run_reference(args):
     """Rank 0 alone runs and prints; the other ranks exit without work."""
     if int(os.environ.get("RANK", "0")) != 0:
@@ -375,6 +399,9 @@ def run_reference(args):
                          "cpu": cpu_model(), "sample": sample},
         "e2e": {"value": value, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
+    ref = numpy_reference_timing(wl, args)
+    if ref is not None:
+        line["cpu_baseline"]["reference"] = ref
     print(json.dumps(line), flush=True)
 
 
@@ -832,6 +859,9 @@ def run_b200(args):
             cpu = {"value": 1.0 / cpu_s, "unit": unit_name, "cores": host_threads(), "kind": "port",
                    "cpu": cpu_model(), "ms_per_step": cpu_s * 1e3,
                    "sample": f"{reps} whole steps of the workload on oracle/ckks_oracle.c (OpenMP)"}
+            ref = numpy_reference_timing(wl, args)
+            if ref is not None:
+                cpu["reference"] = ref
 
     if rank == 0:
         line = {

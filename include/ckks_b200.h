@@ -87,6 +87,13 @@ int ckks_arena_reserve(ckks_ctx* ctx, size_t words_per_lane);
  * per (q, n, psi).  Not capturable (allocates, copies). */
 int ckks_modulus_register(ckks_ctx* ctx, uint32_t q, uint32_t n, uint32_t psi, int32_t* slot);
 
+/* A slot whose twiddle tables are the CALLER's (n words each, residues mod q, schedule order of
+ * transform.py:43-49) instead of powers of a root: `ntt(limb, m, table)` in the reference uses
+ * whatever table it is handed (transform.py:253-276), which is what its twiddle-corruption
+ * negative control relies on (verify.py:51-57).  Always a fresh slot.  Not capturable. */
+int ckks_modulus_register_tables(ckks_ctx* ctx, uint32_t q, uint32_t n, const uint32_t* fwd,
+                                 const uint32_t* inv, uint32_t n_inv, int32_t* slot);
+
 /* Copy a slot's tables back to the host (TwiddleTable.fwd/inv/n_inv,
  * transform.py:43-64); fwd/inv hold n words each. */
 int ckks_modulus_tables(ckks_ctx* ctx, int32_t slot, uint32_t* fwd, uint32_t* inv, uint32_t* n_inv);

@@ -393,6 +393,48 @@ int ckks_modulus_register(ckks_ctx* ctx, uint32_t q, uint32_t n, uint32_t psi, i
     return CKKS_OK;
 }
 
+int ckks_modulus_register_tables(ckks_ctx* ctx, uint32_t q, uint32_t n, const uint32_t* fwd_w,
+                                 const uint32_t* inv_w, uint32_t n_inv, int32_t* slot) {
+    CKS(check_ctx(ctx));
+    if (!slot || !fwd_w || !inv_w) { set_last_error("null pointer"); return CKKS_ERR_ARG; }
+    if (q < 3 || !(q & 1) || (q >> 31)) { set_last_error("custom tables need an odd modulus below 2^31, got %u", q); return CKKS_ERR_ARG; }
+    if (n < 2 || (n & (n - 1))) { set_last_error("ring degree %u is not a power of two >= 2", n); return CKKS_ERR_ARG; }
+    if ((int)ctx->h_slots.size() >= ckks_ctx::kMaxSlots) { set_last_error("modulus slot table full"); return CKKS_ERR_STATE; }
+    ModSlot m{};
+    m.q = q;
+    uint32_t qinv = q;
+    for (int i = 0; i < 5; ++i) qinv *= 2u - q * qinv;
+    m.qinv = qinv;
+    m.r1 = (uint32_t)((1ull << 32) % q);
+    m.r2 = h_mulmod(m.r1, m.r1, q);
+    m.r1s = h_shoup(m.r1, q);
+    m.r2s = h_shoup(m.r2, q);
+    m.fast = (q > (1u << 30) && q < (1u << 31)) ? 1u : 0u;
+    std::vector<uint2> fwd(n), inv(n);
+    for (uint32_t t = 0; t < n; ++t) {
+        if (fwd_w[t] >= q || inv_w[t] >= q) { set_last_error("table entry %u is not a residue mod %u", t, q); return CKKS_ERR_ARG; }
+        fwd[t] = make_uint2(fwd_w[t], h_shoup(fwd_w[t], q));
+        inv[t] = make_uint2(inv_w[t], h_shoup(inv_w[t], q));
+    }
+    uint2 *d_fwd, *d_inv;
+    CKS(upload(fwd, &d_fwd));
+    CKS(upload(inv, &d_inv));
+    ctx->owned.push_back(d_fwd);
+    ctx->owned.push_back(d_inv);
+    m.fwd = d_fwd;
+    m.inv = d_inv;
+    m.n = n;
+    m.n_inv = n_inv % q;
+    m.n_inv_s = h_shoup(m.n_inv, q);
+    m.w_last = h_mulmod(inv[1].x, m.n_inv, q);       // transform.py:243-246: the last stage's twiddle carries N^-1
+    m.w_last_s = h_shoup(m.w_last, q);
+    const int32_t id = (int32_t)ctx->h_slots.size();
+    CK(cudaMemcpy(ctx->d_slots + id, &m, sizeof(ModSlot), cudaMemcpyHostToDevice));
+    ctx->h_slots.push_back(m);                       // not entered in slot_index: never returned for (q, n, psi)
+    *slot = id;
+    return CKKS_OK;
+}
+
 int ckks_modulus_tables(ckks_ctx* ctx, int32_t slot, uint32_t* fwd, uint32_t* inv, uint32_t* n_inv) {
     CKS(check_ctx(ctx));
     CKS(check_slot(ctx, slot));

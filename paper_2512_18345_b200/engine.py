@@ -175,6 +175,21 @@ class Engine:
             s = self._slots[key] = out.value
         return s
 
+    def custom_table_slot(self, q: int, n: int, fwd, inv, n_inv: int) -> int:
+        """Slot whose device twiddle tables are the given host arrays (a caller-built or
+        deliberately corrupted TwiddleTable); memoised on the table contents."""
+        fwd = np.ascontiguousarray(fwd, dtype=np.uint32)
+        inv = np.ascontiguousarray(inv, dtype=np.uint32)
+        key = (q, n, int(n_inv), fwd.tobytes(), inv.tobytes())
+        cache = self.__dict__.setdefault("_custom_slots", {})
+        s = cache.get(key)
+        if s is None:
+            out = ctypes.c_int32()
+            _lib.check(self.lib.ckks_modulus_register_tables(self.ctx, q, n, fwd.ctypes.data, inv.ctypes.data,
+                                                             int(n_inv), ctypes.byref(out)))
+            s = cache[key] = out.value
+        return s
+
     def row_slots(self, basis, n: int = 0, repeat: int = 1):
         """Device int32 array: slot of every row of a limb matrix over `basis`
         (stacked `repeat` times)."""

@@ -181,9 +181,33 @@ def ntt(limb, m: Modulus, table: TwiddleTable | None = None, direction: str = FO
         raise ValueError(f"unknown direction {direction!r}")
     eng = get_engine()
     basis = (m,) * rows.shape[0]
-    out = _transform(eng.upload(rows.astype(np.uint32)), basis, n, direction)
+    if table is not None and not _is_engine_table(table, m, n):
+        # the reference transforms with whatever table it is handed (transform.py:253-276); a table
+        # that is not the engine's own (e.g. verify.py:51-57 corrupts one slot as a negative control)
+        # is uploaded and used as given
+        _check_degree(n)
+        slot = eng.custom_table_slot(m.q, n, table.fwd, table.inv, table.n_inv)
+        slots = eng.torch.full((rows.shape[0],), slot, dtype=eng.torch.int32, device=eng.device)
+        out = eng.ntt(eng.upload(rows.astype(np.uint32)), slots, direction == INVERSE)
+        counters.butterflies += rows.shape[0] * (n // 2) * _log2(n)
+    else:
+        out = _transform(eng.upload(rows.astype(np.uint32)), basis, n, direction)
     host = out.cpu().numpy().view(np.uint32).astype(np.uint64)
     return host[0] if single else host
+
+
+def _is_engine_table(table: TwiddleTable, m: Modulus, n: int) -> bool:
+    """True when `table` holds exactly the twiddles the engine's resident tables hold for (m, n)."""
+    from .engine import get_engine
+
+    eng = get_engine()
+    if not eng.has_tables(m, n):
+        return True                    # no device transform for this modulus: _transform reports it
+    own = twiddle_table(m, n)          # host copy of the resident tables, cached
+    if table is own:
+        return True
+    return (int(table.n_inv) == int(own.n_inv) and np.array_equal(np.asarray(table.fwd, dtype=np.uint64), own.fwd)
+            and np.array_equal(np.asarray(table.inv, dtype=np.uint64), own.inv))
 
 
 def _expect_domain(p: Polynomial, direction: str) -> str:

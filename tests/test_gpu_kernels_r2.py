@@ -61,3 +61,49 @@ def test_small_ring_transform_matches_oracle(env, oracle_mod, lg):
     slots = env.eng.row_slots(mods, n)
     env.eng.ntt(t, slots, False, out=t)
     assert np.array_equal(t.cpu().numpy().view(np.uint32).astype(np.uint64), orc.ntt(x, rm))
+
+
+# ---------------------------------------------------------------- negative control (verify.py:51-57)
+def _schoolbook_negacyclic(a, b, q):
+    n = len(a)
+    c = [0] * n
+    for i in range(n):
+        for j in range(n):
+            k = i + j
+            if k < n:
+                c[k] = (c[k] + int(a[i]) * int(b[j])) % q
+            else:
+                c[k - n] = (c[k - n] - int(a[i]) * int(b[j])) % q
+    return np.array(c, dtype=np.uint64)
+
+
+@pytest.mark.parametrize("n", [4, 16, 256, 4096, 65536])
+def test_twiddle_corruption_is_detected(env, n):
+    """The reference's negative control (verify.py:51-57, transform_suite with fault='twiddle'): one
+    forward twiddle slot off by one.  `ntt(limb, m, table)` must use the table it is handed, so with
+    the corrupted table the round trip / convolution checks fail, and with the clean one they pass:
+    the checks above are able to see a wrong device table."""
+    T = env.transform
+    m = env.rns.find_ntt_primes(1, 31, n)[0]
+    good = T.build_twiddle_table(m, n)
+    bad = T.build_twiddle_table(m, n)
+    slot = n // 2 + 1 if n > 2 else 1
+    fwd = bad.fwd.copy()
+    fwd[slot] = (fwd[slot] + 1) % m.q
+    bad.fwd = fwd
+    rng = np.random.default_rng(n)
+    rows = rng.integers(0, m.q, size=(8, n), dtype=np.uint64)
+    assert np.array_equal(T.ntt(T.ntt(rows, m, good), m, good, direction="inverse"), rows)
+    assert not np.array_equal(T.ntt(T.ntt(rows, m, bad), m, bad, direction="inverse"), rows)
+    # forward transforms differ exactly where the corrupted slot is used
+    assert not np.array_equal(T.ntt(rows, m, bad), T.ntt(rows, m, good))
+    if n <= 256:
+        a, b = rows[0], rows[1]
+        q = np.uint64(m.q)
+        want = _schoolbook_negacyclic(a, b, m.q)
+        ok = T.ntt(T.ntt(a, m, good) * T.ntt(b, m, good) % q, m, good, direction="inverse")
+        ko = T.ntt(T.ntt(a, m, bad) * T.ntt(b, m, bad) % q, m, bad, direction="inverse")
+        assert np.array_equal(ok, want) and not np.array_equal(ko, want)
+    # the corruption lives in its own slot: the engine's resident tables are untouched
+    again = T.build_twiddle_table(m, n)
+    assert np.array_equal(again.fwd, good.fwd)
