@@ -294,6 +294,17 @@ int ckks_ks_stage3_batch(ckks_ctx* ctx, int32_t plan, int count, const uint32_t*
  * accumulator (no separate automorphism pass, no separate sum of the b parts). */
 int ckks_ks_accumulate_rot(ckks_ctx* ctx, int32_t plan, const uint32_t* ct_a, const uint32_t* ct_b,
                            uint32_t k, const uint32_t* evk, int first, void* stream);
+
+/* The a halves only of `count` Q||P accumulators (same layout as ckks_ks_stage3_batch's input,
+ * b halves skipped); out is [count][l][n]. */
+int ckks_ks_stage3_batch_a(ckks_ctx* ctx, int32_t plan, int count, const uint32_t* qp, uint32_t* out,
+                           void* stream);
+
+/* ckks_ks_accumulate_rot for an inner sum kept over Q||P: ct_a = ModDown of its a half ([l][n]),
+ * b_qp its b half as it is ([l + alpha][n]), added to the b accumulator through X -> X^k without
+ * a ModDown or a lift (composition of keyswitch.py:318-332 and rns.py:295-320). */
+int ckks_ks_accumulate_rot_qp(ckks_ctx* ctx, int32_t plan, const uint32_t* ct_a, const uint32_t* b_qp,
+                              uint32_t k, const uint32_t* evk, int first, void* stream);
 int ckks_ks_finish(ckks_ctx* ctx, int32_t plan, int lanes_used, const uint32_t* fold_a,
                    const uint32_t* fold_b, uint32_t* out_a, uint32_t* out_b, void* stream);
 

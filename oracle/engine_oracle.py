@@ -394,6 +394,12 @@ class OracleEngine:
         q = self._np(qps)
         return self._t(np.stack([self._moddown_pair(md, q[g]) for g in range(q.shape[0])]))
 
+    def ks_stage3_batch_a(self, plan: int, qps, l: int):
+        self._tick()
+        md = self._plans[plan]
+        q = self._np(qps)
+        return self._t(np.stack([self._moddown(md, q[g, 0, :md.l], q[g, 0, md.l:]) for g in range(q.shape[0])]))
+
     def keyswitch(self, plan: int, ct_a, ct_b, evk, out=None):
         """keyswitch (keyswitch.py:444-453) at the plan's level."""
         self._tick()
@@ -475,6 +481,16 @@ class OracleEngine:
         acc = None if first else self._acc[plan]
         self._acc[plan] = self._inner(pl, self._raise(pl, self._np(ct_a)), self._np(evk), k=k,
                                       lift_b=self._np(ct_b), acc=acc)
+
+    def ks_accumulate_rot_qp(self, plan: int, ct_a, b_qp, k: int, evk, first: bool):
+        """Stage 1-2 of the key switch of sigma_k(a) accumulated over Q||P, plus sigma_k(b_qp) added
+        to the b accumulator as it is (b_qp already over Q||P)."""
+        self._tick()
+        pl = self._plans[plan]
+        acc = None if first else self._acc[plan]
+        acc = self._inner(pl, self._raise(pl, self._np(ct_a)), self._np(evk), k=k, acc=acc)
+        acc[1] = self._add(acc[1], self._gather(self._np(b_qp), pl.n, k, pl.q[0]), pl.q + pl.p, pl.n)
+        self._acc[plan] = acc
 
     def ks_accumulate(self, plan: int, ct_a, evk, first: bool):
         self._tick()

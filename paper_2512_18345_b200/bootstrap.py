@@ -139,9 +139,13 @@ class LinearTransform:
     unchanged (two limbs where 2^-31 relative plaintext precision is not enough)."""
 
     def __init__(self, diags: dict, params: ParameterSet, level: int, n1: int | None = None,
-                 factor: complex = 1.0, limbs: int = 1, double_hoist: bool = True, fuse_baby_steps: bool = True):
+                 factor: complex = 1.0, limbs: int = 1, double_hoist: bool = True, fuse_baby_steps: bool = True,
+                 keep_b_qp: bool = True):
         n = params.n // 2
         self.fuse_baby_steps = fuse_baby_steps
+        # moving giant steps: scale down only the a half of the inner sum, keep the b half over Q||P
+        # (False: ModDown both halves and lift the b half again, the round-1 schedule)
+        self.keep_b_qp = keep_b_qp
         self.params, self.level, self.n, self.limbs = params, level, n, limbs
         self.double_hoist = double_hoist
         offs = sorted(diags)
@@ -265,7 +269,34 @@ class LinearTransform:
                 i += len(run)
             return out
 
+        def inner_sums_a(gs):
+            """The a halves only of several giant steps' inner sums, scaled down (one batched set of
+            launches per run of up to eight adjacent accumulators); their b halves stay over Q||P.
+            Returns {g: (a over Q_l [level, n], b over Q||P [ext, n])}."""
+            out = {}
+            width = min(8, eng.lane_count())
+            i = 0
+            while i < len(gs):
+                run = [gs[i]]
+                while (len(run) < width and i + len(run) < len(gs) and
+                       qps[gs[i + len(run)]].data_ptr() == qps[run[-1]].data_ptr() + 2 * ext * n_ring * 4):
+                    run.append(gs[i + len(run)])
+                first = qps[run[0]]
+                if len(run) == 1:
+                    stack = first.unsqueeze(0)
+                else:
+                    base = first._base if first._base is not None else first
+                    at = (first.data_ptr() - base.data_ptr()) // (2 * ext * n_ring * 4)
+                    stack = base[at:at + len(run)]
+                res = eng.ks_stage3_batch_a(plan, stack, level)
+                for j, g in enumerate(run):
+                    out[g] = (res[j], qps[g][1])
+                i += len(run)
+            return out
+
         inner_sum.many = inner_sums
+        if n_ring == 65536 and self.keep_b_qp:      # the batched a-half ModDown is an N = 2^16 kernel path
+            inner_sum.many_a = inner_sums_a
         return inner_sum
 
     def rotations(self) -> set[int]:
@@ -297,7 +328,13 @@ class LinearTransform:
         # it is: no ModDown of its own
         base_raw = getattr(inner_sum, "raw", {}).get(0) if moving and p_ok(self) else None
         todo = [g for g in self.giants if not (g == 0 and base_raw is not None)]
-        if hasattr(inner_sum, "many"):
+        qp_b = hasattr(inner_sum, "many_a") and base_raw is not None and all(g != 0 for g in todo)
+        if qp_b:
+            # double hoisting in full: only the a half of a moving giant step's inner sum is scaled
+            # down (it has to be decomposed again); the b half stays over Q||P and joins the shared
+            # accumulator through the rotation as it is
+            inners = inner_sum.many_a(todo)
+        elif hasattr(inner_sum, "many"):
             inners = inner_sum.many(todo)              # batched ModDowns (adjacent accumulators)
         else:
             inners = dict(zip(todo, eng.fork([(lambda g=g: inner_sum(g)) for g in todo])))
@@ -317,8 +354,8 @@ class LinearTransform:
                 if k not in keys.galois:
                     raise RnsError(f"no Galois key for rotation {g * self.n1 * self.step}")
                 # the rotation is never materialised: gather inside the inner product, b part lifted
-                eng.ks_accumulate_rot(plan, inners[g][0], inners[g][1], k, keys.galois[k].matrix(),
-                                      first=(nth == 0))
+                acc_rot = eng.ks_accumulate_rot_qp if qp_b else eng.ks_accumulate_rot
+                acc_rot(plan, inners[g][0], inners[g][1], k, keys.galois[k].matrix(), first=(nth == 0))
 
             eng.fork([(lambda lane, nth, g=g: giant(lane, nth, g)) for g in moving], with_lane=True)
             lanes_used = min(eng.lane_count(), len(moving))

@@ -152,7 +152,7 @@ struct KsPlan {
     bool moddown_only = false;
     // row maps of batched ModDowns (ckks_ks_stage3_batch), by batch size; built on first use
     struct BatchMaps { int32_t *in_row, *pc_row, *p_slot, *conv_row, *q_slot; size_t lane_words; };
-    std::map<int, BatchMaps> s3_batch;
+    std::map<int, BatchMaps> s3_batch;            // key: count * 4 + halves
 };
 
 }  // namespace ckks
@@ -864,7 +864,7 @@ static InnerProductArgs ip_args(KsPlan* pl, const uint32_t* carry, const uint32_
     a.l = pl->l; a.alpha = pl->alpha; a.beta = pl->beta; a.ext = pl->ext; a.evk_ext = pl->evk_ext;
     a.row_lo = row_lo; a.row_hi = row_hi; a.n = pl->n;
     a.galois = 0; a.lg = log2u(pl->n); a.accumulate = 0; a.ordered = 0;
-    a.lift_a = nullptr; a.lift_b = nullptr; a.pmod = nullptr; a.pmod_s = nullptr;
+    a.lift_a = nullptr; a.lift_b = nullptr; a.pmod = nullptr; a.pmod_s = nullptr; a.lift_qp = nullptr;
     return a;
 }
 
@@ -1059,20 +1059,20 @@ int ckks_hmult_relin_rescale(ckks_ctx* ctx, int32_t ks_plan, int32_t md_plan, co
 // BSGS transform): the same five kernels as ckks_ks_stage3, each over count times the rows, instead
 // of count chains of five small launches.  Element g works in the arena of lane (current + g); qp
 // is [count][2][l + alpha][n], out [count][2][l][n].  N = 2^16, count <= 4.
-int ckks_ks_stage3_batch(ckks_ctx* ctx, int32_t plan, int count, const uint32_t* qp, uint32_t* out,
-                         void* stream) {
+static int stage3_batch_core(ckks_ctx* ctx, int32_t plan, int count, int halves, const uint32_t* qp,
+                             uint32_t* out, cudaStream_t st) {
     KsPlan* pl;
     CKS(get_plan(ctx, plan, &pl));
-    if (count < 1 || 2 * count > kMaxBconvJobs || ctx->lane + count > ctx->lanes) {
-        set_last_error("batched ModDown of %d accumulators needs that many lanes from the current one and at most %d",
-                       count, kMaxBconvJobs / 2);
+    if (count < 1 || halves * count > kMaxBconvJobs || ctx->lane + count > ctx->lanes) {
+        set_last_error("batched ModDown of %d accumulators needs that many lanes from the current one and at most %d polynomials",
+                       count, kMaxBconvJobs);
         return CKKS_ERR_ARG;
     }
     if (!ntt_can_fuse_moddown(pl->n) || ctx->ws_words % pl->n) { set_last_error("batched ModDown needs N = 2^16"); return CKKS_ERR_UNSUPPORTED; }
-    cudaStream_t st = (cudaStream_t)stream;
     const size_t n = pl->n;
     const int l = pl->l, alpha = pl->alpha, ext = pl->ext;
-    auto it = pl->s3_batch.find(count);
+    const int key = count * 4 + halves;
+    auto it = pl->s3_batch.find(key);
     if (it == pl->s3_batch.end() || it->second.lane_words != ctx->ws_words) {
         // rows of element g: accumulator at g * 2 ext (+ ext for the b half), workspace at g lanes
         const int32_t lane_rows = (int32_t)(ctx->ws_words / n);
@@ -1081,7 +1081,7 @@ int ckks_ks_stage3_batch(ckks_ctx* ctx, int32_t plan, int count, const uint32_t*
         CK(cudaMemcpy(ps.data(), pl->d_s3_p_slot, sizeof(int32_t) * 2 * alpha, cudaMemcpyDeviceToHost));
         CK(cudaMemcpy(qs.data(), pl->d_s3_q_slot, sizeof(int32_t) * 2 * l, cudaMemcpyDeviceToHost));
         for (int g = 0; g < count; ++g)
-            for (int h = 0; h < 2; ++h) {
+            for (int h = 0; h < halves; ++h) {
                 for (int j = 0; j < alpha; ++j) {
                     in_row.push_back(g * 2 * ext + h * ext + l + j);
                     pc_row.push_back(g * lane_rows + h * alpha + j);
@@ -1101,15 +1101,15 @@ int ckks_ks_stage3_batch(ckks_ctx* ctx, int32_t plan, int count, const uint32_t*
         m.lane_words = ctx->ws_words;
         for (void* ptr : {(void*)m.in_row, (void*)m.pc_row, (void*)m.p_slot, (void*)m.conv_row, (void*)m.q_slot})
             ctx->owned.push_back(ptr);
-        it = pl->s3_batch.insert_or_assign(count, m).first;
+        it = pl->s3_batch.insert_or_assign(key, m).first;
     }
     const KsPlan::BatchMaps& m = it->second;
-    CKS(ntt_launch(qp, pl->ws_pc, m.p_slot, ctx->d_slots, RowMap{m.in_row, m.pc_row}, count * 2 * alpha, pl->n, 1, st));
+    CKS(ntt_launch(qp, pl->ws_pc, m.p_slot, ctx->d_slots, RowMap{m.in_row, m.pc_row}, count * halves * alpha, pl->n, 1, st));
     BconvJobs jobs;
-    jobs.count = 2 * count;
+    jobs.count = halves * count;
     for (int g = 0; g < count; ++g)
-        for (int h = 0; h < 2; ++h) {
-            BconvJob& j = jobs.job[2 * g + h];
+        for (int h = 0; h < halves; ++h) {
+            BconvJob& j = jobs.job[halves * g + h];
             j.tab = ctx->tables[pl->moddown_table]->dev;
             j.in = pl->ws_pc + (size_t)g * ctx->ws_words + (size_t)h * alpha * n;
             j.in_stride = n;
@@ -1124,9 +1124,22 @@ int ckks_ks_stage3_batch(ckks_ctx* ctx, int32_t plan, int count, const uint32_t*
     e.q_slot = pl->d_q_slot; e.pinv = pl->d_pinv; e.pinv_s = pl->d_pinv_s;
     e.l = l; e.n = pl->n; e.galois = 0; e.lg = log2u(pl->n);
     e.xq_stride = (size_t)2 * ext * n;
-    e.out_stride = (size_t)2 * l * n;
+    e.out_stride = (size_t)halves * l * n;
+    e.halves = halves;
     return ntt_launch(pl->ws_conv, pl->ws_conv, m.q_slot, ctx->d_slots, RowMap{m.conv_row, m.conv_row},
-                      count * 2 * l, pl->n, 0, st, &e);
+                      count * halves * l, pl->n, 0, st, &e);
+}
+
+int ckks_ks_stage3_batch(ckks_ctx* ctx, int32_t plan, int count, const uint32_t* qp, uint32_t* out,
+                         void* stream) {
+    return stage3_batch_core(ctx, plan, count, 2, qp, out, (cudaStream_t)stream);
+}
+
+// The a halves only: qp is still [count][2][l + alpha][n] (the b halves are skipped), out is
+// [count][l][n].  For giant steps whose b half stays over Q||P (ckks_ks_accumulate_rot_qp).
+int ckks_ks_stage3_batch_a(ckks_ctx* ctx, int32_t plan, int count, const uint32_t* qp, uint32_t* out,
+                           void* stream) {
+    return stage3_batch_core(ctx, plan, count, 1, qp, out, (cudaStream_t)stream);
 }
 
 // ---- giant steps sharing one ModDown ---------------------------------------------------
@@ -1167,6 +1180,27 @@ int ckks_ks_accumulate_rot(ckks_ctx* ctx, int32_t plan, const uint32_t* ct_a, co
     ip.lift_b = ct_b;
     ip.pmod = pl->d_pmod;
     ip.pmod_s = pl->d_pmod_s;
+    ip.accumulate = first ? 0 : 1;
+    return inner_product_launch(ip, ctx->d_slots, st);
+}
+
+// Giant step of a double-hoisted BSGS transform whose inner sum (u_a, u_b) lives over Q||P: only
+// u_a is scaled down (ct_a = ModDown(u_a), [l][n]) and switched; u_b ([ext][n]) is added to the
+// b accumulator through the automorphism AS IT IS -- no ModDown, no lift by P, one rounding less
+// than ckks_ks_accumulate_rot on (ModDown(u_a), ModDown(u_b)).
+int ckks_ks_accumulate_rot_qp(ckks_ctx* ctx, int32_t plan, const uint32_t* ct_a, const uint32_t* b_qp,
+                              uint32_t k, const uint32_t* evk, int first, void* stream) {
+    KsPlan* pl;
+    CKS(get_plan(ctx, plan, &pl));
+    CKS(need_full_plan(pl));
+    if (!(k & 1)) { set_last_error("automorphism index must be odd"); return CKKS_ERR_ARG; }
+    cudaStream_t st = (cudaStream_t)stream;
+    const size_t n = pl->n;
+    CKS(stage1_core(ctx, pl, ct_a, pl->ws_raised, false, st));
+    InnerProductArgs ip = ip_args(pl, ct_a, pl->ws_raised, evk, 0, pl->ext, pl->ws_acc,
+                                  pl->ws_acc + (size_t)pl->ext * n);
+    ip.galois = k & (2 * pl->n - 1);
+    ip.lift_qp = b_qp;
     ip.accumulate = first ? 0 : 1;
     return inner_product_launch(ip, ctx->d_slots, st);
 }

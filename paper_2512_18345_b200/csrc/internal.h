@@ -191,6 +191,8 @@ struct InnerProductArgs {
     const uint32_t* lift_b;     // non-null: add (P mod q_i) * sigma(lift_b) to the Q rows of acc_b, i.e.
     const uint32_t* pmod;       //   fold the rotated ciphertext's b-part into the Q||P accumulator
     const uint32_t* pmod_s;     //   (double hoisting: no ModDown per rotation)
+    const uint32_t* lift_qp;    // non-null: [ext][n], already over Q||P: add sigma(lift_qp) to EVERY row of acc_b as
+                                //   it is (the b half of a giant step's inner sum never leaves Q||P)
 };
 int inner_product_launch(const InnerProductArgs& a, const ModSlot* slots, cudaStream_t st);
 
@@ -211,6 +213,9 @@ struct ModDownEpilogueArgs {
     // batched ModDown (several accumulators in one launch, rows = batch * 2 l): element g reads
     // xq_* + g * xq_stride and writes out_* + g * out_stride (words); 0 for a single ModDown
     size_t xq_stride, out_stride;
+    // 1: every element is ONE polynomial (a halves only: rows = batch * l, element g reads
+    // xq_a + g * xq_stride and writes out_a + g * out_stride); 0 or 2: both halves
+    int halves;
 };
 // All baby steps of a double-hoisted BSGS linear transform fused with all giant-step inner
 // sums: for every baby step b the Q||P accumulator u_b of the rotation sigma_{k_b} of the

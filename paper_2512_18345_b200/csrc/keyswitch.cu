@@ -170,6 +170,11 @@ inner_product_kernel(InnerProductArgs p, const ModSlot* __restrict__ slots) {
             rb[w] = add_mod(rb[w], shoup_mul(bv, pm, pms, m.q), m.q);
         }
     }
+    if (!TENS && p.lift_qp) {
+        const uint32_t* bsrc = p.lift_qp + (size_t)row * n;
+#pragma unroll
+        for (int w = 0; w < W; ++w) rb[w] = add_mod(rb[w], p.galois ? bsrc[gsrc[w]] : bsrc[i + w], m.q);
+    }
     if (!TENS && p.lift_a && row < p.l) {
         const uint32_t pm = p.pmod[row], pms = p.pmod_s[row];
         const uint32_t* asrc = p.lift_a + (size_t)row * n;

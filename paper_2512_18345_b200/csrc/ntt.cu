@@ -254,8 +254,9 @@ ntt16_fwd_contig(const uint32_t* in, uint32_t* out, const int32_t* __restrict__ 
     const ModSlot& m = slots[row_slot[blockIdx.y]];
     const uint32_t q = m.q;
     const uint32_t B = blockIdx.x * 16 + blk;          // 256-element block index within the limb
-    const int ep_row = EPI ? blockIdx.y % ep.l : 0, ep_half = EPI ? (blockIdx.y / ep.l) & 1 : 0;
-    const size_t ep_g = EPI ? blockIdx.y / (2 * ep.l) : 0;         // element of a batched ModDown
+    const bool ep_single = EPI && ep.halves == 1;
+    const int ep_row = EPI ? blockIdx.y % ep.l : 0, ep_half = (EPI && !ep_single) ? (blockIdx.y / ep.l) & 1 : 0;
+    const size_t ep_g = EPI ? blockIdx.y / ((ep_single ? 1 : 2) * ep.l) : 0;      // element of a batched ModDown
     const size_t ep_at = (size_t)ep_row * kN16 + B * 256 + 16 * e;
     pdl_trigger();
     if (EPI) {
@@ -565,8 +566,9 @@ int ntt_launch(const uint32_t* in, uint32_t* out, const int32_t* row_slot, const
         set_last_error("product-on-load needs an inverse N = 2^16 transform");
         return CKKS_ERR_ARG;
     }
-    if (epi && (inverse || !ntt_can_fuse_moddown(n) || rows % (2 * epi->l) != 0 ||
-                (rows != 2 * epi->l && (epi->fold_a || epi->fold_b)))) {
+    const int epi_unit = epi ? (epi->halves == 1 ? 1 : 2) * epi->l : 1;
+    if (epi && (inverse || !ntt_can_fuse_moddown(n) || rows % epi_unit != 0 ||
+                (rows != epi_unit && (epi->fold_a || epi->fold_b)))) {
         set_last_error("fused ModDown epilogue needs a forward N = 2^16 transform over (a multiple of) 2 l rows");
         return CKKS_ERR_ARG;
     }

@@ -385,6 +385,14 @@ class Engine:
         _lib.check(self.lib.ckks_ks_stage3_batch(self.ctx, plan, count, qps.data_ptr(), out.data_ptr(), self.stream()))
         return out
 
+    def ks_stage3_batch_a(self, plan: int, qps, l: int):
+        """ModDown of the a halves only of qps = [count, 2, ext, n] -> [count, l, n] (the b halves
+        of these giant-step inner sums stay over Q||P, see ks_accumulate_rot_qp)."""
+        count, n = qps.shape[0], qps.shape[3]
+        out = self.empty(count, l, n)
+        _lib.check(self.lib.ckks_ks_stage3_batch_a(self.ctx, plan, count, qps.data_ptr(), out.data_ptr(), self.stream()))
+        return out
+
     def ks_hoisted(self, plan: int, raised, k: int, evk, ct_b):
         """Key switch of the ciphertext rotated by X -> X^k from pre-raised digits."""
         out = self.empty(2, ct_b.shape[0], ct_b.shape[1])
@@ -450,6 +458,12 @@ class Engine:
         the rotation applied as a gather (no automorphism pass), P * sigma_k(ct_b) lifted in."""
         _lib.check(self.lib.ckks_ks_accumulate_rot(self.ctx, plan, ct_a.data_ptr(), ct_b.data_ptr(), k,
                                                    evk.data_ptr(), int(first), self.stream()))
+
+    def ks_accumulate_rot_qp(self, plan: int, ct_a, b_qp, k: int, evk, first: bool):
+        """ks_accumulate_rot for an inner sum whose b half b_qp ([ext, n]) is still over Q||P: it is
+        added to the b accumulator through the rotation as it is (no ModDown, no lift by P)."""
+        _lib.check(self.lib.ckks_ks_accumulate_rot_qp(self.ctx, plan, ct_a.data_ptr(), b_qp.data_ptr(), k,
+                                                      evk.data_ptr(), int(first), self.stream()))
 
     def ks_accumulate(self, plan: int, ct_a, evk, first: bool):
         _lib.check(self.lib.ckks_ks_accumulate(self.ctx, plan, ct_a.data_ptr(), evk.data_ptr(),

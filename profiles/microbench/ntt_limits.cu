@@ -4,9 +4,10 @@
 //             on registers (no global traffic)            -> butterflies / clk / SM vs resident CTAs
 //   memory  : the strided kernel's global access pattern only (16 column loads, 16 column stores)
 //   full    : load + compute + store, one tile per CTA (the production shape)
-// nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o ntt_limits ntt_limits.cu && ./ntt_limits
+// nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o ntt_limits ntt_limits.cu -lcuda && ./ntt_limits
 #include <cstdio>
 #include <cstdint>
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 __device__ __forceinline__ uint32_t csub(uint32_t x, uint32_t q) { return min(x, x - q); }
@@ -225,6 +226,88 @@ void run_overlap(const uint32_t* in, uint32_t* out, const uint2* tw, uint32_t q,
     cudaFree(big);
 }
 
+// TMA variant: the 256 x 16 input tile arrives with ONE cp.async.bulk.tensor.2d (box 16 x 256 of a
+// [rows * 256][256] u32 tensor) signalled on an mbarrier, instead of 16 column loads per thread.
+// T tiles per CTA, double buffered: tile t + 1 is requested before tile t is transformed.
+template <int T>
+__global__ void __launch_bounds__(256) probe_tma(const __grid_constant__ CUtensorMap tmap, uint32_t* out, const uint2* tw, uint32_t q) {
+    // the landing buffer doubles as the transpose buffer: after the first pass row j is written back at
+    // row j ^ ((j >> 4) & 1), which makes both the write (j = g + 16k) and the read (j = 16g + k) conflict-free
+    __shared__ __align__(128) uint32_t inbuf[2][256 * COLS];
+    __shared__ uint2 s_tw[256];
+    __shared__ __align__(8) uint64_t bar[2];
+    const int tid = threadIdx.x;
+    const int c = tid % COLS, g = tid / COLS;
+    for (int i = tid; i < 256; i += 256) s_tw[i] = tw[i];
+    const uint32_t bar0 = (uint32_t)__cvta_generic_to_shared(&bar[0]);
+    if (tid == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(bar0));
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(bar0 + 8));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    auto issue = [&](int t, int buf) {
+        if (tid == 0) {
+            const uint32_t dst = (uint32_t)__cvta_generic_to_shared(&inbuf[buf][0]);
+            const int c0 = (blockIdx.x * T + t) * COLS, c1 = blockIdx.y * 256;
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(bar0 + 8 * buf), "r"(256 * COLS * 4) : "memory");
+            asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
+                         :: "r"(dst), "l"(&tmap), "r"(c0), "r"(c1), "r"(bar0 + 8 * buf) : "memory");
+        }
+    };
+    issue(0, 0);
+#pragma unroll 1
+    for (int t = 0; t < T; ++t) {
+        if (t + 1 < T) issue(t + 1, (t + 1) & 1);
+        const uint32_t b = bar0 + 8 * (t & 1), parity = (t >> 1) & 1;
+        asm volatile("{\n .reg .pred p;\n WAIT:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @p bra DONE;\n bra WAIT;\n DONE:\n}" :: "r"(b), "r"(parity) : "memory");
+        uint32_t v[16];
+#pragma unroll
+        for (int k = 0; k < 16; ++k) v[k] = inbuf[t & 1][(g + 16 * k) * COLS + c];
+        __syncthreads();       // all inputs are in registers before anyone writes back
+        ct16(v, q, TW_MUL(s_tw[(1 << s) + gi]));
+        uint32_t* tile = inbuf[t & 1];
+#pragma unroll
+        for (int k = 0; k < 16; ++k) tile[((g ^ (k & 1)) + 16 * k) * COLS + c] = v[k];
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < 16; ++k) v[k] = tile[(16 * g + (k ^ (g & 1))) * COLS + c];
+        ct16(v, q, TW_MUL(s_tw[(16 << s) + (g << s) + gi]));
+        uint32_t* dst = out + (size_t)blockIdx.y * kN + (blockIdx.x * T + t) * COLS + c;
+#pragma unroll
+        for (int k = 0; k < 16; ++k) dst[(16 * g + k) * 256] = csub(v[k], q);
+        __syncthreads();       // everyone is done with inbuf[t & 1] before it is refilled
+    }
+}
+
+template <int T>
+void run_tma(const uint32_t* in, uint32_t* out, const uint2* tw, uint32_t q, int rows_buf, int sms, int clk_khz) {
+    cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
+    for (int r : {24, 48, 96, 192, 384}) {
+        float best = 1e9, ms;
+        for (int rep = 0; rep < 5; ++rep) {
+            const uint32_t* src = in + (size_t)(rep & 1) * rows_buf * kN * (r <= 192);
+            CUtensorMap tmap;
+            cuuint64_t dims[2] = {256, (cuuint64_t)r * 256};
+            cuuint64_t strides[1] = {256 * 4};
+            cuuint32_t box[2] = {COLS, 256};
+            cuuint32_t estr[2] = {1, 1};
+            CUresult rc = cuTensorMapEncodeTiled(&tmap, CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, (void*)src, dims, strides, box, estr,
+                                                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                                 CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+            if (rc != CUDA_SUCCESS) { printf("cuTensorMapEncodeTiled failed: %d\n", (int)rc); return; }
+            dim3 grid(256 / COLS / T, r);
+            cudaEventRecord(a);
+            probe_tma<T><<<grid, 256>>>(tmap, out, tw, q);
+            cudaEventRecord(b); cudaEventSynchronize(b); cudaEventElapsedTime(&ms, a, b);
+            if (ms < best) best = ms;
+        }
+        const double bf = (double)r * 32768 * 8;
+        printf("tma  T=%d rows=%3d: %7.2f us  %6.0f GB/s (r+w)  %5.2f butterflies/clk/SM (%s)\n", T, r, best * 1e3,
+               2.0 * r * kN * 4 / (best * 1e-3) / 1e9, bf / (best * 1e-3) / sms / (clk_khz * 1e3), cudaGetErrorString(cudaGetLastError()));
+    }
+}
+
 int main() {
     cudaDeviceProp p; cudaGetDeviceProperties(&p, 0);
     const int sms = p.multiProcessorCount;
@@ -273,6 +356,9 @@ int main() {
                    best * 1e3, 2.0 * r * kN * 4 / (best * 1e-3) / 1e9, mode == 0 ? bf / (best * 1e-3) / sms / (clk_khz * 1e3) : 0.0);
         }
     }
+    run_tma<1>(in, out, tw, q, rows, sms, clk_khz);
+    run_tma<2>(in, out, tw, q, rows, sms, clk_khz);
+    run_tma<4>(in, out, tw, q, rows, sms, clk_khz);
     run_overlap(in, out, tw, q, sms);
     for (unsigned delay : {0u, 1000u})
         for (int r : {96, 192, 384}) {

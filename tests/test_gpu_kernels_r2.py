@@ -107,3 +107,46 @@ def test_twiddle_corruption_is_detected(env, n):
     # the corruption lives in its own slot: the engine's resident tables are untouched
     again = T.build_twiddle_table(m, n)
     assert np.array_equal(again.fwd, good.fwd)
+
+
+# ---------------------------------------------------------------- giant steps with the b half over Q||P
+@pytest.mark.parametrize("l,count", [(48, 4), (42, 3), (21, 1), (19, 5)])
+def test_giant_steps_with_b_half_over_qp_match_oracle(env, l, count):
+    """ks_stage3_batch_a (ModDown of the a halves of several Q||P accumulators in one set of launches,
+    keyswitch.py:387-419 per polynomial) and ks_accumulate_rot_qp (stage 1-2 of the key switch of
+    sigma_k(a), keyswitch.py:297-355, plus sigma_k of a b half that stays over Q||P) followed by the
+    shared ModDown: the CUDA engine and the oracle engine run the same calls on the same inputs."""
+    import recipes as R
+    from oracle.engine_oracle import OracleEngine
+
+    eng, p = env.eng, env.ks48
+    eng.set_lanes(8)
+    try:
+        qs = [m.q for m in p.ext_basis]
+        evks = [np.stack([np.stack([R.level_key_rows(qs, p.n, t, h) for h in range(2)]) for t in range(p.dnum)])
+                .astype(np.uint32) for _ in range(1)]
+        q = p.q_basis[:l]
+        ext = l + p.alpha
+        ext_qs = [m.q for m in q + p.p_basis]
+        rng = np.random.default_rng(100 * l + count)
+        qps = np.stack([np.stack([np.stack([rng.integers(0, m, p.n, dtype=np.uint64) for m in ext_qs]) for _ in range(2)])
+                        for _ in range(count)]).astype(np.uint32)
+        ks_idx = [5, 2 * p.n - 1, 25, 3, 125][:count]
+        words = lambda t: t.cpu().numpy().view(np.uint32)
+
+        def run(e):
+            plan = e.ks_plan(p.n, q, p.p_basis, p.alpha, p.l + p.alpha, p.l)
+            t_qps = e.upload(qps.reshape(-1, p.n)).reshape(count, 2, ext, p.n)
+            evk = e.upload(evks[0].reshape(-1, p.n)).reshape(evks[0].shape)
+            a_md = e.ks_stage3_batch_a(plan, t_qps, l)
+            for g in range(count):
+                e.ks_accumulate_rot_qp(plan, a_md[g], t_qps[g][1], ks_idx[g], evk, first=(g == 0))
+            out = e.ks_finish(plan, 1, None, None, l, p.n)
+            return words(a_md).copy(), words(out).copy()
+
+        got_md, got_out = run(eng)
+        want_md, want_out = run(OracleEngine())
+        assert np.array_equal(got_md, want_md), "batched ModDown of the a halves differs from the oracle"
+        assert np.array_equal(got_out, want_out), "accumulated giant steps differ from the oracle"
+    finally:
+        eng.set_lanes(1)
