@@ -35,20 +35,24 @@ __device__ __forceinline__ void ct16(uint32_t (&v)[16], uint32_t q, MUL mul) {
 }
 #define TW_MUL(expr) [&](int s, int gi, uint32_t y) { const uint2 w = (expr); return shoup_mul(y, w.x, w.y, q); }
 
-constexpr int COLS = 16;
+#ifndef NCOLS
+#define NCOLS 16
+#endif
+constexpr int COLS = NCOLS;          // -DNCOLS=32: 128-byte row segments, 512-thread CTAs (probe<> only)
+constexpr int THREADS = 16 * COLS;
 constexpr int kN = 65536;
 
-// MODE 0: full, 1: compute only (ITERS tiles on registers), 2: memory only
+// MODE 0: full, 1: compute only (ITERS tiles on registers), 2: memory only, 3: loads + compute, 4: compute + stores
 template <int MODE>
-__global__ void __launch_bounds__(256) probe(const uint32_t* in, uint32_t* out, const uint2* tw, uint32_t q, int iters) {
+__global__ void __launch_bounds__(THREADS) probe(const uint32_t* in, uint32_t* out, const uint2* tw, uint32_t q, int iters) {
     __shared__ uint2 s_tw[256];
     __shared__ uint32_t tile[271 * COLS];
     const int tid = threadIdx.x;
     const int c = tid % COLS, g = tid / COLS;
-    for (int i = tid; i < 256; i += 256) s_tw[i] = tw[i];
+    for (int i = tid; i < 256; i += THREADS) s_tw[i] = tw[i];
     const size_t base = (size_t)blockIdx.y * kN + blockIdx.x * COLS + c;
     uint32_t v[16];
-    if (MODE == 1) {
+    if (MODE == 1 || MODE == 4) {
 #pragma unroll
         for (int k = 0; k < 16; ++k) v[k] = tid * 16 + k + blockIdx.x;
     } else {
@@ -68,7 +72,7 @@ __global__ void __launch_bounds__(256) probe(const uint32_t* in, uint32_t* out, 
             if (MODE == 1) __syncthreads();
         }
     }
-    if (MODE == 1) {
+    if (MODE == 1 || MODE == 3) {
         uint32_t acc = 0;
 #pragma unroll
         for (int k = 0; k < 16; ++k) acc ^= v[k];
@@ -82,6 +86,7 @@ __global__ void __launch_bounds__(256) probe(const uint32_t* in, uint32_t* out, 
 // Pipelined variant: a CTA walks T consecutive tiles of one limb; tile i+1 is fetched with
 // cp.async (16-byte chunks, no register staging) into the other half of a double buffer while
 // tile i is transformed; the twiddles of the limb are staged once.
+#if NCOLS == 16
 template <int T>
 __global__ void __launch_bounds__(256) probe_pipe(const uint32_t* in, uint32_t* out, const uint2* tw, uint32_t q) {
     __shared__ uint2 s_tw[256];
@@ -207,7 +212,7 @@ void run_overlap(const uint32_t* in, uint32_t* out, const uint2* tw, uint32_t q,
         const float t_stream = ms;
         // alone: transforms
         cudaEventRecord(a, s2);
-        for (int r = 0; r < reps; ++r) probe<0><<<grid, 256, 0, s2>>>(in + (size_t)(r & 1) * 192 * kN, out + 64, tw, q, 1);
+        for (int r = 0; r < reps; ++r) probe<0><<<grid, THREADS, 0, s2>>>(in + (size_t)(r & 1) * 192 * kN, out + 64, tw, q, 1);
         cudaEventRecord(b, s2); cudaEventSynchronize(b); cudaEventElapsedTime(&ms, a, b);
         const float t_ntt = ms;
         // both
@@ -215,7 +220,7 @@ void run_overlap(const uint32_t* in, uint32_t* out, const uint2* tw, uint32_t q,
         cudaEventRecord(a, s1);
         cudaStreamWaitEvent(s2, a, 0);
         stream_read<<<sms * per_sm, 256, 0, s1>>>(big, big_bytes / 16, out);
-        for (int r = 0; r < reps; ++r) probe<0><<<grid, 256, 0, s2>>>(in + (size_t)(r & 1) * 192 * kN, out + 64, tw, q, 1);
+        for (int r = 0; r < reps; ++r) probe<0><<<grid, THREADS, 0, s2>>>(in + (size_t)(r & 1) * 192 * kN, out + 64, tw, q, 1);
         cudaEventRecord(e2, s2);
         cudaStreamWaitEvent(s1, e2, 0);
         cudaEventRecord(b, s1); cudaEventSynchronize(b); cudaEventElapsedTime(&ms, a, b);
@@ -308,6 +313,8 @@ void run_tma(const uint32_t* in, uint32_t* out, const uint2* tw, uint32_t q, int
     }
 }
 
+#endif  // NCOLS == 16
+
 int main() {
     cudaDeviceProp p; cudaGetDeviceProperties(&p, 0);
     const int sms = p.multiProcessorCount;
@@ -330,13 +337,13 @@ int main() {
         if (pad > 200 * 1024) pad = 200 * 1024;
         cudaFuncSetAttribute(probe<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pad);
         dim3 grid(sms * per_sm, 1);
-        probe<1><<<grid, 256, pad>>>(in, out, tw, q, iters);
+        probe<1><<<grid, THREADS, pad>>>(in, out, tw, q, iters);
         cudaDeviceSynchronize();
         cudaEventRecord(a);
-        probe<1><<<grid, 256, pad>>>(in, out, tw, q, iters);
+        probe<1><<<grid, THREADS, pad>>>(in, out, tw, q, iters);
         cudaEventRecord(b); cudaEventSynchronize(b); cudaEventElapsedTime(&ms, a, b);
-        const double bf = (double)grid.x * 256 * 64 * iters;
-        printf("compute-only  %d CTA/SM (%2d warps/SM): %7.3f ms  %5.2f butterflies/clk/SM  (%s)\n", per_sm, per_sm * 8, ms,
+        const double bf = (double)grid.x * THREADS * 64 * iters;
+        printf("compute-only  %d CTA/SM (%2d warps/SM): %7.3f ms  %5.2f butterflies/clk/SM  (%s)\n", per_sm, per_sm * THREADS / 32, ms,
                bf / (ms * 1e-3) / sms / (clk_khz * 1e3), cudaGetErrorString(cudaGetLastError()));
     }
     for (int r : {24, 48, 96, 192, 384}) {
@@ -346,8 +353,8 @@ int main() {
             for (int rep = 0; rep < 5; ++rep) {
                 const uint32_t* src = in + (size_t)(rep & 1) * rows * kN * (r <= 192);
                 cudaEventRecord(a);
-                if (mode == 0) probe<0><<<grid, 256>>>(src, out, tw, q, 1);
-                else probe<2><<<grid, 256>>>(src, out, tw, q, 1);
+                if (mode == 0) probe<0><<<grid, THREADS>>>(src, out, tw, q, 1);
+                else probe<2><<<grid, THREADS>>>(src, out, tw, q, 1);
                 cudaEventRecord(b); cudaEventSynchronize(b); cudaEventElapsedTime(&ms, a, b);
                 if (ms < best) best = ms;
             }
@@ -356,6 +363,36 @@ int main() {
                    best * 1e3, 2.0 * r * kN * 4 / (best * 1e-3) / 1e9, mode == 0 ? bf / (best * 1e-3) / sms / (clk_khz * 1e3) : 0.0);
         }
     }
+    for (int mode = 3; mode <= 4; ++mode)
+        for (int r : {192, 384}) {
+            dim3 grid(256 / COLS, r);
+            float best = 1e9;
+            for (int rep = 0; rep < 5; ++rep) {
+                const uint32_t* src = in + (size_t)(rep & 1) * rows * kN * (r <= 192);
+                cudaEventRecord(a);
+                if (mode == 3) probe<3><<<grid, THREADS>>>(src, out, tw, q, 1);
+                else probe<4><<<grid, THREADS>>>(src, out, tw, q, 1);
+                cudaEventRecord(b); cudaEventSynchronize(b); cudaEventElapsedTime(&ms, a, b);
+                if (ms < best) best = ms;
+            }
+            printf("%s rows=%3d: %7.2f us  %5.2f butterflies/clk/SM\n", mode == 3 ? "loads + compute " : "compute + stores", r, best * 1e3,
+                   (double)r * 32768 * 8 / (best * 1e-3) / sms / (clk_khz * 1e3));
+        }
+    for (int per_sm : {2, 3, 4, 6, 8}) {
+        size_t pad = per_sm >= 8 ? 0 : (size_t)(227 * 1024 / per_sm) - 21 * 1024;
+        cudaFuncSetAttribute(probe<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pad);
+        dim3 grid(256 / COLS, 384);
+        float best = 1e9;
+        for (int rep = 0; rep < 5; ++rep) {
+            cudaEventRecord(a);
+            probe<0><<<grid, THREADS, pad>>>(in, out, tw, q, 1);
+            cudaEventRecord(b); cudaEventSynchronize(b); cudaEventElapsedTime(&ms, a, b);
+            if (ms < best) best = ms;
+        }
+        printf("full rows=384 at most %d CTA/SM: %7.2f us  %5.2f butterflies/clk/SM\n", per_sm, best * 1e3,
+               (double)384 * 32768 * 8 / (best * 1e-3) / sms / (clk_khz * 1e3));
+    }
+#if NCOLS == 16
     run_tma<1>(in, out, tw, q, rows, sms, clk_khz);
     run_tma<2>(in, out, tw, q, rows, sms, clk_khz);
     run_tma<4>(in, out, tw, q, rows, sms, clk_khz);
@@ -376,5 +413,6 @@ int main() {
         }
     run_pipe<2>(in, out, tw, q, rows, sms, clk_khz);
     run_pipe<4>(in, out, tw, q, rows, sms, clk_khz);
+#endif
     return 0;
 }
