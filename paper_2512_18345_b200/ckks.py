@@ -621,3 +621,51 @@ def mul_const(ct: Ciphertext, value: float, params: ParameterSet, out_scale: flo
     pt = encode_constant(value, params, level, out_scale * dropped / ct.scale)
     out = rescale(mul_plain(ct, pt), drop)
     return Ciphertext(a=out.a, b=out.b, scale=out_scale)
+
+
+def capture(fn, *sample_cts: Ciphertext):
+    """Record `fn(*ciphertexts) -> ciphertext` (any composition of the operations above: key
+    switches, HMult + relinearise + rescale chains, rotations) into ONE CUDA graph and return
+    replay(*ciphertexts) -> ciphertext with the same result limbs as the eager call.  The
+    launch overhead of a many-kernel circuit is what capture removes (SURVEY
+    section 7 step 8): at N = 2^13 (BASELINE config 1) an HMult + relinearise + rescale is ~15
+    launches of a few microseconds each.  Operands must keep the sample's level, basis and scale.
+    Like Bootstrapper.capture, the graph holds pointers into the key-switch workspace arena: a
+    replay after the arena moved raises."""
+    import torch
+
+    from .engine import get_engine
+
+    eng = get_engine()
+    statics = [torch.stack([c.a.data, c.b.data]).clone() for c in sample_cts]
+    views = [ct_from_tensor(t, c.a.basis, c.scale) for t, c in zip(statics, sample_cts)]
+    fn(*views)                                             # warm-up: plans, tables, constants
+    torch.cuda.synchronize()
+    graph = torch.cuda.CUDAGraph()
+    side = torch.cuda.Stream(device=eng.device)
+    side.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(side):
+        fn(*views)                                         # settle allocator state on the capture stream
+        torch.cuda.synchronize()
+        with torch.cuda.graph(graph, stream=side):
+            out = fn(*views)
+            static_out = ct_tensor(out)
+    torch.cuda.current_stream().wait_stream(side)
+    out_basis, out_scale = out.a.basis, out.scale
+    generation = eng.arena_generation()
+
+    def replay(*cts: Ciphertext, copy_out: bool = True) -> Ciphertext:
+        if eng.arena_generation() != generation:
+            raise RnsError("the workspace arena was reallocated after this graph was captured: capture again")
+        if len(cts) != len(statics):
+            raise StructureError(f"captured with {len(statics)} operands, called with {len(cts)}")
+        for t, c, s in zip(statics, cts, sample_cts):
+            if c.a.basis != s.a.basis or not _close(c.scale, s.scale):
+                raise StructureError("operand level / basis / scale differs from the captured sample")
+            t[0].copy_(c.a.data, non_blocking=True)
+            t[1].copy_(c.b.data, non_blocking=True)
+        graph.replay()
+        return ct_from_tensor(static_out.clone() if copy_out else static_out, out_basis, out_scale)
+
+    replay.graph, replay.static_in, replay.static_out = graph, statics, static_out
+    return replay

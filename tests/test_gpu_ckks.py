@@ -151,3 +151,28 @@ def test_slotwise_semantics_rotation_conjugation_mult(env):
     assert np.abs(ck.decrypt_decode(half, sk, p) - 0.5 * z1).max() < tol
     with pytest.raises(env.rns.RnsError):
         ck.add(ct1, prod if ck.level_of(prod) == ck.level_of(ct1) else ck.Ciphertext(ct1.a, ct1.b, 3.0))
+
+
+def test_captured_product_equals_eager(golden):
+    """ckks.capture: HMult + relinearise + rescale at BASELINE config 1 (N = 2^13) recorded as one
+    CUDA graph gives the limbs of the eager call, for the captured sample and for fresh operands."""
+    import torch
+
+    from paper_2512_18345_b200 import ckks, keyswitch as ks
+    from paper_2512_18345_b200.params import generate_parameter_set
+
+    p = generate_parameter_set(n=8192, l=12, dnum=3, delta=1 << 40, h_dense=64, h_sparse=32)
+    sk = ks.keygen(p, seed=1)
+    rlk = ckks.relin_keygen(sk, p, seed=41)
+    msgs = [np.random.default_rng(7 + i).integers(1, 9, p.n).astype(np.int64) << 20 for i in range(4)]
+    cts = [ks.encrypt(m, sk, p, seed=2 + 3 * i) for i, m in enumerate(msgs)]
+    product = lambda a, b: ckks.rescale(ckks.hmult(a, b, rlk), 1)
+    replay = ckks.capture(product, cts[0], cts[1])
+    for a, b in ((cts[0], cts[1]), (cts[2], cts[3]), (cts[1], cts[2])):
+        want = product(a, b)
+        got = replay(a, b)
+        torch.cuda.synchronize()
+        assert np.array_equal(got.a.coeffs, want.a.coeffs) and np.array_equal(got.b.coeffs, want.b.coeffs)
+        assert got.scale == want.scale and got.a.basis == want.a.basis
+    with pytest.raises(Exception):
+        replay(ckks.mod_drop(cts[0], 6), ckks.mod_drop(cts[1], 6))
