@@ -150,3 +150,41 @@ def test_giant_steps_with_b_half_over_qp_match_oracle(env, l, count):
         assert np.array_equal(got_out, want_out), "accumulated giant steps differ from the oracle"
     finally:
         eng.set_lanes(1)
+
+
+# ---------------------------------------------------------------- BSGS kernels against the oracle engine
+@pytest.mark.parametrize("level", [42, 21])
+def test_bsgs_inner_matches_oracle_engine(env, level):
+    """The fused baby-step + inner-sum kernel (hoisted rotations + BSGS) against the
+    CPU restatement (OracleEngine.bsgs_inner = keyswitch.py:318-332 per rotation through rns.py:268-292's
+    permutation, then rns.py:243-258 products): Q||P accumulators bit for bit, including an absent
+    diagonal and the unrotated term."""
+    from oracle.engine_oracle import OracleEngine
+    from paper_2512_18345_b200 import ckks
+
+    p = env.ks48
+    basis = p.q_basis[:level]
+    ext = level + p.alpha
+    ext_basis = basis + p.p_basis
+    rng = np.random.default_rng(level)
+    rows = lambda mods: np.stack([rng.integers(0, m.q, p.n, dtype=np.uint64) for m in mods]).astype(np.uint32)
+    a_h, b_h = rows(basis), rows(basis)
+    rots = [0, 1, 3]
+    ks_idx = [0 if r == 0 else ckks.galois_element(r, p.n) for r in rots]
+    evk_h = [None if r == 0 else np.stack([np.stack([rows(p.ext_basis) for _ in range(2)]) for _ in range(p.dnum)])
+             for r in rots]
+    ng = 2
+    table_h = [[None if (g, b) == (1, 2) else rows(ext_basis) for b in range(len(rots))] for g in range(ng)]
+
+    def run(e):
+        plan = e.ks_plan(p.n, basis, p.p_basis, p.alpha, p.l + p.alpha, p.l)
+        ct_a, ct_b = e.upload(a_h), e.upload(b_h)
+        raised = e.ks_stage1(plan, ct_a, -(-level // p.alpha), ext)
+        evks = [None if k is None else e.upload(k.reshape(-1, p.n)).reshape(k.shape) for k in evk_h]
+        table = [[None if t is None else e.upload(t) for t in row] for row in table_h]
+        out = e.bsgs_inner(plan, raised, ct_a, ct_b, ks_idx, evks, table, ext)
+        return [o.cpu().numpy().view(np.uint32).copy() for o in out]
+
+    got, want = run(env.eng), run(OracleEngine())
+    for g in range(ng):
+        assert np.array_equal(got[g], want[g]), g
