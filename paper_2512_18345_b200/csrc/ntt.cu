@@ -244,7 +244,7 @@ __device__ __forceinline__ void load_tw15(const uint2* __restrict__ tab, uint32_
 // halves, and the kernel stores (x_Q - conv) * P^-1 (+ fold) straight into the result, so conv
 // is never written or re-read.
 template <bool EPI>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, EPI ? 5 : 6)
 ntt16_fwd_contig(const uint32_t* in, uint32_t* out, const int32_t* __restrict__ row_slot,
                  const ModSlot* __restrict__ slots, RowMap rm, ModDownEpilogueArgs ep) {
     __shared__ uint32_t tile[16 * 272];
