@@ -8,6 +8,7 @@
 //
 // Stage 3 epilogue (keyswitch.py:412-418, :452): out = (x_Q - conv) * P^-1,
 // with the ciphertext b-part folded into the b half in the same pass.
+#include <cstdlib>
 #include "common.cuh"
 #include "internal.h"
 
@@ -17,10 +18,30 @@ __device__ __forceinline__ uint64_t mad64(uint32_t a, uint32_t b, uint64_t c) {
     return (uint64_t)a * b + c;
 }
 
+// W consecutive words (W = 1, 2, 4) as one access
+template <int W>
+__device__ __forceinline__ void ldw(const uint32_t* p, uint32_t (&v)[W]) {
+    if (W == 4) { const uint4 t = *reinterpret_cast<const uint4*>(p); v[0] = t.x; v[W > 1 ? 1 : 0] = t.y; v[W > 2 ? 2 : 0] = t.z; v[W > 3 ? 3 : 0] = t.w; }
+    else if (W == 2) { const uint2 t = *reinterpret_cast<const uint2*>(p); v[0] = t.x; v[W > 1 ? 1 : 0] = t.y; }
+    else v[0] = p[0];
+}
+template <int W>
+__device__ __forceinline__ void ldw_stream(const uint32_t* p, uint64_t pol, uint32_t (&v)[W]) {
+    if (W == 4) { const uint4 t = ld_stream(reinterpret_cast<const uint4*>(p), pol); v[0] = t.x; v[W > 1 ? 1 : 0] = t.y; v[W > 2 ? 2 : 0] = t.z; v[W > 3 ? 3 : 0] = t.w; }
+    else if (W == 2) { const uint2 t = ld_stream2(reinterpret_cast<const uint2*>(p), pol); v[0] = t.x; v[W > 1 ? 1 : 0] = t.y; }
+    else v[0] = p[0];
+}
+template <int W>
+__device__ __forceinline__ void stw(uint32_t* p, const uint32_t (&v)[W]) {
+    if (W == 4) *reinterpret_cast<uint4*>(p) = make_uint4(v[0], v[W > 1 ? 1 : 0], v[W > 2 ? 2 : 0], v[W > 3 ? 3 : 0]);
+    else if (W == 2) *reinterpret_cast<uint2*>(p) = make_uint2(v[0], v[W > 1 ? 1 : 0]);
+    else p[0] = v[0];
+}
+
 // BETA > 0: digit count known at compile time -- the loop is unrolled and all 3 * BETA
 // 16-byte loads of a thread are issued before the first product, which is what keeps
 // enough bytes in flight per SM to stream the key at HBM speed.  BETA = 0: runtime count.
-template <bool VEC, int BETA, bool TENS>
+template <int W, int BETA, bool TENS>
 __global__ void __launch_bounds__(256)
 inner_product_kernel(InnerProductArgs p, const ModSlot* __restrict__ slots) {
     const int row = p.row_lo + blockIdx.y;
@@ -28,7 +49,6 @@ inner_product_kernel(InnerProductArgs p, const ModSlot* __restrict__ slots) {
     const size_t n = p.n;
     const int digit_of_row = row < p.l ? row / p.alpha : -1;
     const size_t erow = (size_t)p.evk_row[row];
-    constexpr int W = VEC ? 4 : 1;
     const size_t i = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) * W;
     if (i >= n) return;
     const int beta = BETA > 0 ? BETA : p.beta;
@@ -65,29 +85,15 @@ inner_product_kernel(InnerProductArgs p, const ModSlot* __restrict__ slots) {
                                        : p.raised + ((size_t)t * p.ext + row) * n;
             const uint32_t* ka = p.evk + (((size_t)t * 2 + 0) * p.evk_ext + erow) * n;
             const uint32_t* kb = p.evk + (((size_t)t * 2 + 1) * p.evk_ext + erow) * n;
-            if (VEC) {
-                const uint4 av = ld_stream(reinterpret_cast<const uint4*>(ka + i), pol);
-                const uint4 bv = ld_stream(reinterpret_cast<const uint4*>(kb + i), pol);
-                xa[c][0] = av.x; xa[c][W > 1 ? 1 : 0] = av.y; xa[c][W > 2 ? 2 : 0] = av.z; xa[c][W > 3 ? 3 : 0] = av.w;
-                xb[c][0] = bv.x; xb[c][W > 1 ? 1 : 0] = bv.y; xb[c][W > 2 ? 2 : 0] = bv.z; xb[c][W > 3 ? 3 : 0] = bv.w;
-            } else {
-                xa[c][0] = ka[i]; xb[c][0] = kb[i];
-            }
+            ldw_stream<W>(ka + i, pol, xa[c]);
+            ldw_stream<W>(kb + i, pol, xb[c]);
         }
         if (BETA > 0) pdl_wait();
         if (tens && t0 == 0) {
             const size_t at = (size_t)row * n + i;
             uint32_t XA[W], XB[W], YA[W], YB[W];
-            if (VEC) {
-                const uint4 a1 = *reinterpret_cast<const uint4*>(p.tx_a + at), b1 = *reinterpret_cast<const uint4*>(p.tx_b + at);
-                const uint4 a2 = *reinterpret_cast<const uint4*>(p.ty_a + at), b2 = *reinterpret_cast<const uint4*>(p.ty_b + at);
-                XA[0] = a1.x; XA[W > 1 ? 1 : 0] = a1.y; XA[W > 2 ? 2 : 0] = a1.z; XA[W > 3 ? 3 : 0] = a1.w;
-                XB[0] = b1.x; XB[W > 1 ? 1 : 0] = b1.y; XB[W > 2 ? 2 : 0] = b1.z; XB[W > 3 ? 3 : 0] = b1.w;
-                YA[0] = a2.x; YA[W > 1 ? 1 : 0] = a2.y; YA[W > 2 ? 2 : 0] = a2.z; YA[W > 3 ? 3 : 0] = a2.w;
-                YB[0] = b2.x; YB[W > 1 ? 1 : 0] = b2.y; YB[W > 2 ? 2 : 0] = b2.z; YB[W > 3 ? 3 : 0] = b2.w;
-            } else {
-                XA[0] = p.tx_a[at]; XB[0] = p.tx_b[at]; YA[0] = p.ty_a[at]; YB[0] = p.ty_b[at];
-            }
+            ldw<W>(p.tx_a + at, XA); ldw<W>(p.tx_b + at, XB);
+            ldw<W>(p.ty_a + at, YA); ldw<W>(p.ty_b + at, YB);
 #pragma unroll
             for (int w = 0; w < W; ++w) {
                 own[w] = mul_mod(XA[w], YA[w], m);
@@ -108,18 +114,13 @@ inner_product_kernel(InnerProductArgs p, const ModSlot* __restrict__ slots) {
             const uint32_t* dsrc = (p.carry && t == digit_of_row)
                                        ? p.carry + (size_t)row * n
                                        : p.raised + ((size_t)t * p.ext + row) * n;
-            if (VEC) {
-                if (p.galois) {
-                    // hoisted rotation: the raised digit is read through the automorphism
-                    // (sigma_k commutes with ModUp up to a multiple of the digit modulus)
+            if (p.galois) {
+                // hoisted rotation: the raised digit is read through the automorphism
+                // (sigma_k commutes with ModUp up to a multiple of the digit modulus)
 #pragma unroll
-                    for (int w = 0; w < W; ++w) d[c][w] = dsrc[gsrc[w]];
-                } else {
-                    const uint4 dv = *reinterpret_cast<const uint4*>(dsrc + i);
-                    d[c][0] = dv.x; d[c][W > 1 ? 1 : 0] = dv.y; d[c][W > 2 ? 2 : 0] = dv.z; d[c][W > 3 ? 3 : 0] = dv.w;
-                }
+                for (int w = 0; w < W; ++w) d[c][w] = dsrc[gsrc[w]];
             } else {
-                d[c][0] = p.galois ? dsrc[gsrc[0]] : dsrc[i];
+                ldw<W>(dsrc + i, d[c]);
             }
         }
         if (m.fast) {
@@ -188,38 +189,39 @@ inner_product_kernel(InnerProductArgs p, const ModSlot* __restrict__ slots) {
             rb[w] = add_mod(rb[w], ob[w], m.q);
         }
     }
-    if (VEC) {
-        *reinterpret_cast<uint4*>(oa) = make_uint4(ra[0], ra[W > 1 ? 1 : 0], ra[W > 2 ? 2 : 0], ra[W > 3 ? 3 : 0]);
-        *reinterpret_cast<uint4*>(ob) = make_uint4(rb[0], rb[W > 1 ? 1 : 0], rb[W > 2 ? 2 : 0], rb[W > 3 ? 3 : 0]);
-    } else {
-        oa[0] = ra[0];
-        ob[0] = rb[0];
-    }
+    stw<W>(oa, ra);
+    stw<W>(ob, rb);
 }
 
 template <int BETA>
-static cudaError_t inner_product_dispatch(const InnerProductArgs& a, const ModSlot* slots, dim3 grid, bool vec, cudaStream_t st) {
+static cudaError_t inner_product_dispatch(const InnerProductArgs& a, const ModSlot* slots, int width, cudaStream_t st) {
     const bool tens = a.tx_a != nullptr;
     const bool pdl = !a.ordered;
-    if (vec && tens) return launch_opt_pdl(pdl, inner_product_kernel<true, BETA, true>, grid, dim3(256), 0, st, a, slots);
-    if (vec) return launch_opt_pdl(pdl, inner_product_kernel<true, BETA, false>, grid, dim3(256), 0, st, a, slots);
-    if (tens) return launch_opt_pdl(pdl, inner_product_kernel<false, BETA, true>, grid, dim3(256), 0, st, a, slots);
-    return launch_opt_pdl(pdl, inner_product_kernel<false, BETA, false>, grid, dim3(256), 0, st, a, slots);
+    const size_t work = a.n / width;
+    dim3 grid((unsigned)((work + 255) / 256), a.row_hi - a.row_lo);
+    if (width == 4 && tens) return launch_opt_pdl(pdl, inner_product_kernel<4, BETA, true>, grid, dim3(256), 0, st, a, slots);
+    if (width == 4) return launch_opt_pdl(pdl, inner_product_kernel<4, BETA, false>, grid, dim3(256), 0, st, a, slots);
+    if (width == 2 && tens) return launch_opt_pdl(pdl, inner_product_kernel<2, BETA, true>, grid, dim3(256), 0, st, a, slots);
+    if (width == 2) return launch_opt_pdl(pdl, inner_product_kernel<2, BETA, false>, grid, dim3(256), 0, st, a, slots);
+    if (tens) return launch_opt_pdl(pdl, inner_product_kernel<1, BETA, true>, grid, dim3(256), 0, st, a, slots);
+    return launch_opt_pdl(pdl, inner_product_kernel<1, BETA, false>, grid, dim3(256), 0, st, a, slots);
 }
 
 int inner_product_launch(const InnerProductArgs& a, const ModSlot* slots, cudaStream_t st) {
     const int rows = a.row_hi - a.row_lo;
     if (rows <= 0) return CKKS_OK;
-    const bool vec = a.n % 4 == 0;
-    const size_t work = vec ? a.n / 4 : a.n;
-    dim3 grid((unsigned)((work + 255) / 256), rows);
+    // words per thread: 4 (16-byte accesses) by default; CKKS_IP_W=2 halves the per-thread footprint
+    // (registers, bytes in flight) for twice the threads
+    static const int pref = [] { const char* e = getenv("CKKS_IP_W"); return e ? atoi(e) : 4; }();
+    int width = a.n % 4 == 0 ? 4 : 1;
+    if (pref == 2 && a.n % 2 == 0) width = 2;
     ProfScope ps("inner_product", st, 4.0 * a.n * rows * (3.0 * a.beta + 2.0));
     switch (a.beta) {
-        case 1: CK(inner_product_dispatch<1>(a, slots, grid, vec, st)); break;
-        case 2: CK(inner_product_dispatch<2>(a, slots, grid, vec, st)); break;
-        case 3: CK(inner_product_dispatch<3>(a, slots, grid, vec, st)); break;
-        case 4: CK(inner_product_dispatch<4>(a, slots, grid, vec, st)); break;
-        default: CK(inner_product_dispatch<0>(a, slots, grid, vec, st)); break;
+        case 1: CK(inner_product_dispatch<1>(a, slots, width, st)); break;
+        case 2: CK(inner_product_dispatch<2>(a, slots, width, st)); break;
+        case 3: CK(inner_product_dispatch<3>(a, slots, width, st)); break;
+        case 4: CK(inner_product_dispatch<4>(a, slots, width, st)); break;
+        default: CK(inner_product_dispatch<0>(a, slots, width, st)); break;
     }
     CK(cudaGetLastError());
     return CKKS_OK;

@@ -12,6 +12,7 @@
 //    NTT1/NTT2 split, reference n1 = 2^8).  Each kernel runs
 //    two radix-16 passes in registers (Shoup lazy butterflies, values kept in
 //    [0, 2q)) with one conflict-free shared-memory transpose between them.
+#include <cstdlib>
 #include "common.cuh"
 #include "internal.h"
 
