@@ -158,8 +158,10 @@ class LinearTransform:
             n1 = 1 << max(0, round(math.log2(math.sqrt(span))))
             if double_hoist:
                 # baby steps cost one inner product each (no ModUp, no ModDown), giant steps a
-                # ModUp + inner product + a ModDown of their inner sum: favour more baby steps
-                n1 = min(2 * n1, 16)
+                # ModUp + inner product + a ModDown of (half of) their inner sum: favour more baby
+                # steps, up to the 16 the fused kernel takes (measured at ks48, profiles/boot_n1.py:
+                # 16 everywhere 8.79 ms, 8 in the first / last group 8.87, 8 everywhere 10.2)
+                n1 = min(4 * n1, 16)
         self.step, self.n1 = step, n1
         self.pt_scale = float(math.prod(m.q for m in params.q_basis[level - limbs:level]))
         ext_basis = params.q_basis[:level] + params.p_basis
