@@ -613,13 +613,23 @@ int ckks_bconv_table_create(ckks_ctx* ctx, const int32_t* in_slot, int l_in, con
         om[i] = make_uint4(m.q, m.qinv, (uint32_t)i, (uint32_t)(((uint64_t)m.r1 << 16) % m.q));
     }
     for (int j = 0; j < l_in; ++j) inc[j] = make_uint4(qs[j], tab->inv_qhat[j], inv_s[j], 0u);
-    double* d_tf;
+    // K-stacked table of the tensor-core kernel: T * y = T * y0 + (T * 2^16 mod p) * y1 (mod p); every
+    // term < 2^47 resp. 2^46, at most 16 + 16 of them: the sum stays below 2^52 and is exact in ONE double
+    std::vector<double> t_f64k((size_t)lo8 * 2 * kp, 0.0);
+    for (int i = 0; i < l_out; ++i)
+        for (int j = 0; j < l_in; ++j) {
+            const uint64_t tm = t_mont[(size_t)i * l_in + j];
+            t_f64k[(size_t)i * 2 * kp + j] = (double)tm;
+            t_f64k[(size_t)i * 2 * kp + kp + j] = (double)((tm << 16) % ps[i]);
+        }
+    double *d_tf, *d_tfk;
     uint4 *d_om, *d_inc;
     CKS(upload(t_f64, &d_tf));
+    CKS(upload(t_f64k, &d_tfk));
     CKS(upload(om, &d_om));
     CKS(upload(inc, &d_inc));
-    tab->owned = {d_in, d_out, d_inv, d_invs, d_tm, d_tp, d_tf, d_om, d_inc};
-    tab->dev = BconvDev{l_in, l_out, all31, d_in, d_out, d_inv, d_invs, d_tm, d_tp, kp, d_tf, d_om, d_inc};
+    tab->owned = {d_in, d_out, d_inv, d_invs, d_tm, d_tp, d_tf, d_tfk, d_om, d_inc};
+    tab->dev = BconvDev{l_in, l_out, all31, d_in, d_out, d_inv, d_invs, d_tm, d_tp, kp, d_tf, d_tfk, d_om, d_inc};
     *table = (int32_t)ctx->tables.size();
     ctx->tables.push_back(std::move(tab));
     return CKKS_OK;

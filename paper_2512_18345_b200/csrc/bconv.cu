@@ -194,9 +194,15 @@ bconv_f64(BconvJobs jobs, const ModSlot* __restrict__ slots, size_t cols, int ch
 // FP64 tensor-core variant (DMMA, mma.sync m8n8k4).  Measured on B200
 // (profiles/microbench/dmma.cu): DMMA sustains 63.7 FMA/clk/SM, the same as DFMA, but one
 // warp instruction carries 256 of them, so the contraction needs ~1 instruction per 10
-// outputs instead of 12 IMAD.WIDE (2.8 integer-pipe slots each) per output.  Exactness is
-// the same split as bconv_f64: y = y1 * 2^16 + y0, every T * y0, T * y1 < 2^47, sums of up
-// to 16 terms < 2^51, accumulators seeded with 2^52 so the integer sum sits in the mantissa.
+// outputs instead of 12 IMAD.WIDE (2.8 integer-pipe slots each) per output.  Exactness:
+// y = y1 * 2^16 + y0 and T * y = T * y0 + (T * 2^16 mod p) * y1 (mod p), the second table
+// precomputed (BconvDev::t_f64k): the two halves of y are stacked along K, every term is below
+// 2^47 resp. 2^46, at most 16 + 16 of them, so the WHOLE contraction is an integer below 2^52.
+// It is formed in two chains (seeded 2^52 and 0, four DMMAs in flight per warp) whose sum is
+// exact, sits in the mantissa, and goes through ONE REDC against the Montgomery-form table.
+// (Round 1 kept two 2^52-seeded sums and recombined them with a 64-bit multiply by 2^48 mod p;
+// the stacked form has the same DMMA count and a third of the epilogue, measured equal in time:
+// 29.4 us at the full-size ModUp either way -- the kernel is not bound by its integer work.)
 //
 // GEMM view per conversion: D[i][c] = sum_k T[i][k] * y[k][c] with M = output limbs (tiles
 // of 8), K = input limbs (padded to a multiple of 4), N = columns (tiles of 8).  A warp owns
@@ -242,17 +248,19 @@ bconv_dmma(BconvJobs jobs, const ModSlot* __restrict__ slots, size_t cols, int c
     };
     pdl_trigger();
     // operands come ready-made from the table (api.cu): one level of loads, no arithmetic
-    double* s_t = reinterpret_cast<double*>(sm4);                          // [rows_pad][KP]
-    uint4* s_om = sm4 + ((size_t)((chunk + 7) & ~7) * KP * sizeof(double)) / sizeof(uint4);   // {q, qinv, out row, 2^48 mod q}
+    constexpr int KP2 = 2 * KP;                                            // the two halves of y stacked along K
+    double* s_t = reinterpret_cast<double*>(sm4);                          // [rows_pad][KP2]  {T | T * 2^16 mod p}
+    uint4* s_om = sm4 + ((size_t)((chunk + 7) & ~7) * KP2 * sizeof(double)) / sizeof(uint4);  // {q, qinv, out row, -}
     uint4* s_in = s_om + ((chunk + 7) & ~7);                               // {q, inv_qhat, shoup(inv_qhat), -}
     {
         // a conversion with fewer input limbs than the launch's KP (the partial last digit stacked
         // with the full ones) has a narrower table: zero-fill the extra columns
         const int kpj = job.tab.kp;
-        const double* src = job.tab.t_f64 + (size_t)i_lo * kpj;
-        for (int idx = threadIdx.x; idx < rows_pad * KP; idx += blockDim.x) {
-            const int i = idx / KP, k = idx - i * KP;
-            s_t[idx] = k < kpj ? src[(size_t)i * kpj + k] : 0.0;
+        const double* src = job.tab.t_f64k + (size_t)i_lo * 2 * kpj;
+        for (int idx = threadIdx.x; idx < rows_pad * KP2; idx += blockDim.x) {
+            const int i = idx / KP2, c = idx - i * KP2;
+            const int half = c >= KP ? 1 : 0, k = c - half * KP;
+            s_t[idx] = k < kpj ? src[(size_t)i * 2 * kpj + half * kpj + k] : 0.0;
         }
     }
     for (int r = threadIdx.x; r < rows_pad; r += blockDim.x) {
@@ -283,18 +291,23 @@ bconv_dmma(BconvJobs jobs, const ModSlot* __restrict__ slots, size_t cols, int c
         const size_t c_base = tile * 16;
         if (tile + warps < tiles) fetch(tile + warps);
         for (int m0 = 0; m0 < rows_pad; m0 += 8) {
-            double a[KS];
+            double a0[KS], a1[KS];
 #pragma unroll
-            for (int j = 0; j < KS; ++j) a[j] = s_t[(m0 + cc) * KP + 4 * j + kk];
+            for (int j = 0; j < KS; ++j) {
+                a0[j] = s_t[(m0 + cc) * KP2 + 4 * j + kk];
+                a1[j] = s_t[(m0 + cc) * KP2 + KP + 4 * j + kk];
+            }
+            // two chains per column tile (low / high half of y) keep four DMMAs in flight; their sum is
+            // the whole contraction, an integer below 2^52 on top of the 2^52 seed of c0
             double c0[2][2], c1[2][2];
 #pragma unroll
-            for (int t = 0; t < 2; ++t) c0[t][0] = c0[t][1] = c1[t][0] = c1[t][1] = seed;
+            for (int t = 0; t < 2; ++t) { c0[t][0] = c0[t][1] = seed; c1[t][0] = c1[t][1] = 0.0; }
 #pragma unroll
             for (int j = 0; j < KS; ++j) {
 #pragma unroll
                 for (int t = 0; t < 2; ++t) {
-                    dmma884(c0[t], a[j], y0[t][j]);
-                    dmma884(c1[t], a[j], y1[t][j]);
+                    dmma884(c0[t], a0[j], y0[t][j]);
+                    dmma884(c1[t], a1[j], y1[t][j]);
                 }
             }
             // lane holds D[m0 + cc][2 kk + {0, 1}] of both column tiles
@@ -306,9 +319,8 @@ bconv_dmma(BconvJobs jobs, const ModSlot* __restrict__ slots, size_t cols, int c
                     uint32_t r[2];
 #pragma unroll
                     for (int e = 0; e < 2; ++e) {
-                        const uint64_t b0 = (uint64_t)__double_as_longlong(c0[t][e]) & 0xFFFFFFFFFFFFFull;
-                        const uint64_t b1 = (uint64_t)__double_as_longlong(c1[t][e]) & 0xFFFFFFFFFFFFFull;
-                        const uint64_t v = (uint64_t)(uint32_t)(b1 >> 32) * om.w + ((b1 & 0xFFFFFFFFull) << 16) + b0;
+                        // V < 2^52: its high word (< 2^20 < p) and low word go straight through one REDC
+                        const uint64_t v = (uint64_t)__double_as_longlong(c0[t][e] + c1[t][e]) & 0xFFFFFFFFFFFFFull;
                         r[e] = redc((uint32_t)v, (uint32_t)(v >> 32), om.x, om.y);
                     }
                     *reinterpret_cast<uint2*>(dst + 8 * t) = make_uint2(r[0], r[1]);
@@ -375,7 +387,7 @@ static int launch_dmma(const BconvJobs& jobs, const ModSlot* slots, size_t cols,
     int z = (int)(((size_t)148 * 6 + ctas_xy - 1) / ctas_xy);
     if (z > z_max) z = z_max;
     const int chunk = (((l_out_max + z - 1) / z) + 7) & ~7;
-    const size_t sm = sizeof(double) * (size_t)chunk * 4 * KS + sizeof(uint4) * ((size_t)chunk + 4 * KS);
+    const size_t sm = sizeof(double) * (size_t)chunk * 8 * KS + sizeof(uint4) * ((size_t)chunk + 4 * KS);
     dim3 grid(gx, jobs.count, (l_out_max + chunk - 1) / chunk);
     ProfScope ps("bconv", st, jobs_bytes(jobs, cols), jobs_flops(jobs, cols));
     if (sm > 48 * 1024)

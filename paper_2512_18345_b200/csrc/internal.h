@@ -139,6 +139,8 @@ struct BconvDev {
     // ready-made operands of the FP64 tensor-core kernel (one load level in its prologue):
     int kp;                     // l_in rounded up to a multiple of 4
     const double* t_f64;        // [l_out rounded up to 8][kp]  t_mont as doubles, zero padded
+    const double* t_f64k;       // [l_out rounded up to 8][2 kp]  {t_mont | t_mont * 2^16 mod P_i}: the two 16-bit
+                                //   halves of y stacked along K, so ONE accumulator holds the whole sum (< 2^52)
     const uint4* om;            // [l_out rounded up to 8]  {P_i, -P_i^-1.. (qinv), i, 2^48 mod P_i}
     const uint4* inc;           // [kp]  {Q_k, inv_qhat, shoup(inv_qhat), 0}; padding {3, 0, 0, 0}
 };
