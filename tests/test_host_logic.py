@@ -207,3 +207,24 @@ def test_machine_profile_follows_the_reference_schema():
     assert prof["l2_write_bw"] <= prof["l2_read_bw"]
     assert prof["dram_bw"] < prof["l2_write_bw"]
     assert int(prof["l2_capacity"]) == B200_L2_BYTES
+
+
+def test_reference_timing_tool_runs_the_real_reference():
+    """baseline/time_reference.py (bench.py's `cpu_baseline.reference`): imports the travelling copy of the
+    NumPy reference only, times a unit single-process and on a process pool, prints one JSON line."""
+    import json
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    root = Path(__file__).resolve().parent.parent
+    if not (root / "baseline" / "_ref" / "rnscope").is_dir():
+        pytest.skip("no travelling copy of the reference (baseline/_ref); __graft_entry__.build() makes it")
+    res = subprocess.run([sys.executable, str(root / "baseline" / "time_reference.py"), "ntt", "--rows", "2", "--pool", "2"],
+                         capture_output=True, text=True, timeout=300)
+    assert res.returncode == 0, res.stderr[-500:]
+    doc = json.loads([ln for ln in res.stdout.splitlines() if ln.startswith("{")][-1])
+    assert doc["kind"] == "reference" and doc["workload"] == "ntt"
+    assert doc["single_process"]["ms_per_unit"] > 0 and doc["pool"]["processes"] == 2
+    src = (root / "baseline" / "time_reference.py").read_text()
+    assert "paper_2512_18345_b200" not in src.split('"""')[2], "the reference timing tool must not import the product"
