@@ -346,9 +346,142 @@ bsgs_inner_kernel(BsgsInnerArgs p, const ModSlot* __restrict__ slots) {
     }
 }
 
+// Bulk-copy (TMA) variant of the pipeline above: per baby step ONE elected thread requests the CTA's
+// 1 KiB slice of every key / plaintext row with cp.async.bulk (global -> shared, completion counted in
+// bytes on an mbarrier, L2 evict-first hint) instead of 128 threads issuing 2 BETA + NG 8-byte cp.async
+// each; consumers wait on the stage's mbarrier parity.  Same shared layout, same arithmetic, same result.
+// Needs n % 256 == 0 (a CTA's slice is 256 consecutive columns).
+__device__ __forceinline__ void bulk_g2s(uint32_t dst_smem, const void* src, uint32_t bytes, uint32_t bar, uint64_t pol) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
+                 :: "r"(dst_smem), "l"(src), "r"(bytes), "r"(bar), "l"(pol) : "memory");
+}
+
+template <int NG, int BETA>
+__global__ void __launch_bounds__(kBsgsThreads)
+bsgs_inner_tma_kernel(BsgsInnerArgs p, const ModSlot* __restrict__ slots) {
+    const int row = blockIdx.y;
+    const ModSlot m = slots[p.ext_slot[row]];
+    const size_t n = p.n;
+    const size_t i0 = (size_t)blockIdx.x * kBsgsThreads * 2;           // first column of this CTA
+    const size_t i = i0 + (size_t)threadIdx.x * 2;
+    const size_t erow = (size_t)p.evk_row[row];
+    const bool qrow = row < p.l;
+    const uint32_t pm = qrow ? p.pmod[row] : 0u, pms = qrow ? p.pmod_s[row] : 0u;
+    const uint64_t pol = l2_evict_first_policy();
+    const size_t half = (size_t)p.ext * n;
+    const size_t at = (size_t)row * n + i;
+    constexpr int ITEMS = 2 * BETA + NG;
+    constexpr uint32_t kSlice = kBsgsThreads * sizeof(uint2);          // 1 KiB per item
+    extern __shared__ __align__(128) uint2 s_pipe[];
+    __shared__ __align__(8) uint64_t s_full[kBsgsStages];
+    const uint32_t bar0 = (uint32_t)__cvta_generic_to_shared(&s_full[0]);
+    const uint32_t pipe0 = (uint32_t)__cvta_generic_to_shared(&s_pipe[0]);
+    pdl_trigger();
+    if (threadIdx.x == 0) {
+#pragma unroll
+        for (int s = 0; s < kBsgsStages; ++s) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(bar0 + 8 * s));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    pdl_wait();
+    uint64_t sa[NG][2], sb[NG][2];
+#pragma unroll
+    for (int g = 0; g < NG; ++g) sa[g][0] = sa[g][1] = sb[g][0] = sb[g][1] = 0;
+    auto slot = [&](int stage, int item) -> const uint2* { return s_pipe + ((size_t)(stage * ITEMS + item) * kBsgsThreads + threadIdx.x); };
+    auto request = [&](int b) {
+        if (threadIdx.x != 0 || b >= p.nb) return;
+        const int stage = b % kBsgsStages;
+        const uint32_t bar = bar0 + 8 * stage;
+        const bool keyed = p.k[b] != 0;
+        const uint32_t bytes = (uint32_t)((keyed ? 2 * BETA : 0) + NG) * kSlice;
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(bar), "r"(bytes) : "memory");
+        const uint32_t base = pipe0 + (uint32_t)(stage * ITEMS) * kSlice;
+        if (keyed) {
+            const uint32_t* key = p.evk[b];
+#pragma unroll
+            for (int t = 0; t < BETA; ++t) {
+                bulk_g2s(base + (2 * t) * kSlice, key + (((size_t)t * 2 + 0) * p.evk_ext + erow) * n + i0, kSlice, bar, pol);
+                bulk_g2s(base + (2 * t + 1) * kSlice, key + (((size_t)t * 2 + 1) * p.evk_ext + erow) * n + i0, kSlice, bar, pol);
+            }
+        }
+#pragma unroll
+        for (int g = 0; g < NG; ++g) bulk_g2s(base + (2 * BETA + g) * kSlice, p.p[g][b] + (size_t)row * n + i0, kSlice, bar, pol);
+    };
+#pragma unroll
+    for (int b = 0; b < kBsgsStages - 1; ++b) request(b);
+    for (int b = 0; b < p.nb; ++b) {
+        if (b > 0) __syncthreads();                      // everyone is done with the stage that is refilled next
+        request(b + kBsgsStages - 1);
+        const int stage = b % kBsgsStages;
+        {
+            const uint32_t bar = bar0 + 8 * stage, parity = (uint32_t)(b / kBsgsStages) & 1u;
+            asm volatile("{\n .reg .pred p;\n W%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @p bra D%=;\n bra W%=;\n D%=:\n}"
+                         :: "r"(bar), "r"(parity) : "memory");
+        }
+        uint32_t ra[2], rb[2];
+        const uint32_t k = p.k[b];
+        if (k == 0) {
+            if (qrow) {
+                const uint2 av = *reinterpret_cast<const uint2*>(p.ct_a + at);
+                const uint2 bv = *reinterpret_cast<const uint2*>(p.ct_b + at);
+                ra[0] = av.x; ra[1] = av.y; rb[0] = bv.x; rb[1] = bv.y;
+            } else {
+                ra[0] = ra[1] = rb[0] = rb[1] = 0;
+            }
+        } else {
+            const uint32_t g0 = galois_src((uint32_t)i, k, p.n, p.lg), g1 = galois_src((uint32_t)i + 1, k, p.n, p.lg);
+            uint64_t ta[2] = {0, 0}, tb[2] = {0, 0};
+#pragma unroll
+            for (int t = 0; t < BETA; ++t) {
+                const uint32_t* dsrc = p.raised + ((size_t)t * p.ext + row) * n;
+                const uint32_t d0 = dsrc[g0], d1 = dsrc[g1];
+                const uint2 xa = *slot(stage, 2 * t), xb = *slot(stage, 2 * t + 1);
+                ta[0] = mad64(d0, xa.x, ta[0]); ta[1] = mad64(d1, xa.y, ta[1]);
+                tb[0] = mad64(d0, xb.x, tb[0]); tb[1] = mad64(d1, xb.y, tb[1]);
+            }
+            ra[0] = reduce64(ta[0], m); ra[1] = reduce64(ta[1], m);
+            rb[0] = reduce64(tb[0], m); rb[1] = reduce64(tb[1], m);
+            if (qrow) {
+                const uint32_t* bsrc = p.ct_b + (size_t)row * n;
+                rb[0] = add_mod(rb[0], shoup_mul(bsrc[g0], pm, pms, m.q), m.q);
+                rb[1] = add_mod(rb[1], shoup_mul(bsrc[g1], pm, pms, m.q), m.q);
+            }
+        }
+#pragma unroll
+        for (int g = 0; g < NG; ++g) {
+            const uint2 pv = *slot(stage, 2 * BETA + g);
+            sa[g][0] += (uint64_t)ra[0] * pv.x; sa[g][1] += (uint64_t)ra[1] * pv.y;
+            sb[g][0] += (uint64_t)rb[0] * pv.x; sb[g][1] += (uint64_t)rb[1] * pv.y;
+        }
+        if ((b & 3) == 3) {
+#pragma unroll
+            for (int g = 0; g < NG; ++g) {
+                sa[g][0] = reduce64(sa[g][0], m); sa[g][1] = reduce64(sa[g][1], m);
+                sb[g][0] = reduce64(sb[g][0], m); sb[g][1] = reduce64(sb[g][1], m);
+            }
+        }
+    }
+#pragma unroll
+    for (int g = 0; g < NG; ++g) {
+        uint32_t* o = p.out[g];
+        *reinterpret_cast<uint2*>(o + at) = make_uint2(reduce64(sa[g][0], m), reduce64(sa[g][1], m));
+        *reinterpret_cast<uint2*>(o + half + at) = make_uint2(reduce64(sb[g][0], m), reduce64(sb[g][1], m));
+    }
+}
+
 template <int NG, int BETA>
 static int bsgs_launch_one(const BsgsInnerArgs& a, const ModSlot* slots, dim3 grid, cudaStream_t st) {
     const size_t sm = sizeof(uint2) * kBsgsThreads * (size_t)kBsgsStages * (2 * BETA + NG);
+    // default: the bulk-copy (TMA) pipeline; CKKS_BSGS_TMA=0: per-thread cp.async (also the path for ring
+    // degrees that are not a multiple of a CTA's 256 columns).  Measured at ks48: 400 vs 430 us per launch
+    // run eagerly, equal inside the bootstrap graph.
+    static const bool tma = [] { const char* e = getenv("CKKS_BSGS_TMA"); return !(e && e[0] == '0'); }();
+    if (tma && a.n % (2 * kBsgsThreads) == 0) {
+        if (sm > 48 * 1024)
+            CK(cudaFuncSetAttribute(bsgs_inner_tma_kernel<NG, BETA>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+        CK(launch_pdl(bsgs_inner_tma_kernel<NG, BETA>, grid, dim3(kBsgsThreads), sm, st, a, slots));
+        return CKKS_OK;
+    }
     if (sm > 48 * 1024)
         CK(cudaFuncSetAttribute(bsgs_inner_kernel<NG, BETA>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     CK(launch_pdl(bsgs_inner_kernel<NG, BETA>, grid, dim3(kBsgsThreads), sm, st, a, slots));

@@ -2,7 +2,8 @@
     python profiles/sass_summary.py > profiles/r2_sass_summary.txt
 For every kernel: instruction count, the integer / FP64 / tensor / memory opcode classes the hot
 loops are built from, and the Blackwell-specific opcodes the profiling guide asks to look for
-(UTCxMMA = tcgen05.mma, LDTM/STTM = tensor memory, UTMALDG/UTMASTG = TMA, ACQBULK/PREEXIT = PDL,
+(UTCxMMA = tcgen05.mma, LDTM/STTM = tensor memory, UTMALDG/UTMASTG = tensor TMA, UBLKCP = bulk TMA copy,
+SYNCS = mbarrier, ACQBULK/PREEXIT = PDL,
 256-bit LDG/STG).  Evidence of what the library is -- and is not -- built from."""
 import collections
 import re
@@ -15,7 +16,7 @@ CLASSES = [
     ("IMAD.HI", r"^IMAD\.HI"), ("IMAD.WIDE", r"^IMAD\.WIDE"), ("IMAD", r"^IMAD(?!\.HI|\.WIDE|\.MOV|\.IADD)"),
     ("IMAD.MOV/IADD", r"^IMAD\.(MOV|IADD)"), ("VIADDMNMX", r"^VIADDMNMX"), ("IADD3", r"^IADD3"), ("LOP3/SHF", r"^(LOP3|SHF)"),
     ("DMMA", r"^DMMA"), ("DFMA/DADD", r"^(DFMA|DADD|DMUL)"), ("HMMA/IMMA", r"^(HMMA|IMMA)"),
-    ("UTCxMMA", r"^UTC.*MMA"), ("LDTM/STTM", r"^(LDTM|STTM)"), ("UTMALDG/STG", r"^UTMA(LDG|STG)"),
+    ("UTCxMMA", r"^UTC.*MMA"), ("LDTM/STTM", r"^(LDTM|STTM)"), ("UTMALDG/STG", r"^UTMA(LDG|STG)"), ("UBLKCP", r"^UBLKCP"), ("SYNCS(mbarrier)", r"^SYNCS"),
     ("LDGSTS", r"^LDGSTS"), ("LDG", r"^LDG"), ("LDG.256", r"^LDG.*\.256"), ("STG", r"^STG"), ("STG.256", r"^STG.*\.256"),
     ("LDS", r"^LDS"), ("STS", r"^STS"), ("BAR", r"^BAR"), ("PDL", r"^(ACQBULK|PREEXIT)"), ("SHFL", r"^SHFL"),
 ]
@@ -48,9 +49,10 @@ def main():
         print(f"{k}\n    instructions={c['_total']}  {body}")
     print("\n# whole library")
     print("  ".join(f"{lab}={total[lab]}" for lab in labels))
-    print("# Blackwell-only opcodes: UTCxMMA (tcgen05.mma) = %d, LDTM/STTM (tensor memory) = %d, UTMALDG/UTMASTG (TMA) = %d; "
-          "PDL (ACQBULK/PREEXIT) = %d, 256-bit LDG/STG = %d" % (total["UTCxMMA"], total["LDTM/STTM"], total["UTMALDG/STG"],
-                                                               total["PDL"], total["LDG.256"] + total["STG.256"]))
+    print("# Hopper/Blackwell opcodes: UTCxMMA (tcgen05.mma) = %d, LDTM/STTM (tensor memory) = %d, UTMALDG/UTMASTG (tensor TMA) = %d, "
+          "UBLKCP (bulk async copy = TMA engine, cp.async.bulk) = %d with SYNCS (mbarrier) = %d; PDL (ACQBULK/PREEXIT) = %d, "
+          "256-bit LDG/STG = %d" % (total["UTCxMMA"], total["LDTM/STTM"], total["UTMALDG/STG"], total["UBLKCP"],
+                                    total["SYNCS(mbarrier)"], total["PDL"], total["LDG.256"] + total["STG.256"]))
 
 
 if __name__ == "__main__":
