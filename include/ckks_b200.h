@@ -105,6 +105,16 @@ int ckks_modulus_tables(ckks_ctx* ctx, int32_t slot, uint32_t* fwd, uint32_t* in
 int ckks_ntt(ckks_ctx* ctx, const uint32_t* in, uint32_t* out, const int32_t* row_slot, int rows,
              uint32_t n, int inverse, void* stream);
 
+/* Scheduling of the N = 2^16 transform (no effect on results): launches of at most
+ * cluster_max_rows limbs run as ONE kernel over thread-block clusters of eight CTAs per
+ * limb (the intermediate of transform.py:290-323's two phases is exchanged through
+ * distributed shared memory), taller ones as the two-kernel split; 0 = two kernels
+ * everywhere.  ctas_per_sm is 2 or 3.  Negative arguments leave a setting unchanged; the
+ * current values are returned through the pointers (may be null).  Process-wide host state:
+ * set it before capturing graphs.  Environment defaults: CKKS_NTT_CLUSTER_MAX_ROWS,
+ * CKKS_NTT_CLUSTER_OCC. */
+int ckks_ntt_policy(int cluster_max_rows, int ctas_per_sm, int* cluster_max_rows_now, int* ctas_per_sm_now);
+
 /* _run_stages over [stage_lo, stage_hi) (transform.py:203-250), the building
  * block of ntt_two_phase (transform.py:290-323). */
 int ckks_ntt_stages(ckks_ctx* ctx, const uint32_t* in, uint32_t* out, const int32_t* row_slot,

@@ -459,6 +459,11 @@ int ckks_ntt(ckks_ctx* ctx, const uint32_t* in, uint32_t* out, const int32_t* ro
                       (cudaStream_t)stream);
 }
 
+int ckks_ntt_policy(int cluster_max_rows, int ctas_per_sm, int* cluster_max_rows_now, int* ctas_per_sm_now) {
+    ntt_policy(cluster_max_rows, ctas_per_sm, cluster_max_rows_now, ctas_per_sm_now);
+    return CKKS_OK;
+}
+
 int ckks_ntt_stages(ckks_ctx* ctx, const uint32_t* in, uint32_t* out, const int32_t* row_slot,
                     int rows, uint32_t n, int inverse, uint32_t stage_lo, uint32_t stage_hi,
                     void* stream) {

@@ -85,6 +85,9 @@ int ntt_launch(const uint32_t* in, uint32_t* out, const int32_t* row_slot, const
                const ModDownEpilogueArgs* epi = nullptr, const uint32_t* mul_in = nullptr);
 // mul_in != null (inverse, N = 2^16 only): the input is in (.) mul_in, multiplied on load.
 bool ntt_can_fuse_moddown(uint32_t n);
+// Which N = 2^16 launches take the single-pass cluster kernels (at most max_rows limbs; 0: none)
+// and at how many CTAs per SM (2 or 3); negative / other values leave a setting as it is.
+void ntt_policy(int max_rows, int occ, int* max_rows_now, int* occ_now);
 int ntt_stages_launch(const uint32_t* in, uint32_t* out, const int32_t* row_slot,
                       const ModSlot* slots, int rows, uint32_t n, int inverse, uint32_t s_lo,
                       uint32_t s_hi, cudaStream_t st);

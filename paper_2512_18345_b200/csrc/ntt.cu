@@ -386,6 +386,249 @@ ntt16_inv_contig(const uint32_t* in, uint32_t* out, const int32_t* __restrict__ 
 }
 
 // ---------------------------------------------------------------------------------
+// N = 2^16, single pass over a thread-block cluster (the transform the
+// two-kernel split of transform.py:290-323 / PAPER.md:355-365 approximates).  A cluster of
+// eight CTAs owns one limb; each CTA keeps 1/8 of it (32 KiB) in shared memory and the
+// intermediate of the two phases never goes to global memory: it is exchanged through
+// distributed shared memory (st.shared::cluster into the CTA that owns the element in the
+// other phase's layout).
+//
+//   forward:  CTA r loads columns [32r, 32r + 32) of the 256 x 256 view (128-byte row
+//             segments), runs stages 0..7 as the strided phase does, sends row j to CTA
+//             j / 32, then runs stages 8..15 on its 32 contiguous 256-blocks and stores them
+//             (or the ModDown epilogue's result) as one contiguous 32 KiB piece.
+//   inverse:  the mirror image: blocks [32r, 32r + 32) in, stages 0..7, column c to CTA
+//             c / 32, stages 8..15 with N^-1 folded into the last, 128-byte row segments out.
+//
+// Same butterflies, same twiddle slots and the same register passes as the two-kernel
+// path (bit-exact to it and to _run_stages), half its global traffic, one launch.
+// 512 threads x 16 residues; thread layouts: strided passes (g, c) = (tid / 32, tid % 32),
+// contiguous passes (blk, e) = (tid / 16, tid % 16).
+// ---------------------------------------------------------------------------------
+constexpr int kClusterCtas = 8;
+constexpr int kClusterDefaultMaxRows = 0;     // default policy of ntt_launch, see cluster_max_rows()
+constexpr int kClusterThreads = 512;
+constexpr int kXbufWords = 32 * 272;           // 32 blocks, padded as in the contiguous kernels
+constexpr int kTileWords = 256 * 32;
+constexpr size_t kClusterSmem = sizeof(uint32_t) * (kXbufWords + kTileWords) + sizeof(uint2) * (256 + 32 * 16);
+
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void cluster_arrive() { asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory"); }
+__device__ __forceinline__ void cluster_wait() { asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory"); }
+__device__ __forceinline__ uint32_t smem_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ uint32_t map_to_rank(uint32_t addr, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void st_cluster(uint32_t addr, uint32_t v) {
+    asm volatile("st.shared::cluster.u32 [%0], %1;" :: "r"(addr), "r"(v) : "memory");
+}
+
+template <bool EPI, int OCC>
+__global__ void __cluster_dims__(kClusterCtas, 1, 1) __launch_bounds__(kClusterThreads, OCC)
+ntt16_fwd_cluster(const uint32_t* in, uint32_t* out, const int32_t* __restrict__ row_slot,
+                  const ModSlot* __restrict__ slots, RowMap rm, ModDownEpilogueArgs ep) {
+    extern __shared__ __align__(16) uint32_t dyn_smem[];
+    uint32_t* tile = dyn_smem;                               // [256][32]  strided-phase transpose
+    uint32_t* xbuf = dyn_smem + kTileWords;                  // [32][272]  this CTA's blocks, filled by the cluster
+    uint2* s_tw = reinterpret_cast<uint2*>(xbuf + kXbufWords);       // [256]     twiddles of stages 0..7
+    uint2* s_blk = s_tw + 256;                               // [32][16]  per block: twiddles of stages 8..11
+    const int tid = threadIdx.x;
+    const uint32_t rank = cluster_ctarank();
+    const ModSlot& m = slots[row_slot[blockIdx.y]];
+    const uint32_t q = m.q;
+    const uint2* __restrict__ fwd = m.fwd;
+    const int e = tid & 15, blk = tid >> 4;                  // contiguous-phase coordinates
+    const uint32_t B = rank * 32 + blk;
+    const bool ep_single = EPI && ep.halves == 1;
+    const int ep_row = EPI ? blockIdx.y % ep.l : 0, ep_half = (EPI && !ep_single) ? (blockIdx.y / ep.l) & 1 : 0;
+    const size_t ep_g = EPI ? blockIdx.y / ((ep_single ? 1 : 2) * ep.l) : 0;
+    const size_t ep_at = (size_t)ep_row * kN16 + B * 256 + 16 * e;
+    pdl_trigger();
+    cluster_arrive();                                        // (1) "this CTA is running"
+    if (EPI) {
+        asm volatile("prefetch.global.L2 [%0];" :: "l"((ep_half ? ep.xq_b : ep.xq_a) + ep_g * ep.xq_stride + ep_at));
+        const uint32_t* f = ep_half ? ep.fold_b : ep.fold_a;
+        if (f && !ep.galois) asm volatile("prefetch.global.L2 [%0];" :: "l"(f + ep_at));
+    }
+    if (tid < 256) s_tw[tid] = fwd[tid];
+    if (e < 15) {
+        const int st = 31 - __clz(e + 1);
+        s_blk[blk * 16 + e] = fwd[((256 + B) << st) + (e + 1 - (1 << st))];
+    }
+    const int c = tid & 31, g = tid >> 5;                    // strided-phase coordinates
+    const uint32_t* src = in + rm.in_row(blockIdx.y) * kN16 + rank * 32 + c;
+    uint32_t v[16];
+    pdl_wait();
+#pragma unroll
+    for (int k = 0; k < 16; ++k) v[k] = src[(g + 16 * k) * 256];
+    __syncthreads();
+    ct16(v, q, TW_MUL(s_tw[(1 << s) + gi]));                 // stages 0..3, rows g + 16k
+#pragma unroll
+    for (int k = 0; k < 16; ++k) tile[(g + 16 * k) * 32 + c] = v[k];
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < 16; ++k) v[k] = tile[(16 * g + k) * 32 + c];
+    ct16(v, q, TW_MUL(s_tw[(16 << s) + (g << s) + gi]));     // stages 4..7, rows 16g + k
+    // row j = 16g + k is block j of the contiguous phase: it belongs to CTA j / 32 = g / 2
+    cluster_wait();                                          // (1) every CTA of the cluster is running
+    {
+        const uint32_t at = smem_addr(xbuf + (16 * (g & 1)) * 272 + rank * 32 + c);
+        const uint32_t remote = map_to_rank(at, g >> 1);
+#pragma unroll
+        for (int k = 0; k < 16; ++k) st_cluster(remote + k * 272 * 4, v[k]);
+    }
+    cluster_arrive();                                        // (2) my rows are delivered
+    Tw15 tw;
+    load_tw15(fwd, (256 + B) * 16 + e, tw);
+    cluster_wait();                                          // (2) my blocks are complete
+    uint32_t* xb = xbuf + blk * 272;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) v[k] = xb[e + 16 * k];
+    __syncwarp();
+    ct16(v, q, TW_MUL(s_blk[blk * 16 + (1 << s) - 1 + gi]));  // stages 8..11, elements e + 16k
+#pragma unroll
+    for (int k = 0; k < 16; ++k) xb[e + 17 * k] = v[k];
+    __syncwarp();
+#pragma unroll
+    for (int k = 0; k < 16; ++k) v[k] = xb[17 * e + k];
+    // stages 12..15, elements 16e + k
+    ct16(v, q, TW_MUL(s == 0 ? tw.t1 : (s == 1 ? tw.t2[gi & 1] : (s == 2 ? tw.t4[gi & 3] : tw.t8[gi & 7]))));
+    if (EPI) {
+        const uint32_t pinv = ep.pinv[ep_row], pinv_s = ep.pinv_s[ep_row];
+        const uint32_t* x = (ep_half ? ep.xq_b : ep.xq_a) + ep_g * ep.xq_stride + ep_at;
+        const uint32_t* fsrc = ep_half ? ep.fold_b : ep.fold_a;
+        uint32_t* o = (ep_half ? ep.out_b : ep.out_a) + ep_g * ep.out_stride + ep_at;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            uint32_t xv[8], r[8];
+            ld256(x + 8 * h, xv);
+#pragma unroll
+            for (int k = 0; k < 8; ++k) r[k] = shoup_mul(xv[k] - csub(v[8 * h + k], q) + q, pinv, pinv_s, q);
+            if (fsrc && ep.galois) {
+                const uint32_t* f = fsrc + (size_t)ep_row * kN16;
+#pragma unroll
+                for (int k = 0; k < 8; ++k)
+                    r[k] = add_mod(r[k], f[galois_src(B * 256 + 16 * e + 8 * h + k, ep.galois, kN16, 16)], q);
+            } else if (fsrc) {
+                uint32_t fv[8];
+                ld256(fsrc + ep_at + 8 * h, fv);
+#pragma unroll
+                for (int k = 0; k < 8; ++k) r[k] = add_mod(r[k], fv[k], q);
+            }
+            st256(o + 8 * h, r);
+        }
+        return;
+    }
+    uint32_t* dst = out + rm.out_row(blockIdx.y) * kN16 + B * 256 + 16 * e;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        uint32_t r[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) r[k] = csub(v[8 * h + k], q);
+        st256(dst + 8 * h, r);
+    }
+}
+
+template <bool MUL, int OCC>
+__global__ void __cluster_dims__(kClusterCtas, 1, 1) __launch_bounds__(kClusterThreads, OCC)
+ntt16_inv_cluster(const uint32_t* in, uint32_t* out, const int32_t* __restrict__ row_slot,
+                  const ModSlot* __restrict__ slots, RowMap rm, const uint32_t* in2) {
+    extern __shared__ __align__(16) uint32_t dyn_smem[];
+    uint32_t* cbuf = dyn_smem;                               // [32][272]  contiguous-phase transposes, later [256][32]
+    uint32_t* xt = dyn_smem + kXbufWords;                    // [256][32]  this CTA's columns, filled by the cluster
+    uint2* s_tw = reinterpret_cast<uint2*>(xt + kTileWords);
+    uint2* s_blk = s_tw + 256;
+    const int tid = threadIdx.x;
+    const uint32_t rank = cluster_ctarank();
+    const ModSlot& m = slots[row_slot[blockIdx.y]];
+    const uint32_t q = m.q;
+    const uint2* __restrict__ inv = m.inv;
+    const int e = tid & 15, blk = tid >> 4;
+    const uint32_t B = rank * 32 + blk;
+    const uint32_t* src = in + rm.in_row(blockIdx.y) * kN16 + B * 256 + 16 * e;
+    pdl_trigger();
+    cluster_arrive();                                        // (1)
+    if (tid < 256) s_tw[tid] = inv[tid];
+    if (e < 15) {
+        const int st = e < 8 ? 0 : (e < 12 ? 1 : (e < 14 ? 2 : 3));
+        const int off = st == 0 ? 0 : (st == 1 ? 8 : (st == 2 ? 12 : 14));
+        s_blk[blk * 16 + e] = inv[(256 + B) * (8 >> st) + (e - off)];
+    }
+    Tw15 tw;
+    load_tw15(inv, (256 + B) * 16 + e, tw);
+    uint32_t v[16];
+    pdl_wait();
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        uint32_t r[8];
+        ld256(src + 8 * h, r);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) v[8 * h + k] = r[k];
+    }
+    if (MUL) {
+        const uint32_t* src2 = in2 + rm.in_row(blockIdx.y) * kN16 + B * 256 + 16 * e;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            uint32_t r[8];
+            ld256(src2 + 8 * h, r);
+#pragma unroll
+            for (int k = 0; k < 8; ++k) v[8 * h + k] = mul_mod(v[8 * h + k], r[k], m);
+        }
+    }
+    __syncwarp();
+    // stages 0..3 on elements 16e + k
+    gs16(v, q, TW_MUL(s == 0 ? tw.t8[gi & 7] : (s == 1 ? tw.t4[gi & 3] : (s == 2 ? tw.t2[gi & 1] : tw.t1))));
+    uint32_t* cb = cbuf + blk * 272;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) cb[17 * e + k] = v[k];
+    __syncwarp();
+#pragma unroll
+    for (int k = 0; k < 16; ++k) v[k] = cb[e + 17 * k];
+    // stages 4..7 on elements e + 16k
+    gs16(v, q, TW_MUL(s_blk[blk * 16 + (s == 0 ? 0 : (s == 1 ? 8 : (s == 2 ? 12 : 14))) + gi]));
+    // element e + 16k of block B is (row B, column e + 16k) of the 256 x 256 view: its column
+    // belongs to CTA (e + 16k) / 32 = k / 2.  Rows are stored with the two 16-word halves
+    // swapped on odd rows so that the two blocks of a warp hit different banks.
+    cluster_wait();                                          // (1)
+    {
+        const uint32_t sw = 16 * (B & 1);
+        const uint32_t at0 = smem_addr(xt + B * 32 + (e ^ sw)), at1 = smem_addr(xt + B * 32 + ((e + 16) ^ sw));
+#pragma unroll
+        for (int k = 0; k < 16; ++k) st_cluster(map_to_rank((k & 1) ? at1 : at0, k >> 1), v[k]);
+    }
+    cluster_arrive();                                        // (2)
+    const int c = tid & 31, g = tid >> 5;
+    uint32_t* dst = out + rm.out_row(blockIdx.y) * kN16 + rank * 32 + c;
+    const uint32_t ninv = m.n_inv, ninv_s = m.n_inv_s, wl = m.w_last, wl_s = m.w_last_s;
+    cluster_wait();                                          // (2): also orders s_tw and frees cbuf
+#pragma unroll
+    for (int k = 0; k < 16; ++k) v[k] = xt[(16 * g + k) * 32 + (c ^ (16 * (k & 1)))];
+    // global stages 8..11 on rows 16g + k
+    gs16(v, q, TW_MUL(s_tw[(16 + g) * (8 >> s) + gi]));
+#pragma unroll
+    for (int k = 0; k < 16; ++k) cbuf[(16 * g + k) * 32 + c] = v[k];
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < 16; ++k) v[k] = cbuf[(g + 16 * k) * 32 + c];
+    // global stages 12..14 on rows g + 16k, then the last stage with N^-1
+    gs16<3>(v, q, TW_MUL(s_tw[(8 >> s) + gi]));
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        const uint32_t x = v[j], y = v[j + 8];
+        const uint32_t total = csub(x + y, q);
+        const uint32_t diff = x - y + q;
+        dst[(g + 16 * j) * 256] = shoup_mul(total, ninv, ninv_s, q);
+        dst[(g + 16 * (j + 8)) * 256] = shoup_mul(diff, wl, wl_s, q);
+    }
+}
+
+// ---------------------------------------------------------------------------------
 // N <= 2^15: the whole limb lives in one CTA's shared memory (N * 4 B <= 128 KiB), so
 // the transform is ONE launch: radix-4 steps (two stages per barrier) on the
 // shared copy, same butterflies and twiddle slots as _run_stages.  Serves
@@ -559,6 +802,46 @@ static int launch_small(const uint32_t* in, uint32_t* out, const int32_t* row_sl
 
 bool ntt_can_fuse_moddown(uint32_t n) { return n == (uint32_t)kN16; }
 
+// Which N = 2^16 launches take the single-pass cluster kernels: those of at most
+// CKKS_NTT_CLUSTER_MAX_ROWS limbs (0: none, the two-kernel path everywhere).
+static int g_cluster_max_rows = -1, g_cluster_occ = -1;      // -1: not decided yet (environment, then default)
+static int cluster_max_rows() {
+    if (g_cluster_max_rows < 0) {
+        const char* s = getenv("CKKS_NTT_CLUSTER_MAX_ROWS");
+        g_cluster_max_rows = s ? atoi(s) : kClusterDefaultMaxRows;
+        if (g_cluster_max_rows < 0) g_cluster_max_rows = 0;
+    }
+    return g_cluster_max_rows;
+}
+static int cluster_occ() {
+    if (g_cluster_occ < 0) {
+        const char* s = getenv("CKKS_NTT_CLUSTER_OCC");
+        g_cluster_occ = (s && atoi(s) == 2) ? 2 : 3;
+    }
+    return g_cluster_occ;
+}
+void ntt_policy(int max_rows, int occ, int* max_rows_now, int* occ_now) {
+    if (max_rows >= 0) g_cluster_max_rows = max_rows;
+    if (occ == 2 || occ == 3) g_cluster_occ = occ;
+    if (max_rows_now) *max_rows_now = cluster_max_rows();
+    if (occ_now) *occ_now = cluster_occ();
+}
+static int cluster_attrs() {
+    static bool done = false;
+    if (done) return CKKS_OK;
+    const int bytes = (int)kClusterSmem;
+    CK(cudaFuncSetAttribute(ntt16_fwd_cluster<false, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    CK(cudaFuncSetAttribute(ntt16_fwd_cluster<false, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    CK(cudaFuncSetAttribute(ntt16_fwd_cluster<true, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    CK(cudaFuncSetAttribute(ntt16_fwd_cluster<true, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    CK(cudaFuncSetAttribute(ntt16_inv_cluster<false, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    CK(cudaFuncSetAttribute(ntt16_inv_cluster<false, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    CK(cudaFuncSetAttribute(ntt16_inv_cluster<true, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    CK(cudaFuncSetAttribute(ntt16_inv_cluster<true, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    done = true;
+    return CKKS_OK;
+}
+
 int ntt_launch(const uint32_t* in, uint32_t* out, const int32_t* row_slot, const ModSlot* slots,
                RowMap rm, int rows, uint32_t n, int inverse, cudaStream_t st,
                const ModDownEpilogueArgs* epi, const uint32_t* mul_in) {
@@ -572,6 +855,34 @@ int ntt_launch(const uint32_t* in, uint32_t* out, const int32_t* row_slot, const
                 (rows != epi_unit && (epi->fold_a || epi->fold_b)))) {
         set_last_error("fused ModDown epilogue needs a forward N = 2^16 transform over (a multiple of) 2 l rows");
         return CKKS_ERR_ARG;
+    }
+    if (n == (uint32_t)kN16 && rows <= cluster_max_rows()) {
+        // single-pass transform, one cluster of eight CTAs per limb: 2 * R * N * 4 bytes in ONE launch
+        CKS(cluster_attrs());
+        const dim3 grid(kClusterCtas, rows), block(kClusterThreads);
+        const bool occ3 = cluster_occ() == 3;
+        if (!inverse) {
+            if (epi) {
+                ProfScope ps("ntt16_fwd_cluster_moddown", st, 4.0 * rows * kN16 * (epi->fold_b ? 3.5 : 3.0));
+                if (occ3) CK(launch_pdl(ntt16_fwd_cluster<true, 3>, grid, block, kClusterSmem, st, in, out, row_slot, slots, rm, *epi));
+                else CK(launch_pdl(ntt16_fwd_cluster<true, 2>, grid, block, kClusterSmem, st, in, out, row_slot, slots, rm, *epi));
+            } else {
+                ProfScope ps("ntt16_fwd_cluster", st, 8.0 * rows * kN16);
+                if (occ3) CK(launch_pdl(ntt16_fwd_cluster<false, 3>, grid, block, kClusterSmem, st, in, out, row_slot, slots, rm, ModDownEpilogueArgs{}));
+                else CK(launch_pdl(ntt16_fwd_cluster<false, 2>, grid, block, kClusterSmem, st, in, out, row_slot, slots, rm, ModDownEpilogueArgs{}));
+            }
+        } else {
+            ProfScope ps("ntt16_inv_cluster", st, (mul_in ? 12.0 : 8.0) * rows * kN16);
+            if (mul_in) {
+                if (occ3) CK(launch_pdl(ntt16_inv_cluster<true, 3>, grid, block, kClusterSmem, st, in, out, row_slot, slots, rm, mul_in));
+                else CK(launch_pdl(ntt16_inv_cluster<true, 2>, grid, block, kClusterSmem, st, in, out, row_slot, slots, rm, mul_in));
+            } else {
+                if (occ3) CK(launch_pdl(ntt16_inv_cluster<false, 3>, grid, block, kClusterSmem, st, in, out, row_slot, slots, rm, (const uint32_t*)nullptr));
+                else CK(launch_pdl(ntt16_inv_cluster<false, 2>, grid, block, kClusterSmem, st, in, out, row_slot, slots, rm, (const uint32_t*)nullptr));
+            }
+        }
+        CK(cudaGetLastError());
+        return CKKS_OK;
     }
     if (n == (uint32_t)kN16) {
         constexpr int COLS = 16;

@@ -239,6 +239,16 @@ class Engine:
                                      a.shape[0], a.shape[1], int(inverse), self.stream()))
         return out
 
+    def ntt_policy(self, cluster_max_rows: int = -1, ctas_per_sm: int = -1) -> tuple[int, int]:
+        """Set (negative: only read) which N = 2^16 transforms run as one cluster kernel: those
+        of at most `cluster_max_rows` limbs (0: the two-kernel split everywhere).  Scheduling
+        only, results are identical.  Returns the values now in force."""
+        import ctypes
+
+        rows, occ = ctypes.c_int(0), ctypes.c_int(0)
+        _lib.check(self.lib.ckks_ntt_policy(int(cluster_max_rows), int(ctas_per_sm), ctypes.byref(rows), ctypes.byref(occ)))
+        return rows.value, occ.value
+
     def ntt_stages(self, a, row_slot, inverse: bool, lo: int, hi: int, out=None):
         out = self.torch.empty_like(a) if out is None else out
         _lib.check(self.lib.ckks_ntt_stages(self.ctx, a.data_ptr(), out.data_ptr(),
