@@ -5,13 +5,16 @@
 // table and Gentleman-Sande inverse with N^-1 folded into the last stage;
 // natural order in, bit-reversed evaluation order out (SURVEY 8a').
 //
-// Two implementations:
+// Implementations:
 //  * generic: one radix-2 stage per launch straight on global memory; any N,
 //    any stage range (serves ntt_two_phase with arbitrary n1 and small rings).
 //  * N = 2^16 fast path: two kernels of eight stages each (the paper's
 //    NTT1/NTT2 split, reference n1 = 2^8).  Each kernel runs
 //    two radix-16 passes in registers (Shoup lazy butterflies, values kept in
 //    [0, 2q)) with one conflict-free shared-memory transpose between them.
+//  * N = 2^16, launches of few limbs: the same passes as ONE kernel over clusters of eight
+//    CTAs per limb, the intermediate exchanged through distributed shared memory.
+//  * N <= 2^15: one CTA per limb, the limb in shared memory.
 #include <cstdlib>
 #include "common.cuh"
 #include "internal.h"
@@ -406,7 +409,11 @@ ntt16_inv_contig(const uint32_t* in, uint32_t* out, const int32_t* __restrict__ 
 // contiguous passes (blk, e) = (tid / 16, tid % 16).
 // ---------------------------------------------------------------------------------
 constexpr int kClusterCtas = 8;
-constexpr int kClusterDefaultMaxRows = 0;     // default policy of ntt_launch, see cluster_max_rows()
+// Default policy of ntt_launch (see cluster_max_rows()): measured on B200 (profiles/ntt_cluster_ab.py,
+// r2l_ntt_cluster_ab.json) the single launch wins up to ~28 limbs (2 rows: 6.4 vs 11.5 us inverse, 28
+// rows: 12.7 vs 15.0 us) and loses above (192 rows: 63 vs 48 us: two cluster barriers and a 21 B/clk/SM
+// DSMEM exchange per CTA cost more than the global round trip they replace).
+constexpr int kClusterDefaultMaxRows = 28;
 constexpr int kClusterThreads = 512;
 constexpr int kXbufWords = 32 * 272;           // 32 blocks, padded as in the contiguous kernels
 constexpr int kTileWords = 256 * 32;
@@ -816,7 +823,7 @@ static int cluster_max_rows() {
 static int cluster_occ() {
     if (g_cluster_occ < 0) {
         const char* s = getenv("CKKS_NTT_CLUSTER_OCC");
-        g_cluster_occ = (s && atoi(s) == 2) ? 2 : 3;
+        g_cluster_occ = (s && atoi(s) == 3) ? 3 : 2;
     }
     return g_cluster_occ;
 }
