@@ -292,6 +292,18 @@ int ckks_bsgs_inner(ckks_ctx* ctx, int32_t plan, const uint32_t* raised, const u
                     const uint32_t* ct_b, int nb, const uint32_t* k, const uint32_t* const* evk, int ng,
                     const uint32_t* const* p, const uint32_t* zero, uint32_t* const* out, void* stream);
 
+/* The same for `batch` (<= 2) independent ciphertexts at the same level, through the same keys and
+ * diagonals, in ONE launch: each key / plaintext slice is staged in shared memory once and
+ * multiplied into every ciphertext's sums (the reference batches key switches in a loop,
+ * keyswitch.py:456-459; the paper's L2-aware multi-polynomial grouping is this sharing).  raised,
+ * ct_a, ct_b: host arrays of `batch` device pointers; out: host array [batch][ng], element c's
+ * results at out[c * ng + g].  Values equal `batch` calls of ckks_bsgs_inner bit for bit.
+ * Needs n % 256 == 0 (CKKS_ERR_UNSUPPORTED otherwise: call ckks_bsgs_inner per ciphertext). */
+int ckks_bsgs_inner_batch(ckks_ctx* ctx, int32_t plan, int batch, const uint32_t* const* raised,
+                          const uint32_t* const* ct_a, const uint32_t* const* ct_b, int nb, const uint32_t* k,
+                          const uint32_t* const* evk, int ng, const uint32_t* const* p, const uint32_t* zero,
+                          uint32_t* const* out, void* stream);
+
 /* ckks_ks_stage3 (ModDown) of `count` <= 4 accumulators in one set of launches: qp is
  * [count][2][l + alpha][n] (Q rows then P rows per half), out [count][2][l][n]; element g uses the
  * workspace of lane (current + g), so count lanes from the current one must exist and be idle.

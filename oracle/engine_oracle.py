@@ -450,6 +450,11 @@ class OracleEngine:
                     self._pmult_acc(u, self._np(row[bi]), outs[g], rm, False)
         return [self._t(o) for o in outs]
 
+    def bsgs_inner_batch(self, plan: int, raised, ct_a, ct_b, ks, evks, table, ext: int):
+        """Engine.bsgs_inner_batch: the batch is a scheduling device of the CUDA engine (shared key
+        traffic); its values are those of one bsgs_inner per ciphertext, which is what runs here."""
+        return [self.bsgs_inner(plan, raised[c], ct_a[c], ct_b[c], ks, evks, table, ext) for c in range(len(raised))]
+
     def _relin_rescale(self, pl: _Plan, md: _Plan, d0, d1, d2, evk, add_a=None, add_b=None):
         acc = self._inner(pl, self._raise(pl, d2), evk, lift_a=d1, lift_b=d0)
         res = self._moddown_pair(md, acc)

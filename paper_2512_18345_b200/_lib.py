@@ -21,7 +21,7 @@ SYMBOLS = (
     "ckks_modulus_register", "ckks_modulus_register_tables", "ckks_modulus_tables", "ckks_ntt", "ckks_ntt_policy", "ckks_ntt_stages",
     "ckks_elementwise", "ckks_automorphism_eval", "ckks_automorphism_coeff", "ckks_lift2_centered", "ckks_pmult_accumulate", "ckks_fused_terms", "ckks_fused_terms_multi", "ckks_tensor", "ckks_tensor_halves",
     "ckks_bconv_table_create", "ckks_bconv_table_read", "ckks_bconv",
-    "ckks_ks_plan_create", "ckks_moddown_plan_create", "ckks_ks_stage1", "ckks_ks_stage2", "ckks_ks_stage3", "ckks_ks_stage3_batch", "ckks_ks_stage3_batch_a", "ckks_keyswitch", "ckks_ks_hoisted", "ckks_ks_hoisted_raw", "ckks_bsgs_inner", "ckks_ks_relin_rescale", "ckks_hmult_relin_rescale", "ckks_ks_accumulate", "ckks_ks_accumulate_rot", "ckks_ks_accumulate_rot_qp", "ckks_ks_finish", "ckks_ks_finish_rescale",
+    "ckks_ks_plan_create", "ckks_moddown_plan_create", "ckks_ks_stage1", "ckks_ks_stage2", "ckks_ks_stage3", "ckks_ks_stage3_batch", "ckks_ks_stage3_batch_a", "ckks_keyswitch", "ckks_ks_hoisted", "ckks_ks_hoisted_raw", "ckks_bsgs_inner", "ckks_bsgs_inner_batch", "ckks_ks_relin_rescale", "ckks_hmult_relin_rescale", "ckks_ks_accumulate", "ckks_ks_accumulate_rot", "ckks_ks_accumulate_rot_qp", "ckks_ks_finish", "ckks_ks_finish_rescale",
 )
 
 
@@ -99,6 +99,7 @@ def load() -> ctypes.CDLL:
     L.ckks_ks_stage3_batch_a.argtypes = [vp, i32, ctypes.c_int, vp, vp, vp]
     L.ckks_hmult_relin_rescale.argtypes = [vp, i32, i32, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]
     L.ckks_bsgs_inner.argtypes = [vp, i32, vp, vp, vp, ctypes.c_int, vp, vp, ctypes.c_int, vp, vp, vp, vp]
+    L.ckks_bsgs_inner_batch.argtypes = [vp, i32, ctypes.c_int, vp, vp, vp, ctypes.c_int, vp, vp, ctypes.c_int, vp, vp, vp, vp]
     L.ckks_ks_accumulate.argtypes = [vp, i32, vp, vp, ctypes.c_int, vp]
     L.ckks_ks_accumulate_rot.argtypes = [vp, i32, vp, vp, ctypes.c_uint32, vp, ctypes.c_int, vp]
     L.ckks_ks_accumulate_rot_qp.argtypes = [vp, i32, vp, vp, ctypes.c_uint32, vp, ctypes.c_int, vp]

@@ -183,9 +183,46 @@ class LinearTransform:
         self.baby = sorted({b for row in table.values() for b in row})
         self.giants = sorted(table)
 
-    def _double_hoisted_inner(self, ct, keys, eng):
+    def _fused_ok(self, eng) -> bool:
+        """The fused baby-step kernel (bsgs_inner) takes this transform."""
+        beta = -(-self.level // self.params.alpha)
+        return self.params.n % 2 == 0 and len(self.baby) <= 16 and beta <= 4 and self.fuse_baby_steps
+
+    def _bsgs_prepare(self, ct, keys, eng):
+        """ModUp of the input and the argument lists of the fused baby-step kernel (everything of a
+        double-hoisted transform that precedes the bsgs_inner launch)."""
+        p = self.params
+        n_ring, level, alpha = p.n, self.level, p.alpha
+        ext = level + alpha
+        plan = eng.ks_plan(n_ring, ct.a.basis, p.p_basis, alpha, p.l + alpha, p.l)
+        raised = eng.ks_stage1(plan, ct.a.data, -(-level // alpha), ext)
+        babies = list(self.baby)
+        ks_idx, evks = [], []
+        for b in babies:
+            if b == 0:
+                ks_idx.append(0)
+                evks.append(None)
+                continue
+            k = ckks.galois_element(b * self.step, n_ring)
+            if k not in keys.galois:
+                raise RnsError(f"no Galois key for rotation {b * self.step}")
+            ks_idx.append(k)
+            evks.append(keys.galois[k].matrix())
+        # the unrotated giant step first, the moving ones after it in one allocation (so that a
+        # batched ModDown can take them as one [count, 2, ext, n] slice)
+        order = [g for g in self.giants if g == 0] + [g for g in self.giants if g != 0]
+        chunks = []
+        for g0 in range(0, len(order), 8):
+            chunk = order[g0:g0 + 8]
+            chunks.append((chunk, [[self.table[g][b].poly.data if b in self.table[g] else None for b in babies]
+                                   for g in chunk]))
+        return {"plan": plan, "raised": raised, "ks": ks_idx, "evks": evks, "chunks": chunks, "ext": ext}
+
+    def _double_hoisted_inner(self, ct, keys, eng, qps=None):
         """Baby steps as raw Q||P accumulators sharing one ModUp; returns inner_sum(g) that
-        forms sum_b pt_{g,b} * u_b over Q||P in one fused pass and scales it down once."""
+        forms sum_b pt_{g,b} * u_b over Q||P in one fused pass and scales it down once.
+        `qps`: the giant steps' Q||P accumulators when a batched launch (apply_batch) has already
+        formed them."""
         import torch
 
         p = self.params
@@ -193,43 +230,30 @@ class LinearTransform:
         ext = level + alpha
         basis = ct.a.basis
         plan = eng.ks_plan(n_ring, basis, p.p_basis, alpha, p.l + alpha, p.l)
-        ext_slots = eng.row_slots(basis + p.p_basis)
-        raised = eng.ks_stage1(plan, ct.a.data, -(-level // alpha), ext)
-        b_half = ct.b.data
-        moving = [b for b in self.baby if b]
-
-        def raw(b):
-            k = ckks.galois_element(b * self.step, n_ring)
-            if k not in keys.galois:
-                raise RnsError(f"no Galois key for rotation {b * self.step}")
-            return eng.ks_hoisted_raw(plan, raised, k, keys.galois[k].matrix(), b_half, ext)
-
         giants = self.giants
-        qps = {}
-        beta = -(-level // alpha)
-        if n_ring % 2 == 0 and len(self.baby) <= 16 and beta <= 4 and self.fuse_baby_steps:
+        if qps is not None:
+            pass
+        elif self._fused_ok(eng):
             # baby steps and inner sums in ONE pass: each rotated accumulator is formed in
             # registers and multiplied into every giant step's sum, never written
-            babies = list(self.baby)
-            ks_idx, evks = [], []
-            for b in babies:
-                if b == 0:
-                    ks_idx.append(0)
-                    evks.append(None)
-                    continue
+            pre = self._bsgs_prepare(ct, keys, eng)
+            qps = {}
+            for chunk, table in pre["chunks"]:
+                qps.update(zip(chunk, eng.bsgs_inner(plan, pre["raised"], ct.a.data, ct.b.data, pre["ks"], pre["evks"],
+                                                     table, ext)))
+        else:
+            ext_slots = eng.row_slots(basis + p.p_basis)
+            raised = eng.ks_stage1(plan, ct.a.data, -(-level // alpha), ext)
+            b_half = ct.b.data
+            moving = [b for b in self.baby if b]
+
+            def raw(b):
                 k = ckks.galois_element(b * self.step, n_ring)
                 if k not in keys.galois:
                     raise RnsError(f"no Galois key for rotation {b * self.step}")
-                ks_idx.append(k)
-                evks.append(keys.galois[k].matrix())
-            # the unrotated giant step first, the moving ones after it in one allocation (so that a
-            # batched ModDown can take them as one [count, 2, ext, n] slice)
-            order = [g for g in giants if g == 0] + [g for g in giants if g != 0]
-            for g0 in range(0, len(order), 8):
-                chunk = order[g0:g0 + 8]
-                table = [[self.table[g][b].poly.data if b in self.table[g] else None for b in babies] for g in chunk]
-                qps.update(zip(chunk, eng.bsgs_inner(plan, raised, ct.a.data, b_half, ks_idx, evks, table, ext)))
-        else:
+                return eng.ks_hoisted_raw(plan, raised, k, keys.galois[k].matrix(), b_half, ext)
+
+            qps = {}
             acc = dict(zip(moving, eng.fork([(lambda b=b: raw(b)) for b in moving])))
             if 0 in self.baby:
                 x = ckks.ct_tensor(ct)
@@ -306,7 +330,35 @@ class LinearTransform:
         out |= {(g * self.n1 * self.step) % self.n for g in self.giants if g}
         return out
 
-    def apply(self, ct, keys: ckks.EvaluationKeys):
+    def apply_batch(self, cts, keys: ckks.EvaluationKeys):
+        """The transform of several independent ciphertexts at once (BASELINE config 5: batches of
+        independent bootstraps).  Each ciphertext keeps its own lanes for ModUp, giant steps and
+        ModDown; what the batch shares is the traffic of the fused baby-step kernel, 27 % of a
+        bootstrap: pairs go through one launch that reads every rotation key and every plaintext
+        diagonal once for both (Engine.bsgs_inner_batch).  Results equal apply() per ciphertext bit
+        for bit."""
+        from .engine import get_engine
+
+        eng = get_engine()
+        cts = list(cts)
+        if len(cts) == 1 or not (self.double_hoist and self._fused_ok(eng)):
+            return eng.fork([(lambda ct=ct: self.apply(ct, keys)) for ct in cts]) if len(cts) > 1 else [self.apply(cts[0], keys)]
+        for ct in cts:
+            if ckks.level_of(ct) != self.level:
+                raise RnsError(f"linear transform encoded for level {self.level}, ciphertext at {ckks.level_of(ct)}")
+        pre = eng.fork([(lambda ct=ct: self._bsgs_prepare(ct, keys, eng)) for ct in cts])
+        first = pre[0]
+        qps = [{} for _ in cts]
+        for chunk, table in first["chunks"]:
+            outs = eng.bsgs_inner_batch(first["plan"], [q["raised"] for q in pre], [ct.a.data for ct in cts],
+                                        [ct.b.data for ct in cts], first["ks"], first["evks"], table, first["ext"])
+            for mine, o in zip(qps, outs):
+                mine.update(zip(chunk, o))
+        out = eng.fork([(lambda ct=ct, q=q: self.apply(ct, keys, _qps=q)) for ct, q in zip(cts, qps)])
+        del pre                                   # raised digits stay referenced until the joins above
+        return out
+
+    def apply(self, ct, keys: ckks.EvaluationKeys, _qps=None):
         from .engine import get_engine
 
         eng = get_engine()
@@ -315,7 +367,7 @@ class LinearTransform:
         basis = ct.a.basis
         slots = eng.row_slots(basis)
         if self.double_hoist:
-            inner_sum = self._double_hoisted_inner(ct, keys, eng)
+            inner_sum = self._double_hoisted_inner(ct, keys, eng, qps=_qps)
         else:
             # baby steps: rotations of the same input sharing one ModUp, spread over the lanes
             hoisted = ckks.hrot_hoisted(ct, [b * self.step for b in self.baby], keys)
@@ -667,6 +719,94 @@ class Bootstrapper:
         for lt in self.stc:
             ct = lt.apply(ct, self.keys)
         return ct
+
+    def bootstrap_batch(self, cts):
+        """Several independent bootstraps at once (BASELINE config 5: batches of independent
+        bootstraps on one GPU).  Every ciphertext runs the circuit of bootstrap() on its own share
+        of the engine's lanes; the six linear transforms go through LinearTransform.apply_batch,
+        which reads each rotation key and plaintext diagonal once per PAIR of ciphertexts.  The
+        results equal bootstrap() per ciphertext limb for limb."""
+        from .engine import get_engine
+
+        eng = get_engine()
+        cts = list(cts)
+        if len(cts) == 1:
+            return [self.bootstrap(cts[0])]
+        for ct in cts:
+            if not ckks._close(ct.scale, self.delta_in):
+                raise RnsError(f"bootstrap expects scale 2^{self.cfg.log_delta_in}, got {ct.scale}")
+
+        def lift(ct):
+            if self.to_sparse is not None:
+                ct = ckks.keyswitch_level(ct, self.to_sparse)
+            raised = self.mod_raise(ct)
+            if self.to_dense is not None:
+                back = ckks.keyswitch_level(ckks.Ciphertext(raised.a, raised.b, raised.scale), self.to_dense)
+                raised = ckks.Ciphertext(a=back.a, b=back.b, scale=raised.scale)
+            return raised
+
+        def split(ct):
+            conj = ckks.conjugate_fused(ct, self.keys)
+            lo, hi = ckks.add(ct, conj), ckks.sub(ct, conj)
+            return ckks.Ciphertext(lo.a, lo.b, self.eval_scale), ckks.Ciphertext(hi.a, hi.b, self.eval_scale)
+
+        xs = eng.fork([(lambda ct=ct: lift(ct)) for ct in cts])
+        for lt in self.cts:
+            xs = lt.apply_batch(xs, self.keys)
+        halves = eng.fork([(lambda x=x: split(x)) for x in xs])
+        kappa = self.q0 / (4.0 * math.pi * self.delta_in) / 1j
+        jobs = []
+        for lo, hi in halves:
+            jobs.append(lambda lo=lo: self.eval_mod(lo, self.coef_lo, kappa))
+            jobs.append(lambda hi=hi: self.eval_mod(hi, self.coef_hi, kappa * 1j))
+        ms = eng.fork(jobs)
+        ws = [ckks.mod_drop(ckks.add(ms[2 * i], ms[2 * i + 1]), self.lvl_stc) for i in range(len(cts))]
+        for lt in self.stc:
+            ws = lt.apply_batch(ws, self.keys)
+        return [ckks.Ciphertext(w.a, w.b, self.out_scale) for w in ws]
+
+    def capture_batch(self, sample_cts):
+        """bootstrap_batch recorded as one CUDA graph: replay(cts) -> list of ciphertexts."""
+        import torch
+
+        from .engine import get_engine
+
+        eng = get_engine()
+        count = len(sample_cts)
+        basis, scale = sample_cts[0].a.basis, sample_cts[0].scale
+        static_in = torch.stack([torch.stack([ct.a.data, ct.b.data]) for ct in sample_cts]).clone()
+        views = [ct_from_tensor(static_in[i], basis, scale) for i in range(count)]
+        self.bootstrap_batch(views)                           # warm-up: plans, constants, caches
+        torch.cuda.synchronize()
+        graph = torch.cuda.CUDAGraph()
+        side = torch.cuda.Stream(device=eng.device)
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            self.bootstrap_batch(views)                       # settle allocator state on the side stream
+            torch.cuda.synchronize()
+            with torch.cuda.graph(graph, stream=side):
+                outs = self.bootstrap_batch(views)
+                static_out = torch.stack([torch.stack([o.a.data, o.b.data]) for o in outs])
+        torch.cuda.current_stream().wait_stream(side)
+        out_basis, out_scale = outs[0].a.basis, outs[0].scale
+        generation = eng.arena_generation()
+
+        def replay(cts, copy_out: bool = True):
+            if eng.arena_generation() != generation:
+                raise RnsError("the workspace arena was reallocated after this graph was captured (lane count "
+                               "changed or a larger key-switch plan was created): capture again")
+            if len(cts) != count:
+                raise RnsError(f"graph was captured for {count} ciphertexts, got {len(cts)}")
+            for i, ct in enumerate(cts):
+                static_in[i, 0].copy_(ct.a.data)
+                static_in[i, 1].copy_(ct.b.data)
+            graph.replay()
+            res = static_out.clone() if copy_out else static_out
+            return [ct_from_tensor(res[i], out_basis, out_scale) for i in range(count)]
+
+        replay.graph, replay.static_in, replay.static_out = graph, static_in, static_out
+        replay.valid = lambda: eng.arena_generation() == generation
+        return replay
 
     def capture(self, sample_ct):
         """Record one whole bootstrap (ModRaise .. SlotToCoeff, ~2.5k kernel launches) into a

@@ -971,9 +971,10 @@ int ckks_ks_hoisted_raw(ckks_ctx* ctx, int32_t plan, const uint32_t* raised, uin
     return inner_product_launch(ip, ctx->d_slots, (cudaStream_t)stream);
 }
 
-int ckks_bsgs_inner(ckks_ctx* ctx, int32_t plan, const uint32_t* raised, const uint32_t* ct_a,
-                    const uint32_t* ct_b, int nb, const uint32_t* k, const uint32_t* const* evk, int ng,
-                    const uint32_t* const* p, const uint32_t* zero, uint32_t* const* out, void* stream) {
+static int bsgs_inner_core(ckks_ctx* ctx, int32_t plan, int batch, const uint32_t* const* raised,
+                           const uint32_t* const* ct_a, const uint32_t* const* ct_b, int nb, const uint32_t* k,
+                           const uint32_t* const* evk, int ng, const uint32_t* const* p, const uint32_t* zero,
+                           uint32_t* const* out, void* stream) {
     KsPlan* pl;
     CKS(get_plan(ctx, plan, &pl));
     CKS(need_full_plan(pl));
@@ -981,8 +982,16 @@ int ckks_bsgs_inner(ckks_ctx* ctx, int32_t plan, const uint32_t* raised, const u
         set_last_error("bsgs_inner: %d baby x %d giant steps out of range [1, %d] x [1, %d]", nb, ng, kMaxTerms, kMaxGiants);
         return CKKS_ERR_ARG;
     }
+    if (batch < 1 || batch > kMaxBsgsBatch || !raised || !ct_a || !ct_b) {
+        set_last_error("bsgs_inner: batch of %d ciphertexts out of range [1, %d]", batch, kMaxBsgsBatch);
+        return CKKS_ERR_ARG;
+    }
     BsgsInnerArgs a{};
-    a.raised = raised; a.ct_a = ct_a; a.ct_b = ct_b;
+    a.batch = batch;
+    for (int c = 0; c < batch; ++c) {
+        if (!raised[c] || !ct_a[c] || !ct_b[c]) { set_last_error("bsgs_inner: null operand in batch element %d", c); return CKKS_ERR_ARG; }
+        a.raised[c] = raised[c]; a.ct_a[c] = ct_a[c]; a.ct_b[c] = ct_b[c];
+    }
     a.ext_slot = pl->d_ext_slot; a.evk_row = pl->d_evk_row; a.pmod = pl->d_pmod; a.pmod_s = pl->d_pmod_s;
     a.l = pl->l; a.alpha = pl->alpha; a.beta = pl->beta; a.ext = pl->ext; a.evk_ext = pl->evk_ext;
     a.n = pl->n; a.lg = log2u(pl->n);
@@ -994,13 +1003,29 @@ int ckks_bsgs_inner(ckks_ctx* ctx, int32_t plan, const uint32_t* raised, const u
         if (a.k[b] && !a.evk[b]) { set_last_error("bsgs_inner: rotation %d has no key", b); return CKKS_ERR_ARG; }
     }
     for (int g = 0; g < ng; ++g) {
-        a.out[g] = out[g];
+        for (int c = 0; c < batch; ++c) {
+            a.out[c][g] = out[(size_t)c * ng + g];
+            if (!a.out[c][g]) { set_last_error("bsgs_inner: null output (%d, %d)", c, g); return CKKS_ERR_ARG; }
+        }
         for (int b = 0; b < nb; ++b) {
             a.p[g][b] = p[(size_t)g * nb + b] ? p[(size_t)g * nb + b] : zero;
             if (!a.p[g][b]) { set_last_error("bsgs_inner: absent diagonal (%d, %d) but no zero plaintext given", g, b); return CKKS_ERR_ARG; }
         }
     }
     return bsgs_inner_launch(a, ctx->d_slots, (cudaStream_t)stream);
+}
+
+int ckks_bsgs_inner(ckks_ctx* ctx, int32_t plan, const uint32_t* raised, const uint32_t* ct_a,
+                    const uint32_t* ct_b, int nb, const uint32_t* k, const uint32_t* const* evk, int ng,
+                    const uint32_t* const* p, const uint32_t* zero, uint32_t* const* out, void* stream) {
+    return bsgs_inner_core(ctx, plan, 1, &raised, &ct_a, &ct_b, nb, k, evk, ng, p, zero, out, stream);
+}
+
+int ckks_bsgs_inner_batch(ckks_ctx* ctx, int32_t plan, int batch, const uint32_t* const* raised,
+                          const uint32_t* const* ct_a, const uint32_t* const* ct_b, int nb, const uint32_t* k,
+                          const uint32_t* const* evk, int ng, const uint32_t* const* p, const uint32_t* zero,
+                          uint32_t* const* out, void* stream) {
+    return bsgs_inner_core(ctx, plan, batch, raised, ct_a, ct_b, nb, k, evk, ng, p, zero, out, stream);
 }
 
 // Relinearisation (or any key switch) fused with the rescale that follows it: the

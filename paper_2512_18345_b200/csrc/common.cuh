@@ -64,27 +64,26 @@ __device__ __forceinline__ uint32_t redc(uint32_t lo, uint32_t hi, uint32_t q, u
     return min(r, r + q);
 }
 
-// x mod q for any 64-bit x.  Fast moduli: fold hi into [0, q), REDC, then
-// multiply by 2^32 mod q to undo the Montgomery factor.
+// x mod q for any 64-bit x.  Fast moduli (2^30 < q < 2^31): x = hi * 2^32 + lo, so
+// x = hi * (2^32 mod q) + lo (mod q): one lazy Shoup product (valid for any 32-bit hi) and
+// conditional subtractions -- 1 IMAD.HI + 2 IMAD on the multiplier pipe.  (Rounds 1-2 used a
+// Montgomery REDC followed by a Shoup multiplication by 2^32 mod q to cancel its factor: 2 IMAD.HI
+// + 3 IMAD for the same canonical residue.)
 __device__ __forceinline__ uint32_t reduce64(uint64_t x, const ModSlot& m) {
     if (m.fast) {
-        uint32_t lo = (uint32_t)x, hi = (uint32_t)(x >> 32);
-        hi = min(hi, hi - 2u * m.q);     // hi < 2^32 < 4q
-        hi = csub(hi, m.q);
-        uint32_t r = redc(lo, hi, m.q, m.qinv);
-        return shoup_mul(r, m.r1, m.r1s, m.q);
+        uint32_t lo = (uint32_t)x;
+        const uint32_t hi = (uint32_t)(x >> 32);
+        const uint32_t t = shoup_mul(hi, m.r1, m.r1s, m.q);     // hi * 2^32 mod q, canonical
+        lo = min(lo, lo - 2u * m.q);                             // lo < 2^32 < 4q
+        lo = csub(lo, m.q);
+        return csub(t + lo, m.q);
     }
     return (uint32_t)(x % m.q);
 }
 
 // a * b mod q for canonical a, b.
 __device__ __forceinline__ uint32_t mul_mod(uint32_t a, uint32_t b, const ModSlot& m) {
-    if (m.fast) {
-        uint64_t x = (uint64_t)a * b;                 // < q^2 < q * 2^32: hi < q
-        uint32_t r = redc((uint32_t)x, (uint32_t)(x >> 32), m.q, m.qinv);
-        return shoup_mul(r, m.r1, m.r1s, m.q);
-    }
-    return (uint32_t)(((uint64_t)a * b) % m.q);
+    return reduce64((uint64_t)a * b, m);
 }
 
 // Source column of output column t under the evaluation-domain automorphism X -> X^k

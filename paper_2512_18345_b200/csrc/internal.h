@@ -227,10 +227,17 @@ struct ModDownEpilogueArgs {
 // ciphertext (inner product of the raised digits with key b, P * sigma(ct_b) lifted in; k_b = 0:
 // the ciphertext itself on the Q rows) is formed in registers and immediately multiplied into
 // out[g] += p[g][b] (.) u_b.  The u_b are never written.
+constexpr int kMaxBsgsBatch = 2;
 struct BsgsInnerArgs {
-    const uint32_t* raised;                     // [beta][ext][n]
-    const uint32_t* ct_a;                       // [l][n]
-    const uint32_t* ct_b;                       // [l][n]
+    // `batch` independent ciphertexts at the same level go through the same keys and diagonals in
+    // ONE launch (CTAs of 128 * batch threads: every key / plaintext slice is fetched into shared
+    // memory once and multiplied into each ciphertext's sums: the L2-aware multi-polynomial grouping
+    // of the paper, PAPER.md "scheduling", done inside the kernel).  Element c uses raised[c],
+    // ct_a[c], ct_b[c] and out[c][*].
+    int batch;
+    const uint32_t* raised[kMaxBsgsBatch];      // [beta][ext][n]
+    const uint32_t* ct_a[kMaxBsgsBatch];        // [l][n]
+    const uint32_t* ct_b[kMaxBsgsBatch];        // [l][n]
     const int32_t* ext_slot;                    // [ext]
     const int32_t* evk_row;                     // [ext]
     const uint32_t* pmod;                       // [l]  P mod q_i
@@ -241,7 +248,7 @@ struct BsgsInnerArgs {
     uint32_t k[kMaxTerms];                      // automorphism index of baby step b (0: none)
     const uint32_t* evk[kMaxTerms];             // its switching key [beta_total][2][evk_ext][n] (unused for k = 0)
     const uint32_t* p[kMaxGiants][kMaxTerms];   // plaintext diagonal over Q||P, or `zero`
-    uint32_t* out[kMaxGiants];                  // [2][ext][n]
+    uint32_t* out[kMaxBsgsBatch][kMaxGiants];   // [2][ext][n] each
 };
 int bsgs_inner_launch(const BsgsInnerArgs& a, const ModSlot* slots, cudaStream_t st);
 

@@ -301,8 +301,8 @@ bsgs_inner_kernel(BsgsInnerArgs p, const ModSlot* __restrict__ slots) {
         if (k == 0) {
             // the unrotated term: the ciphertext on the Q rows (its plaintext carries the factor P)
             if (qrow) {
-                const uint2 av = *reinterpret_cast<const uint2*>(p.ct_a + at);
-                const uint2 bv = *reinterpret_cast<const uint2*>(p.ct_b + at);
+                const uint2 av = *reinterpret_cast<const uint2*>(p.ct_a[0] + at);
+                const uint2 bv = *reinterpret_cast<const uint2*>(p.ct_b[0] + at);
                 ra[0] = av.x; ra[1] = av.y; rb[0] = bv.x; rb[1] = bv.y;
             } else {
                 ra[0] = ra[1] = rb[0] = rb[1] = 0;
@@ -312,7 +312,7 @@ bsgs_inner_kernel(BsgsInnerArgs p, const ModSlot* __restrict__ slots) {
             uint64_t ta[2] = {0, 0}, tb[2] = {0, 0};
 #pragma unroll
             for (int t = 0; t < BETA; ++t) {
-                const uint32_t* dsrc = p.raised + ((size_t)t * p.ext + row) * n;
+                const uint32_t* dsrc = p.raised[0] + ((size_t)t * p.ext + row) * n;
                 const uint32_t d0 = dsrc[g0], d1 = dsrc[g1];
                 const uint2 xa = *slot(stage, 2 * t), xb = *slot(stage, 2 * t + 1);
                 ta[0] = mad64(d0, xa.x, ta[0]); ta[1] = mad64(d1, xa.y, ta[1]);
@@ -321,7 +321,7 @@ bsgs_inner_kernel(BsgsInnerArgs p, const ModSlot* __restrict__ slots) {
             ra[0] = reduce64(ta[0], m); ra[1] = reduce64(ta[1], m);
             rb[0] = reduce64(tb[0], m); rb[1] = reduce64(tb[1], m);
             if (qrow) {
-                const uint32_t* bsrc = p.ct_b + (size_t)row * n;
+                const uint32_t* bsrc = p.ct_b[0] + (size_t)row * n;
                 rb[0] = add_mod(rb[0], shoup_mul(bsrc[g0], pm, pms, m.q), m.q);
                 rb[1] = add_mod(rb[1], shoup_mul(bsrc[g1], pm, pms, m.q), m.q);
             }
@@ -343,7 +343,7 @@ bsgs_inner_kernel(BsgsInnerArgs p, const ModSlot* __restrict__ slots) {
     }
 #pragma unroll
     for (int g = 0; g < NG; ++g) {
-        uint32_t* o = p.out[g];
+        uint32_t* o = p.out[0][g];
         *reinterpret_cast<uint2*>(o + at) = make_uint2(reduce64(sa[g][0], m), reduce64(sa[g][1], m));
         *reinterpret_cast<uint2*>(o + half + at) = make_uint2(reduce64(sb[g][0], m), reduce64(sb[g][1], m));
     }
@@ -359,14 +359,19 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst_smem, const void* src, uin
                  :: "r"(dst_smem), "l"(src), "r"(bytes), "r"(bar), "l"(pol) : "memory");
 }
 
-template <int NG, int BETA>
-__global__ void __launch_bounds__(kBsgsThreads)
+template <int NG, int BETA, int BATCH>
+__global__ void __launch_bounds__(kBsgsThreads * BATCH)
 bsgs_inner_tma_kernel(BsgsInnerArgs p, const ModSlot* __restrict__ slots) {
     const int row = blockIdx.y;
     const ModSlot m = slots[p.ext_slot[row]];
     const size_t n = p.n;
     const size_t i0 = (size_t)blockIdx.x * kBsgsThreads * 2;           // first column of this CTA
-    const size_t i = i0 + (size_t)threadIdx.x * 2;
+    const int tx = threadIdx.x % kBsgsThreads;                         // column pair within the CTA's slice
+    const int cb = BATCH == 1 ? 0 : threadIdx.x / kBsgsThreads;        // which ciphertext of the batch
+    const size_t i = i0 + (size_t)tx * 2;
+    const uint32_t* __restrict__ raised = p.raised[cb];
+    const uint32_t* __restrict__ ct_a = p.ct_a[cb];
+    const uint32_t* __restrict__ ct_b = p.ct_b[cb];
     const size_t erow = (size_t)p.evk_row[row];
     const bool qrow = row < p.l;
     const uint32_t pm = qrow ? p.pmod[row] : 0u, pms = qrow ? p.pmod_s[row] : 0u;
@@ -390,7 +395,7 @@ bsgs_inner_tma_kernel(BsgsInnerArgs p, const ModSlot* __restrict__ slots) {
     uint64_t sa[NG][2], sb[NG][2];
 #pragma unroll
     for (int g = 0; g < NG; ++g) sa[g][0] = sa[g][1] = sb[g][0] = sb[g][1] = 0;
-    auto slot = [&](int stage, int item) -> const uint2* { return s_pipe + ((size_t)(stage * ITEMS + item) * kBsgsThreads + threadIdx.x); };
+    auto slot = [&](int stage, int item) -> const uint2* { return s_pipe + ((size_t)(stage * ITEMS + item) * kBsgsThreads + tx); };
     auto request = [&](int b) {
         if (threadIdx.x != 0 || b >= p.nb) return;
         const int stage = b % kBsgsStages;
@@ -425,8 +430,8 @@ bsgs_inner_tma_kernel(BsgsInnerArgs p, const ModSlot* __restrict__ slots) {
         const uint32_t k = p.k[b];
         if (k == 0) {
             if (qrow) {
-                const uint2 av = *reinterpret_cast<const uint2*>(p.ct_a + at);
-                const uint2 bv = *reinterpret_cast<const uint2*>(p.ct_b + at);
+                const uint2 av = *reinterpret_cast<const uint2*>(ct_a + at);
+                const uint2 bv = *reinterpret_cast<const uint2*>(ct_b + at);
                 ra[0] = av.x; ra[1] = av.y; rb[0] = bv.x; rb[1] = bv.y;
             } else {
                 ra[0] = ra[1] = rb[0] = rb[1] = 0;
@@ -436,7 +441,7 @@ bsgs_inner_tma_kernel(BsgsInnerArgs p, const ModSlot* __restrict__ slots) {
             uint64_t ta[2] = {0, 0}, tb[2] = {0, 0};
 #pragma unroll
             for (int t = 0; t < BETA; ++t) {
-                const uint32_t* dsrc = p.raised + ((size_t)t * p.ext + row) * n;
+                const uint32_t* dsrc = raised + ((size_t)t * p.ext + row) * n;
                 const uint32_t d0 = dsrc[g0], d1 = dsrc[g1];
                 const uint2 xa = *slot(stage, 2 * t), xb = *slot(stage, 2 * t + 1);
                 ta[0] = mad64(d0, xa.x, ta[0]); ta[1] = mad64(d1, xa.y, ta[1]);
@@ -445,7 +450,7 @@ bsgs_inner_tma_kernel(BsgsInnerArgs p, const ModSlot* __restrict__ slots) {
             ra[0] = reduce64(ta[0], m); ra[1] = reduce64(ta[1], m);
             rb[0] = reduce64(tb[0], m); rb[1] = reduce64(tb[1], m);
             if (qrow) {
-                const uint32_t* bsrc = p.ct_b + (size_t)row * n;
+                const uint32_t* bsrc = ct_b + (size_t)row * n;
                 rb[0] = add_mod(rb[0], shoup_mul(bsrc[g0], pm, pms, m.q), m.q);
                 rb[1] = add_mod(rb[1], shoup_mul(bsrc[g1], pm, pms, m.q), m.q);
             }
@@ -466,7 +471,7 @@ bsgs_inner_tma_kernel(BsgsInnerArgs p, const ModSlot* __restrict__ slots) {
     }
 #pragma unroll
     for (int g = 0; g < NG; ++g) {
-        uint32_t* o = p.out[g];
+        uint32_t* o = p.out[cb][g];
         *reinterpret_cast<uint2*>(o + at) = make_uint2(reduce64(sa[g][0], m), reduce64(sa[g][1], m));
         *reinterpret_cast<uint2*>(o + half + at) = make_uint2(reduce64(sb[g][0], m), reduce64(sb[g][1], m));
     }
@@ -479,10 +484,18 @@ static int bsgs_launch_one(const BsgsInnerArgs& a, const ModSlot* slots, dim3 gr
     // degrees that are not a multiple of a CTA's 256 columns).  Measured at ks48: 400 vs 430 us per launch
     // run eagerly, equal inside the bootstrap graph.
     static const bool tma = [] { const char* e = getenv("CKKS_BSGS_TMA"); return !(e && e[0] == '0'); }();
+    if (a.batch == 2) {
+        // two ciphertexts per CTA share the staged key / plaintext slices (bulk-copy pipeline only)
+        if (a.n % (2 * kBsgsThreads) != 0) { set_last_error("batched bsgs_inner needs n %% 256 == 0"); return CKKS_ERR_UNSUPPORTED; }
+        if (sm > 48 * 1024)
+            CK(cudaFuncSetAttribute(bsgs_inner_tma_kernel<NG, BETA, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+        CK(launch_pdl(bsgs_inner_tma_kernel<NG, BETA, 2>, grid, dim3(2 * kBsgsThreads), sm, st, a, slots));
+        return CKKS_OK;
+    }
     if (tma && a.n % (2 * kBsgsThreads) == 0) {
         if (sm > 48 * 1024)
-            CK(cudaFuncSetAttribute(bsgs_inner_tma_kernel<NG, BETA>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-        CK(launch_pdl(bsgs_inner_tma_kernel<NG, BETA>, grid, dim3(kBsgsThreads), sm, st, a, slots));
+            CK(cudaFuncSetAttribute(bsgs_inner_tma_kernel<NG, BETA, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+        CK(launch_pdl(bsgs_inner_tma_kernel<NG, BETA, 1>, grid, dim3(kBsgsThreads), sm, st, a, slots));
         return CKKS_OK;
     }
     if (sm > 48 * 1024)
@@ -504,15 +517,16 @@ static int bsgs_dispatch(const BsgsInnerArgs& a, const ModSlot* slots, dim3 grid
 }
 
 int bsgs_inner_launch(const BsgsInnerArgs& a, const ModSlot* slots, cudaStream_t st) {
-    if (a.n % 2 || a.nb < 1 || a.nb > kMaxTerms || a.ng < 1 || a.ng > kMaxGiants) {
-        set_last_error("bsgs_inner needs even n, 1..%d baby steps, 1..%d giant steps", kMaxTerms, kMaxGiants);
+    if (a.n % 2 || a.nb < 1 || a.nb > kMaxTerms || a.ng < 1 || a.ng > kMaxGiants || a.batch < 1 || a.batch > kMaxBsgsBatch) {
+        set_last_error("bsgs_inner needs even n, 1..%d baby steps, 1..%d giant steps, 1..%d ciphertexts", kMaxTerms, kMaxGiants, kMaxBsgsBatch);
         return CKKS_ERR_UNSUPPORTED;
     }
     int keyed = 0;
     for (int b = 0; b < a.nb; ++b) keyed += a.k[b] ? 1 : 0;
     // keys + plaintexts + outputs (+ the ciphertext once); raised digits are re-read through L2
-    const double limbs = (double)a.ext * (2.0 * a.beta * keyed + (double)a.nb * a.ng + 2.0 * a.ng) + 2.0 * a.l;
-    ProfScope ps("bsgs_inner", st, 4.0 * a.n * limbs);
+    // (a batch shares the keys and plaintexts: only the outputs and the ciphertexts scale with it)
+    const double limbs = (double)a.ext * (2.0 * a.beta * keyed + (double)a.nb * a.ng + 2.0 * a.ng * a.batch) + 2.0 * a.l * a.batch;
+    ProfScope ps(a.batch > 1 ? "bsgs_inner_batch" : "bsgs_inner", st, 4.0 * a.n * limbs);
     dim3 grid((unsigned)((a.n / 2 + kBsgsThreads - 1) / kBsgsThreads), a.ext);
     int rc = CKKS_ERR_UNSUPPORTED;
     switch (a.ng) {

@@ -443,6 +443,35 @@ class Engine:
                                             nb, kk, ep, ng, pp, zero, op, self.stream()))
         return outs
 
+    def bsgs_inner_batch(self, plan: int, raised, ct_a, ct_b, ks, evks, table, ext: int):
+        """bsgs_inner for a batch of independent ciphertexts at the same level (lists `raised`, `ct_a`,
+        `ct_b`) through the same keys and diagonals: pairs go through ONE launch that stages every key
+        and plaintext slice once for both (ckks_bsgs_inner_batch); results equal the single calls bit
+        for bit.  Returns one list of [2, ext, n] accumulators per ciphertext."""
+        count = len(raised)
+        n = ct_a[0].shape[1]
+        if count == 1 or n % 256:
+            return [self.bsgs_inner(plan, raised[c], ct_a[c], ct_b[c], ks, evks, table, ext) for c in range(count)]
+        nb, ng = len(ks), len(table)
+        kk = (ctypes.c_uint32 * nb)(*ks)
+        ep = (ctypes.c_void_p * nb)(*[None if e is None else e.data_ptr() for e in evks])
+        flat = [None if pt is None else pt.data_ptr() for row in table for pt in row]
+        pp = (ctypes.c_void_p * (nb * ng))(*flat)
+        zero = self._zero_plain(ext, n).data_ptr() if any(f is None for f in flat) else None
+        res = []
+        for c0 in range(0, count, 2):
+            group = list(range(c0, min(c0 + 2, count)))
+            if len(group) == 1:
+                res.append(self.bsgs_inner(plan, raised[c0], ct_a[c0], ct_b[c0], ks, evks, table, ext))
+                continue
+            bigs = [self.empty(ng, 2, ext, n) for _ in group]
+            ptrs = lambda ts: (ctypes.c_void_p * len(group))(*[ts[c].data_ptr() for c in group])
+            op = (ctypes.c_void_p * (len(group) * ng))(*[big[g].data_ptr() for big in bigs for g in range(ng)])
+            _lib.check(self.lib.ckks_bsgs_inner_batch(self.ctx, plan, len(group), ptrs(raised), ptrs(ct_a), ptrs(ct_b),
+                                                      nb, kk, ep, ng, pp, zero, op, self.stream()))
+            res.extend([[big[g] for g in range(ng)] for big in bigs])
+        return res
+
     def ks_relin_rescale(self, ks_plan: int, md_plan: int, d, evk, out_rows: int):
         """d = [3, l, n] tensor product (d0, d1, d2) -> rescaled relinearised ciphertext [2, out_rows, n]."""
         out = self.empty(2, out_rows, d.shape[2])

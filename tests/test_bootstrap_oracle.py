@@ -84,3 +84,52 @@ def test_cuda_bootstrap_equals_oracle(name, bar):
         assert phases[nm] == rec["phases"][nm], f"CUDA and oracle limbs differ after {nm}"
     assert ckks.level_of(o_out) == rec["out_level"]
     check_against_committed(name, rec)
+
+
+def test_oracle_bootstrap_batch_equals_single_bootstraps():
+    """bootstrap_batch (BASELINE config 5: independent bootstraps in one batch) is the same circuit per
+    ciphertext: on the CPU oracle two inputs through the batch give the limbs of two single runs."""
+    from paper_2512_18345_b200.bootstrap import standard_input, standard_setup
+
+    def run():
+        spec, h_dense = G.CASES["n2048"]
+        p = G.load_params(spec)
+        sk, _sparse, boot = standard_setup(p, h_dense=h_dense)
+        cts = [standard_input(p, boot, sk, i)[1] for i in range(2)]
+        singles = [G.ct_digest(boot.bootstrap(ct)) for ct in cts]
+        batch = [G.ct_digest(out) for out in boot.bootstrap_batch(cts)]
+        return singles, batch
+
+    singles, batch = with_oracle(run)
+    assert singles == batch
+    assert singles[0] != singles[1]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["n2048", "ks48"])
+def test_cuda_bootstrap_batch_equals_single_bootstraps(name):
+    """The batched graph (two bootstraps on 16 lanes, every rotation key and diagonal of the six
+    linear transforms read once for the pair: ckks_bsgs_inner_batch) returns, for each input, exactly
+    the limbs of that input's own bootstrap -- which test_cuda_bootstrap_equals_oracle pins to the
+    CPU oracle."""
+    import torch
+
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    from paper_2512_18345_b200.bootstrap import standard_input, standard_setup
+    from paper_2512_18345_b200.engine import get_engine
+
+    eng = get_engine()
+    spec, h_dense = G.CASES[name]
+    p = G.load_params(spec)
+    sk, _sparse, boot = standard_setup(p, h_dense=h_dense)
+    cts = [standard_input(p, boot, sk, i)[1] for i in range(3)]
+    eng.set_lanes(1)
+    singles = [G.ct_digest(boot.bootstrap(ct)) for ct in cts]
+    eager = [G.ct_digest(out) for out in boot.bootstrap_batch(cts)]          # a pair and an odd one
+    assert eager == singles
+    eng.set_lanes(16)
+    replay = boot.capture_batch(cts[:2])
+    outs = replay([cts[1], cts[2]])
+    torch.cuda.synchronize()
+    assert [G.ct_digest(o) for o in outs] == [singles[1], singles[2]]
+    eng.set_lanes(1)
