@@ -30,6 +30,13 @@ namespace ckks {
 // l_in * chunk MACs, so chunks stay >= 8 limbs).
 constexpr int kTargetCtas = 148 * 8;
 constexpr int kMinChunk = 8;
+// Doubles of padding per row of the tensor kernel's shared table.  KP2 + 4 doubles per row removes every
+// bank conflict of the A-fragment loads (1.18 M -> 2 k per full-size ModUp in ncu) and is SLOWER (32.0 /
+// 21.1 us against 30.0 / 16.6 us for the two conversions of a ks48 key switch, measured twice): kept at 0.
+#ifndef CKKS_BCONV_TABLE_PAD
+#define CKKS_BCONV_TABLE_PAD 0
+#endif
+constexpr int kBconvTablePad = CKKS_BCONV_TABLE_PAD;
 
 static int out_chunk(size_t ctas_xy, int l_out_max) {
     int z = (int)((kTargetCtas + ctas_xy - 1) / ctas_xy);
@@ -198,8 +205,12 @@ bconv_f64(BconvJobs jobs, const ModSlot* __restrict__ slots, size_t cols, int ch
 // y = y1 * 2^16 + y0 and T * y = T * y0 + (T * 2^16 mod p) * y1 (mod p), the second table
 // precomputed (BconvDev::t_f64k): the two halves of y are stacked along K, every term is below
 // 2^47 resp. 2^46, at most 16 + 16 of them, so the WHOLE contraction is an integer below 2^52.
-// It is formed in two chains (seeded 2^52 and 0, four DMMAs in flight per warp) whose sum is
-// exact, sits in the mantissa, and goes through ONE REDC against the Montgomery-form table.
+// It is formed in two chains (four DMMAs in flight per warp) of SUBNORMAL doubles (sub2d above): the
+// chains' bit patterns are the integer partial sums, added on the integer pipe, and the total goes
+// through ONE REDC against the Montgomery-form table.  (Until round 2 the operands were ordinary
+// doubles, one chain seeded with 2^52 and the chains joined by an FP64 add: per 8 x 16 output tile
+// that put 4 DADDs and, per column tile, 12 conversion DADDs on the FP64 pipe between the DMMAs;
+// ncu's source view showed those DADDs stalled on the math pipe as long as the DMMAs themselves.)
 // (Round 1 kept two 2^52-seeded sums and recombined them with a 64-bit multiply by 2^48 mod p;
 // the stacked form has the same DMMA count and a third of the epilogue, measured equal in time:
 // 29.4 us at the full-size ModUp either way -- the kernel is not bound by its integer work.)
@@ -217,6 +228,16 @@ __device__ __forceinline__ void dmma884(double (&c)[2], double a, double b) {
 // exact u32 (< 2^32) -> double without the slow I2F path
 __device__ __forceinline__ double u2d(uint32_t x) {
     return __hiloint2double(0x43300000, (int)x) - 4503599627370496.0;
+}
+
+// x * 2^-1074: the SUBNORMAL double whose bit pattern is the integer x (no instruction at all: a
+// register pair {x, 0}).  FP64 arithmetic never flushes subnormals, and below 2^-1022 a double is a
+// 52-bit fixed-point number: with the residues' 16-bit halves fed to the tensor pipe in this form the
+// products T * y * 2^-1074 (T * y < 2^47) and their sums (< 2^52) are exact and the accumulator's bit
+// pattern is the integer sum itself -- no 2^52 seed, no conversion add per operand, no mask and no FP64
+// add per output on the pipe that bounds this kernel.
+__device__ __forceinline__ double sub2d(uint32_t x) {
+    return __hiloint2double(0, (int)x);
 }
 
 template <int KS>
@@ -249,18 +270,30 @@ bconv_dmma(BconvJobs jobs, const ModSlot* __restrict__ slots, size_t cols, int c
     pdl_trigger();
     // operands come ready-made from the table (api.cu): one level of loads, no arithmetic
     constexpr int KP2 = 2 * KP;                                            // the two halves of y stacked along K
-    double* s_t = reinterpret_cast<double*>(sm4);                          // [rows_pad][KP2]  {T | T * 2^16 mod p}
-    uint4* s_om = sm4 + ((size_t)((chunk + 7) & ~7) * KP2 * sizeof(double)) / sizeof(uint4);  // {q, qinv, out row, -}
+    constexpr int TS = KP2 + kBconvTablePad;
+    double* s_t = reinterpret_cast<double*>(sm4);                          // [rows_pad][TS]  {T | T * 2^16 mod p | pad}
+    uint4* s_om = sm4 + ((size_t)((chunk + 7) & ~7) * TS * sizeof(double)) / sizeof(uint4);  // {q, qinv, out row, -}
     uint4* s_in = s_om + ((chunk + 7) & ~7);                               // {q, inv_qhat, shoup(inv_qhat), -}
     {
-        // a conversion with fewer input limbs than the launch's KP (the partial last digit stacked
-        // with the full ones) has a narrower table: zero-fill the extra columns
         const int kpj = job.tab.kp;
         const double* src = job.tab.t_f64k + (size_t)i_lo * 2 * kpj;
-        for (int idx = threadIdx.x; idx < rows_pad * KP2; idx += blockDim.x) {
-            const int i = idx / KP2, c = idx - i * KP2;
-            const int half = c >= KP ? 1 : 0, k = c - half * KP;
-            s_t[idx] = k < kpj ? src[(size_t)i * 2 * kpj + half * kpj + k] : 0.0;
+        if (kpj == KP) {
+            // the CTA's rows of the table are one contiguous block: asynchronous 16-byte copies straight
+            // into shared memory, in flight while the residues are fetched (no register round trip)
+            const uint32_t dst = (uint32_t)__cvta_generic_to_shared(s_t);
+            for (int idx = threadIdx.x; idx < rows_pad * KP; idx += blockDim.x) {
+                const int i = idx / KP, c = idx - i * KP;             // 16-byte chunk c of row i
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;"
+                             :: "r"(dst + (uint32_t)(i * TS * 8 + 16 * c)), "l"(src + 2 * idx) : "memory");
+            }
+        } else {
+            // a conversion with fewer input limbs than the launch's KP (the partial last digit stacked
+            // with the full ones) has a narrower table: zero-fill the extra columns
+            for (int idx = threadIdx.x; idx < rows_pad * KP2; idx += blockDim.x) {
+                const int i = idx / KP2, c = idx - i * KP2;
+                const int half = c >= KP ? 1 : 0, k = c - half * KP;
+                s_t[i * TS + c] = k < kpj ? src[(size_t)i * 2 * kpj + half * kpj + k] : 0.0;
+            }
         }
     }
     for (int r = threadIdx.x; r < rows_pad; r += blockDim.x) {
@@ -272,9 +305,9 @@ bconv_dmma(BconvJobs jobs, const ModSlot* __restrict__ slots, size_t cols, int c
         s_in[k] = k < job.tab.kp ? job.tab.inc[k] : make_uint4(3u, 0u, 0u, 0u);
     pdl_wait();                                 // tables are static; the residues are not
     if (tile < tiles) fetch(tile);
+    asm volatile("cp.async.wait_all;" ::: "memory");
     __syncthreads();
     if (tile >= tiles) return;
-    const double seed = 4503599627370496.0;     // 2^52
     for (; tile < tiles; tile += warps) {
         // B fragments: lane (kk, cc) holds y[4j + kk][16 tile + 8t + cc], split in 16-bit halves
         double y0[2][KS], y1[2][KS];
@@ -284,8 +317,8 @@ bconv_dmma(BconvJobs jobs, const ModSlot* __restrict__ slots, size_t cols, int c
 #pragma unroll
             for (int t = 0; t < 2; ++t) {
                 const uint32_t y = 4 * j + kk < l_in ? shoup_mul(raw[t][j], im.y, im.z, im.x) : 0u;
-                y0[t][j] = u2d(y & 0xFFFFu);
-                y1[t][j] = u2d(y >> 16);
+                y0[t][j] = sub2d(y & 0xFFFFu);
+                y1[t][j] = sub2d(y >> 16);
             }
         }
         const size_t c_base = tile * 16;
@@ -294,14 +327,14 @@ bconv_dmma(BconvJobs jobs, const ModSlot* __restrict__ slots, size_t cols, int c
             double a0[KS], a1[KS];
 #pragma unroll
             for (int j = 0; j < KS; ++j) {
-                a0[j] = s_t[(m0 + cc) * KP2 + 4 * j + kk];
-                a1[j] = s_t[(m0 + cc) * KP2 + KP + 4 * j + kk];
+                a0[j] = s_t[(m0 + cc) * TS + 4 * j + kk];
+                a1[j] = s_t[(m0 + cc) * TS + KP + 4 * j + kk];
             }
             // two chains per column tile (low / high half of y) keep four DMMAs in flight; their sum is
             // the whole contraction, an integer below 2^52 on top of the 2^52 seed of c0
             double c0[2][2], c1[2][2];
 #pragma unroll
-            for (int t = 0; t < 2; ++t) { c0[t][0] = c0[t][1] = seed; c1[t][0] = c1[t][1] = 0.0; }
+            for (int t = 0; t < 2; ++t) { c0[t][0] = c0[t][1] = 0.0; c1[t][0] = c1[t][1] = 0.0; }
 #pragma unroll
             for (int j = 0; j < KS; ++j) {
 #pragma unroll
@@ -319,8 +352,10 @@ bconv_dmma(BconvJobs jobs, const ModSlot* __restrict__ slots, size_t cols, int c
                     uint32_t r[2];
 #pragma unroll
                     for (int e = 0; e < 2; ++e) {
-                        // V < 2^52: its high word (< 2^20 < p) and low word go straight through one REDC
-                        const uint64_t v = (uint64_t)__double_as_longlong(c0[t][e] + c1[t][e]) & 0xFFFFFFFFFFFFFull;
+                        // the chains are subnormal doubles: their bit patterns ARE the integer sums, added on the
+                        // integer pipe (no FP64 add, no mask).  V < 2^52: its high word (< 2^20 < p) and low word
+                        // go straight through one REDC
+                        const uint64_t v = (uint64_t)__double_as_longlong(c0[t][e]) + (uint64_t)__double_as_longlong(c1[t][e]);
                         r[e] = redc((uint32_t)v, (uint32_t)(v >> 32), om.x, om.y);
                     }
                     *reinterpret_cast<uint2*>(dst + 8 * t) = make_uint2(r[0], r[1]);
@@ -387,7 +422,7 @@ static int launch_dmma(const BconvJobs& jobs, const ModSlot* slots, size_t cols,
     int z = (int)(((size_t)148 * 6 + ctas_xy - 1) / ctas_xy);
     if (z > z_max) z = z_max;
     const int chunk = (((l_out_max + z - 1) / z) + 7) & ~7;
-    const size_t sm = sizeof(double) * (size_t)chunk * 8 * KS + sizeof(uint4) * ((size_t)chunk + 4 * KS);
+    const size_t sm = sizeof(double) * (size_t)chunk * (8 * KS + kBconvTablePad) + sizeof(uint4) * ((size_t)chunk + 4 * KS);
     dim3 grid(gx, jobs.count, (l_out_max + chunk - 1) / chunk);
     ProfScope ps("bconv", st, jobs_bytes(jobs, cols), jobs_flops(jobs, cols));
     if (sm > 48 * 1024)
