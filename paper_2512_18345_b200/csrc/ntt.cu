@@ -132,12 +132,16 @@ ntt16_fwd_strided(const uint32_t* in, uint32_t* out, const int32_t* __restrict__
     const ModSlot& m = slots[row_slot[blockIdx.y]];
     const uint32_t q = m.q;
     pdl_trigger();
-    for (int i = tid; i < 256; i += 16 * COLS) s_tw[i] = m.fwd[i];
+    // twiddles go through a register and are stored only after the data loads are in flight: the
+    // in-order issue would otherwise serialise the table's latency with the data's
+    static_assert(16 * COLS == 256, "one twiddle pair per thread");
+    const uint2 tw_stage = m.fwd[tid];
     const uint32_t* src = in + rm.in_row(blockIdx.y) * kN16 + blockIdx.x * COLS + c;
     uint32_t v[16];
     pdl_wait();
 #pragma unroll
     for (int k = 0; k < 16; ++k) v[k] = src[(g + 16 * k) * 256];
+    s_tw[tid] = tw_stage;
     __syncthreads();
     // stages 0..3: rows j = g + 16k, group index = k >> (4 - s): uniform twiddles
     ct16(v, q, TW_MUL(s_tw[(1 << s) + gi]));
@@ -164,12 +168,16 @@ ntt16_inv_strided(const uint32_t* in, uint32_t* out, const int32_t* __restrict__
     const ModSlot& m = slots[row_slot[blockIdx.y]];
     const uint32_t q = m.q;
     pdl_trigger();
-    for (int i = tid; i < 256; i += 16 * COLS) s_tw[i] = m.inv[i];
+    // twiddles go through a register and are stored only after the data loads are in flight: the
+    // in-order issue would otherwise serialise the table's latency with the data's
+    static_assert(16 * COLS == 256, "one twiddle pair per thread");
+    const uint2 tw_stage = m.inv[tid];
     const uint32_t* src = in + rm.in_row(blockIdx.y) * kN16 + blockIdx.x * COLS + c;
     uint32_t v[16];
     pdl_wait();
 #pragma unroll
     for (int k = 0; k < 16; ++k) v[k] = src[(16 * g + k) * 256];
+    s_tw[tid] = tw_stage;
     __syncthreads();
     // global stages 8..11 = 256-point GS stages 0..3 on rows j = 16g + k
     gs16(v, q, TW_MUL(s_tw[(16 + g) * (8 >> s) + gi]));
@@ -274,9 +282,10 @@ ntt16_fwd_contig(const uint32_t* in, uint32_t* out, const int32_t* __restrict__ 
     const uint2* __restrict__ fwd = m.fwd;
     // the 16 threads of a 256-block stage that block's table entries themselves: the whole
     // kernel then only needs warp-level synchronisation (a block's exchange is half a warp)
+    uint2 tw_stage = make_uint2(0u, 0u);
     if (e < 15) {
         const int st = 31 - __clz(e + 1);              // local stage, group = e + 1 - 2^st
-        s_blk[blk][e] = fwd[((256 + B) << st) + (e + 1 - (1 << st))];
+        tw_stage = fwd[((256 + B) << st) + (e + 1 - (1 << st))];
     }
     Tw15 tw;
     load_tw15(fwd, (256 + B) * 16 + e, tw);
@@ -284,6 +293,7 @@ ntt16_fwd_contig(const uint32_t* in, uint32_t* out, const int32_t* __restrict__ 
     pdl_wait();
 #pragma unroll
     for (int k = 0; k < 16; ++k) v[k] = src[e + 16 * k];
+    s_blk[blk][e] = tw_stage;                          // stored once the data loads are in flight
     __syncwarp();
     // global stages 8..11: elements e + 16k, slot = (256 + B) * 2^s + group
     ct16(v, q, TW_MUL(s_blk[blk][(1 << s) - 1 + gi]));
@@ -346,11 +356,12 @@ ntt16_inv_contig(const uint32_t* in, uint32_t* out, const int32_t* __restrict__ 
     const uint32_t* src = in + rm.in_row(blockIdx.y) * kN16 + B * 256 + 16 * e;
     const uint2* __restrict__ inv = m.inv;
     pdl_trigger();
+    uint2 tw_stage = make_uint2(0u, 0u);
     if (e < 15) {
         // stage s of 4..7 has (8 >> s) groups
         const int st = e < 8 ? 0 : (e < 12 ? 1 : (e < 14 ? 2 : 3));
         const int off = st == 0 ? 0 : (st == 1 ? 8 : (st == 2 ? 12 : 14));
-        s_blk[blk][e] = inv[(256 + B) * (8 >> st) + (e - off)];
+        tw_stage = inv[(256 + B) * (8 >> st) + (e - off)];
     }
     Tw15 tw;
     load_tw15(inv, (256 + B) * 16 + e, tw);
@@ -363,6 +374,7 @@ ntt16_inv_contig(const uint32_t* in, uint32_t* out, const int32_t* __restrict__ 
 #pragma unroll
         for (int k = 0; k < 8; ++k) v[8 * h + k] = r[k];
     }
+    s_blk[blk][e] = tw_stage;                          // stored once the data loads are in flight
     if (MUL) {
         const uint32_t* src2 = in2 + rm.in_row(blockIdx.y) * kN16 + B * 256 + 16 * e;
 #pragma unroll
@@ -463,10 +475,12 @@ ntt16_fwd_cluster(const uint32_t* in, uint32_t* out, const int32_t* __restrict__
         const uint32_t* f = ep_half ? ep.fold_b : ep.fold_a;
         if (f && !ep.galois) asm volatile("prefetch.global.L2 [%0];" :: "l"(f + ep_at));
     }
-    if (tid < 256) s_tw[tid] = fwd[tid];
+    // table entries go through registers and are stored after the data loads are in flight
+    const uint2 tw_stage = fwd[tid & 255];
+    uint2 blk_stage = make_uint2(0u, 0u);
     if (e < 15) {
         const int st = 31 - __clz(e + 1);
-        s_blk[blk * 16 + e] = fwd[((256 + B) << st) + (e + 1 - (1 << st))];
+        blk_stage = fwd[((256 + B) << st) + (e + 1 - (1 << st))];
     }
     const int c = tid & 31, g = tid >> 5;                    // strided-phase coordinates
     const uint32_t* src = in + rm.in_row(blockIdx.y) * kN16 + rank * 32 + c;
@@ -474,6 +488,8 @@ ntt16_fwd_cluster(const uint32_t* in, uint32_t* out, const int32_t* __restrict__
     pdl_wait();
 #pragma unroll
     for (int k = 0; k < 16; ++k) v[k] = src[(g + 16 * k) * 256];
+    if (tid < 256) s_tw[tid] = tw_stage;
+    s_blk[blk * 16 + e] = blk_stage;
     __syncthreads();
     ct16(v, q, TW_MUL(s_tw[(1 << s) + gi]));                 // stages 0..3, rows g + 16k
 #pragma unroll
@@ -561,11 +577,12 @@ ntt16_inv_cluster(const uint32_t* in, uint32_t* out, const int32_t* __restrict__
     const uint32_t* src = in + rm.in_row(blockIdx.y) * kN16 + B * 256 + 16 * e;
     pdl_trigger();
     cluster_arrive();                                        // (1)
-    if (tid < 256) s_tw[tid] = inv[tid];
+    const uint2 tw_stage = inv[tid & 255];
+    uint2 blk_stage = make_uint2(0u, 0u);
     if (e < 15) {
         const int st = e < 8 ? 0 : (e < 12 ? 1 : (e < 14 ? 2 : 3));
         const int off = st == 0 ? 0 : (st == 1 ? 8 : (st == 2 ? 12 : 14));
-        s_blk[blk * 16 + e] = inv[(256 + B) * (8 >> st) + (e - off)];
+        blk_stage = inv[(256 + B) * (8 >> st) + (e - off)];
     }
     Tw15 tw;
     load_tw15(inv, (256 + B) * 16 + e, tw);
@@ -578,6 +595,8 @@ ntt16_inv_cluster(const uint32_t* in, uint32_t* out, const int32_t* __restrict__
 #pragma unroll
         for (int k = 0; k < 8; ++k) v[8 * h + k] = r[k];
     }
+    if (tid < 256) s_tw[tid] = tw_stage;                     // stored once the data loads are in flight
+    s_blk[blk * 16 + e] = blk_stage;
     if (MUL) {
         const uint32_t* src2 = in2 + rm.in_row(blockIdx.y) * kN16 + B * 256 + 16 * e;
 #pragma unroll
