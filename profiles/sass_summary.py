@@ -3,7 +3,8 @@
 For every kernel: instruction count, the integer / FP64 / tensor / memory opcode classes the hot
 loops are built from, and the Blackwell-specific opcodes the profiling guide asks to look for
 (UTCxMMA = tcgen05.mma, LDTM/STTM = tensor memory, UTMALDG/UTMASTG = tensor TMA, UBLKCP = bulk TMA copy,
-SYNCS = mbarrier, ACQBULK/PREEXIT = PDL,
+SYNCS = mbarrier, UCGABAR = barrier.cluster, ST (generic, not STG / STS) = st.shared::cluster into another
+CTA's shared memory, ACQBULK/PREEXIT = PDL,
 256-bit LDG/STG).  Evidence of what the library is -- and is not -- built from."""
 import collections
 import re
@@ -17,6 +18,7 @@ CLASSES = [
     ("IMAD.MOV/IADD", r"^IMAD\.(MOV|IADD)"), ("VIADDMNMX", r"^VIADDMNMX"), ("IADD3", r"^IADD3"), ("LOP3/SHF", r"^(LOP3|SHF)"),
     ("DMMA", r"^DMMA"), ("DFMA/DADD", r"^(DFMA|DADD|DMUL)"), ("HMMA/IMMA", r"^(HMMA|IMMA)"),
     ("UTCxMMA", r"^UTC.*MMA"), ("LDTM/STTM", r"^(LDTM|STTM)"), ("UTMALDG/STG", r"^UTMA(LDG|STG)"), ("UBLKCP", r"^UBLKCP"), ("SYNCS(mbarrier)", r"^SYNCS"),
+    ("UCGABAR(cluster barrier)", r"^UCGABAR"), ("ST(DSMEM)", r"^ST(\.|$)"),
     ("LDGSTS", r"^LDGSTS"), ("LDG", r"^LDG"), ("LDG.256", r"^LDG.*\.256"), ("STG", r"^STG"), ("STG.256", r"^STG.*\.256"),
     ("LDS", r"^LDS"), ("STS", r"^STS"), ("BAR", r"^BAR"), ("PDL", r"^(ACQBULK|PREEXIT)"), ("SHFL", r"^SHFL"),
 ]
