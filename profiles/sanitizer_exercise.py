@@ -31,6 +31,21 @@ eng.ks_accumulate_rot_qp(plan, a_md[1], qps[1][1], 5, m, False)
 fin = eng.ks_finish(plan, 1, None, None, l, p.n)
 table = [[raw[0] * 0 + 1, None], [None, raw[0] * 0 + 2]]
 bs = eng.bsgs_inner(plan, raised, ct.a.data, ct.b.data, [0, 5], [None, m], table, ext)
+# late round 2: a pair through the batched baby-step kernel; both transform policies (single-pass cluster
+# kernels at 2 and 3 CTAs per SM with their ModDown-epilogue and product-on-load variants, two-kernel split)
+bsb = eng.bsgs_inner_batch(plan, [raised, raised], [ct.a.data, ct.a.data], [ct.b.data, ct.b.data], [0, 5], [None, m], table, ext)
+assert torch.equal(bsb[0][0], bs[0]) and torch.equal(bsb[1][1], bs[1])
+rlk16 = ckks.relin_keygen(s1, p, seed=9)
+ct16 = ckks.Ciphertext(ct.a, ct.b, float(p.delta))
+saved = eng.ntt_policy()
+prods = []
+for pol in ((1 << 20, 2), (1 << 20, 3), (0, 2)):
+    eng.ntt_policy(*pol)
+    prods.append(ckks.hmult_rescale(ct16, ct16, rlk16, 2))
+    x = eng.ntt(ct.a.data, eng.row_slots(q, p.n), True)
+    assert torch.equal(eng.ntt(x, eng.row_slots(q, p.n), False), ct.a.data)
+assert all(torch.equal(pr.a.data, prods[0].a.data) and torch.equal(pr.b.data, prods[0].b.data) for pr in prods)
+eng.ntt_policy(*saved)
 # small-ring transform + config 1 product
 p1 = generate_parameter_set(n=8192, l=12, dnum=3, delta=1 << 40, h_dense=64, h_sparse=32)
 sk = ks.keygen(p1, seed=1); rlk = ckks.relin_keygen(sk, p1, seed=41)
