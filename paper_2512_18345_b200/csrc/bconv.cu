@@ -225,11 +225,6 @@ __device__ __forceinline__ void dmma884(double (&c)[2], double a, double b) {
                  : "+d"(c[0]), "+d"(c[1]) : "d"(a), "d"(b));
 }
 
-// exact u32 (< 2^32) -> double without the slow I2F path
-__device__ __forceinline__ double u2d(uint32_t x) {
-    return __hiloint2double(0x43300000, (int)x) - 4503599627370496.0;
-}
-
 // x * 2^-1074: the SUBNORMAL double whose bit pattern is the integer x (no instruction at all: a
 // register pair {x, 0}).  FP64 arithmetic never flushes subnormals, and below 2^-1022 a double is a
 // 52-bit fixed-point number: with the residues' 16-bit halves fed to the tensor pipe in this form the
