@@ -188,3 +188,41 @@ def test_bsgs_inner_matches_oracle_engine(env, level):
     got, want = run(env.eng), run(OracleEngine())
     for g in range(ng):
         assert np.array_equal(got[g], want[g]), g
+
+
+# ---------------------------------------------------------------- 64-bit reduction at the top of its range
+@pytest.mark.parametrize("count", [1, 3, 4, 5, 8, 13, 16])
+def test_accumulating_kernels_at_the_largest_residues(env, count):
+    """reduce64 (csrc/common.cuh: x mod q as hi * (2^32 mod q) + lo with one lazy Shoup product) fed the
+    largest values its callers can produce: every operand q - 1, so each product is (q-1)^2 = 1 (mod q),
+    four of them plus a carried residue sit just below 2^64 in the fused PMult kernels' accumulators and
+    the inner product sums beta of them.  Expected residues in closed form: the number of terms
+    (poly_elementwise mul / add chains, reference rns.py:243-258; _stage2_accumulate, keyswitch.py:318-332)."""
+    p = env.ks48
+    torch, eng = env.torch, env.eng
+    mods = tuple(p.q_basis[:6]) + tuple(p.p_basis[:2])
+    n = p.n
+    slots = eng.row_slots(mods, n)
+    top = torch.tensor([m.q - 1 for m in mods], dtype=torch.int64, device=eng.device)[:, None].expand(len(mods), n)
+    top32 = top.to(torch.int32).contiguous()                       # q - 1 < 2^31
+    ct = torch.stack([top32, top32]).contiguous()
+    out = eng.fused_terms([ct] * count, [top32] * count, slots)
+    assert bool((out == count).all())
+    multi = eng.fused_terms_multi([ct] * count, [[top32] * count, [top32] + [None] * (count - 1)], slots)
+    assert bool((multi[0] == count).all()) and bool((multi[1] == 1).all())
+    prod = eng.elementwise(top32, top32, slots, 2)
+    assert bool((prod == 1).all())
+
+
+def test_inner_product_at_the_largest_residues(env):
+    """Stage 2 with every raised digit and every key word q - 1: acc = beta * (q-1)^2 = beta (mod q) on
+    both halves and every row of the extended basis (keyswitch.py:318-332)."""
+    p = env.ks48
+    torch, eng = env.torch, env.eng
+    ext = tuple(p.q_basis) + tuple(p.p_basis)
+    plan = env.ks._tables(p).plan()
+    top = torch.tensor([m.q - 1 for m in ext], dtype=torch.int64, device=eng.device)[:, None].expand(len(ext), p.n).to(torch.int32)
+    raised = top.unsqueeze(0).expand(p.dnum, len(ext), p.n).contiguous()
+    evk = top.unsqueeze(0).unsqueeze(0).expand(p.dnum, 2, len(ext), p.n).contiguous()
+    acc = eng.ks_stage2(plan, raised, evk, 0, len(ext))
+    assert bool((acc == p.dnum).all())
