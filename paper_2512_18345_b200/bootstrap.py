@@ -447,7 +447,12 @@ class BootstrapConfig:
     k_bound: int = 12             # |I| <= K for the polynomial's interval.  I is a sum of h + 1 terms
                                   # uniform in [-1/2, 1/2): standard deviation 1.66 at h = 32, K = 12 is
                                   # 7.2 sigma (6e-14 per coefficient); the absolute bound is (h + 1) / 2
-    log_delta_in: int = 52        # input scale 2^log_delta_in at two limbs (Q0 ~ 2^62)
+    log_delta_in: int = 54        # input scale 2^log_delta_in at two limbs (Q0 ~ 2^62).  Errors made before
+                                  # EvalMod return to the message amplified by Q0 * 2^r / (2 pi Delta): every
+                                  # bit of Delta is a bit of precision until the sine's cubic term (Delta |m| /
+                                  # Q0)^2 takes over.  Measured at ks48, slots in the unit square
+                                  # (profiles/boot_delta.py): 2^-17.1 / -19.1 / -21.0 / -22.2 / -18.6 at
+                                  # 50 / 52 / 54 / 56 / 58; 54 keeps a factor 4 of headroom in |m|
     groups: int = 3               # stage groups per linear transform
     n1: int | None = None         # baby-step count (default ~ sqrt of the diagonal span)
 

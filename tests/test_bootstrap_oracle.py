@@ -57,9 +57,10 @@ def test_oracle_bootstrap_n2048_matches_committed_digests():
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("name,bar", [("n2048", -20.0), ("ks48", -18.57)])
+@pytest.mark.parametrize("name,bar", [("n2048", -20.0), ("ks48", -20.0)])
 def test_cuda_bootstrap_equals_oracle(name, bar):
-    """bar: 2^-20 at N = 2^11; at N = 2^16 the paper's reported precision."""
+    """bar: north_star's example tolerance 2^-20 at both sizes (the paper reports 2^-18.57 for its
+    bootstrap at N = 2^16; measured here: 2^-21.9 at N = 2^11, 2^-21.1 at ks48)."""
     import torch
 
     assert torch.cuda.is_available(), "GPU tests need a CUDA device"
