@@ -134,3 +134,31 @@ def test_cuda_bootstrap_batch_equals_single_bootstraps(name):
     torch.cuda.synchronize()
     assert [G.ct_digest(o) for o in outs] == [singles[1], singles[2]]
     eng.set_lanes(1)
+
+
+def test_apply_batch_covers_the_unfused_and_single_paths():
+    """LinearTransform.apply_batch: a batch of one, and a transform whose baby steps are not fused
+    (fuse_baby_steps off: per-rotation accumulators + fused_terms_multi, no batched launch), give what
+    apply() gives per ciphertext (CPU oracle, N = 2^11)."""
+    from paper_2512_18345_b200.bootstrap import standard_input, standard_setup
+
+    def run():
+        spec, h_dense = G.CASES["n2048"]
+        p = G.load_params(spec)
+        sk, _sparse, boot = standard_setup(p, h_dense=h_dense)
+        xs = [boot.mod_raise(standard_input(p, boot, sk, i)[1]) for i in range(2)]
+        lt = boot.cts[0]
+        want = [G.ct_digest(lt.apply(x, boot.keys)) for x in xs]
+        one = [G.ct_digest(c) for c in lt.apply_batch(xs[:1], boot.keys)]
+        both = [G.ct_digest(c) for c in lt.apply_batch(xs, boot.keys)]
+        lt.fuse_baby_steps = False
+        try:
+            unfused = [G.ct_digest(c) for c in lt.apply_batch(xs, boot.keys)]
+        finally:
+            lt.fuse_baby_steps = True
+        return want, one, both, unfused
+
+    want, one, both, unfused = with_oracle(run)
+    assert one == want[:1]
+    assert both == want
+    assert unfused == want
