@@ -438,6 +438,10 @@ __device__ __forceinline__ uint32_t cluster_ctarank() {
 }
 __device__ __forceinline__ void cluster_arrive() { asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory"); }
 __device__ __forceinline__ void cluster_wait() { asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory"); }
+// the first barrier phase only says "every CTA of the cluster is running" (no data is handed over): relaxed,
+// so that it costs no memory fence (the release form compiles to MEMBAR.ALL.GPU + ERRBAR)
+__device__ __forceinline__ void cluster_arrive_relaxed() { asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory"); }
+__device__ __forceinline__ void cluster_wait_relaxed() { asm volatile("barrier.cluster.wait.aligned;" ::: "memory"); }
 __device__ __forceinline__ uint32_t smem_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ uint32_t map_to_rank(uint32_t addr, uint32_t rank) {
     uint32_t r;
@@ -469,7 +473,7 @@ ntt16_fwd_cluster(const uint32_t* in, uint32_t* out, const int32_t* __restrict__
     const size_t ep_g = EPI ? blockIdx.y / ((ep_single ? 1 : 2) * ep.l) : 0;
     const size_t ep_at = (size_t)ep_row * kN16 + B * 256 + 16 * e;
     pdl_trigger();
-    cluster_arrive();                                        // (1) "this CTA is running"
+    cluster_arrive_relaxed();                                // (1) "this CTA is running"
     if (EPI) {
         asm volatile("prefetch.global.L2 [%0];" :: "l"((ep_half ? ep.xq_b : ep.xq_a) + ep_g * ep.xq_stride + ep_at));
         const uint32_t* f = ep_half ? ep.fold_b : ep.fold_a;
@@ -499,7 +503,7 @@ ntt16_fwd_cluster(const uint32_t* in, uint32_t* out, const int32_t* __restrict__
     for (int k = 0; k < 16; ++k) v[k] = tile[(16 * g + k) * 32 + c];
     ct16(v, q, TW_MUL(s_tw[(16 << s) + (g << s) + gi]));     // stages 4..7, rows 16g + k
     // row j = 16g + k is block j of the contiguous phase: it belongs to CTA j / 32 = g / 2
-    cluster_wait();                                          // (1) every CTA of the cluster is running
+    cluster_wait_relaxed();                                  // (1) every CTA of the cluster is running
     {
         const uint32_t at = smem_addr(xbuf + (16 * (g & 1)) * 272 + rank * 32 + c);
         const uint32_t remote = map_to_rank(at, g >> 1);
@@ -576,7 +580,7 @@ ntt16_inv_cluster(const uint32_t* in, uint32_t* out, const int32_t* __restrict__
     const uint32_t B = rank * 32 + blk;
     const uint32_t* src = in + rm.in_row(blockIdx.y) * kN16 + B * 256 + 16 * e;
     pdl_trigger();
-    cluster_arrive();                                        // (1)
+    cluster_arrive_relaxed();                                // (1)
     const uint2 tw_stage = inv[tid & 255];
     uint2 blk_stage = make_uint2(0u, 0u);
     if (e < 15) {
@@ -621,7 +625,7 @@ ntt16_inv_cluster(const uint32_t* in, uint32_t* out, const int32_t* __restrict__
     // element e + 16k of block B is (row B, column e + 16k) of the 256 x 256 view: its column
     // belongs to CTA (e + 16k) / 32 = k / 2.  Rows are stored with the two 16-word halves
     // swapped on odd rows so that the two blocks of a warp hit different banks.
-    cluster_wait();                                          // (1)
+    cluster_wait_relaxed();                                  // (1)
     {
         const uint32_t sw = 16 * (B & 1);
         const uint32_t at0 = smem_addr(xt + B * 32 + (e ^ sw)), at1 = smem_addr(xt + B * 32 + ((e + 16) ^ sw));
