@@ -156,6 +156,13 @@ int ckks_pmult_accumulate(ckks_ctx* ctx, const uint32_t* x, const uint32_t* p, u
  * poly_elementwise "mul", each sum "add", rns.py:243-258). */
 int ckks_fused_terms(ckks_ctx* ctx, int count, const uint32_t* const* x, const uint32_t* const* p,
                      uint32_t* out, const int32_t* row_slot, int rows, size_t cols, void* stream);
+/* The same with the two halves of every term given separately: xa[t], xb[t] are [rows][cols] each
+ * (xb NULL, or xb[t] NULL: the b half follows the a half as in ckks_fused_terms).  For ciphertexts
+ * whose halves are not adjacent -- a ciphertext with limbs dropped keeps them a full level apart --
+ * so that no gathering copy is needed. */
+int ckks_fused_terms_halves(ckks_ctx* ctx, int count, const uint32_t* const* xa, const uint32_t* const* xb,
+                            const uint32_t* const* p, uint32_t* out, const int32_t* row_slot, int rows,
+                            size_t cols, void* stream);
 
 /* All giant-step inner sums of a BSGS linear transform in one pass:
  * out[g] = sum_b x[b] (.) p[g * nb + b] for g < ng <= 8, b < nb <= 16; x[b] and out[g]

@@ -231,14 +231,16 @@ class OracleEngine:
     def fused_terms(self, xs, ps, row_slot, out=None):
         """sum_t xs[t] (.) ps[t] (ps[t] None: the term itself): poly_elementwise mul / add chain."""
         self._tick()
-        n = xs[0].shape[2]
+        halves = lambda x: np.stack([self._np(x[0]), self._np(x[1])]) if isinstance(x, (tuple, list)) else self._np(x)
+        first = halves(xs[0])
+        n = first.shape[2]
         rm = self._rm(row_slot, n)
         rm2 = np.concatenate([rm, rm])
-        rows = xs[0].shape[1]
+        rows = first.shape[1]
         acc = np.zeros((2, rows, n), np.uint32)
         ctx = self._context(n)
         for t, (x, p) in enumerate(zip(xs, ps)):
-            xv = self._np(x)
+            xv = halves(x)
             if p is None:
                 acc = ctx.elementwise(acc.reshape(2 * rows, n), xv.reshape(2 * rows, n), rm2, "add").reshape(2, rows, n)
             else:

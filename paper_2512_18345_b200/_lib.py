@@ -19,7 +19,7 @@ ABI_VERSION = 1
 SYMBOLS = (
     "ckks_abi_version", "ckks_last_error", "ckks_profile_enable", "ckks_profile_read", "ckks_ctx_create", "ckks_ctx_destroy", "ckks_set_lanes", "ckks_select_lane", "ckks_arena_generation", "ckks_arena_reserve",
     "ckks_modulus_register", "ckks_modulus_register_tables", "ckks_modulus_tables", "ckks_ntt", "ckks_ntt_policy", "ckks_ntt_stages",
-    "ckks_elementwise", "ckks_automorphism_eval", "ckks_automorphism_coeff", "ckks_lift2_centered", "ckks_pmult_accumulate", "ckks_fused_terms", "ckks_fused_terms_multi", "ckks_tensor", "ckks_tensor_halves",
+    "ckks_elementwise", "ckks_automorphism_eval", "ckks_automorphism_coeff", "ckks_lift2_centered", "ckks_pmult_accumulate", "ckks_fused_terms", "ckks_fused_terms_halves", "ckks_fused_terms_multi", "ckks_tensor", "ckks_tensor_halves",
     "ckks_bconv_table_create", "ckks_bconv_table_read", "ckks_bconv",
     "ckks_ks_plan_create", "ckks_moddown_plan_create", "ckks_ks_stage1", "ckks_ks_stage2", "ckks_ks_stage3", "ckks_ks_stage3_batch", "ckks_ks_stage3_batch_a", "ckks_keyswitch", "ckks_ks_hoisted", "ckks_ks_hoisted_raw", "ckks_bsgs_inner", "ckks_bsgs_inner_batch", "ckks_ks_relin_rescale", "ckks_hmult_relin_rescale", "ckks_ks_accumulate", "ckks_ks_accumulate_rot", "ckks_ks_accumulate_rot_qp", "ckks_ks_finish", "ckks_ks_finish_rescale",
 )
@@ -79,6 +79,7 @@ def load() -> ctypes.CDLL:
     L.ckks_lift2_centered.argtypes = [vp, vp, i32, i32, vp, vp, ctypes.c_int, sz, vp]
     L.ckks_pmult_accumulate.argtypes = [vp, vp, vp, vp, vp, ctypes.c_int, sz, ctypes.c_int, vp]
     L.ckks_fused_terms.argtypes = [vp, ctypes.c_int, vp, vp, vp, vp, ctypes.c_int, sz, vp]
+    L.ckks_fused_terms_halves.argtypes = [vp, ctypes.c_int, vp, vp, vp, vp, vp, ctypes.c_int, sz, vp]
     L.ckks_fused_terms_multi.argtypes = [vp, ctypes.c_int, ctypes.c_int, vp, vp, vp, vp, vp, ctypes.c_int, sz, vp]
     L.ckks_tensor.argtypes = [vp, vp, vp, vp, vp, ctypes.c_int, sz, vp]
     L.ckks_tensor_halves.argtypes = [vp, vp, vp, vp, vp, vp, vp, ctypes.c_int, sz, vp]

@@ -625,7 +625,7 @@ class Bootstrapper:
         xs = [ckks.mod_drop(x, lq), ckks.mod_drop(x2, lq), x3]
         giants = {1: ckks.mod_drop(x4, lt), 2: ckks.mod_drop(x8, lt), 3: x12}
         slots = eng.row_slots(xs[0].a.basis)
-        xts = [ckks.ct_tensor(v) for v in xs]          # gathered once, read by every baby polynomial
+        xts = [ckks.ct_term(v) for v in xs]            # mod-dropped halves go to the kernel as they lie
 
         def baby(j):
             """q_j at level lq - 2 with the exact scale that makes q_j * x^(4j) land on sigma

@@ -369,6 +369,13 @@ def ct_tensor(ct: Ciphertext):
     return base if base is not None else torch.stack([ct.a.data, ct.b.data])
 
 
+def ct_term(ct: Ciphertext):
+    """A ciphertext as a term of Engine.fused_terms: its [2, l, n] tensor when the halves are adjacent,
+    the pair of halves otherwise (the kernel takes them separately: no gathering copy)."""
+    base = _halves(ct)
+    return base if base is not None else (ct.a.data, ct.b.data)
+
+
 def ct_from_tensor(t, basis, scale) -> Ciphertext:
     return Ciphertext(a=Polynomial(basis, t[0], EVALUATION), b=Polynomial(basis, t[1], EVALUATION), scale=scale)
 

@@ -518,14 +518,20 @@ int ckks_pmult_accumulate(ckks_ctx* ctx, const uint32_t* x, const uint32_t* p, u
     return pmult_acc_launch(x, p, acc, row_slot, ctx->d_slots, rows, cols, first, (cudaStream_t)stream);
 }
 
-int ckks_fused_terms(ckks_ctx* ctx, int count, const uint32_t* const* x, const uint32_t* const* p,
-                     uint32_t* out, const int32_t* row_slot, int rows, size_t cols, void* stream) {
+int ckks_fused_terms_halves(ckks_ctx* ctx, int count, const uint32_t* const* xa, const uint32_t* const* xb,
+                            const uint32_t* const* p, uint32_t* out, const int32_t* row_slot, int rows,
+                            size_t cols, void* stream) {
     CKS(check_ctx(ctx));
-    if (count < 1 || count > kMaxTerms || !x || !p) { set_last_error("term count %d out of range [1, %d]", count, kMaxTerms); return CKKS_ERR_ARG; }
+    if (count < 1 || count > kMaxTerms || !xa || !p) { set_last_error("term count %d out of range [1, %d]", count, kMaxTerms); return CKKS_ERR_ARG; }
     FusedTerms t{};
     t.count = count;
-    for (int i = 0; i < count; ++i) { t.x[i] = x[i]; t.p[i] = p[i]; }
+    for (int i = 0; i < count; ++i) { t.x[i] = xa[i]; t.xb[i] = xb ? xb[i] : nullptr; t.p[i] = p[i]; }
     return fused_terms_launch(t, out, row_slot, ctx->d_slots, rows, cols, (cudaStream_t)stream);
+}
+
+int ckks_fused_terms(ckks_ctx* ctx, int count, const uint32_t* const* x, const uint32_t* const* p,
+                     uint32_t* out, const int32_t* row_slot, int rows, size_t cols, void* stream) {
+    return ckks_fused_terms_halves(ctx, count, x, nullptr, p, out, row_slot, rows, cols, stream);
 }
 
 int ckks_fused_terms_multi(ckks_ctx* ctx, int nb, int ng, const uint32_t* const* x,

@@ -243,7 +243,8 @@ fused_terms_kernel(FusedTerms terms, uint4* out, const int32_t* __restrict__ row
         int pending = 0;
         for (int t = 0; t < terms.count; ++t) {
             const uint4* x = reinterpret_cast<const uint4*>(terms.x[t]);
-            const uint4 xa = x[at], xb = x[half + at];
+            const uint4* xh = terms.xb[t] ? reinterpret_cast<const uint4*>(terms.xb[t]) : x + half;
+            const uint4 xa = x[at], xb = xh[at];
             if (terms.p[t]) {
                 const uint4 pv = ld_stream(reinterpret_cast<const uint4*>(terms.p[t]) + at, pol);
                 sa[0] += (uint64_t)xa.x * pv.x; sa[1] += (uint64_t)xa.y * pv.y;

@@ -110,6 +110,8 @@ constexpr int kMaxTerms = 16;
 struct FusedTerms {
     int count;
     const uint32_t* x[kMaxTerms];   // ciphertexts [2][rows][n]
+    const uint32_t* xb[kMaxTerms];  // b half of term t when it does not sit at x[t] + rows * n (a mod-dropped
+                                    // ciphertext keeps its halves a full level apart); null: adjacent
     const uint32_t* p[kMaxTerms];   // plaintexts [rows][n] or null
 };
 int fused_terms_launch(const FusedTerms& terms, uint32_t* out, const int32_t* row_slot,

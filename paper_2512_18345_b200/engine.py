@@ -271,13 +271,18 @@ class Engine:
         return acc
 
     def fused_terms(self, xs, ps, row_slot, out=None):
-        """out = sum_t xs[t] * ps[t] (ps[t] None: plain term); xs are [2, rows, n] tensors."""
+        """out = sum_t xs[t] * ps[t] (ps[t] None: plain term); xs[t] is a [2, rows, n] tensor, or a pair
+        (a, b) of [rows, n] tensors for a ciphertext whose halves are not adjacent (no gathering copy)."""
         count = len(xs)
-        out = self.torch.empty_like(xs[0]) if out is None else out
-        xp = (ctypes.c_void_p * count)(*[x.data_ptr() for x in xs])
+        pair = lambda x: isinstance(x, (tuple, list))
+        first = xs[0][0]                   # the a half either way: [rows, n]
+        rows, n = first.shape[0], first.shape[1]
+        out = self.empty(2, rows, n) if out is None else out
+        xa = (ctypes.c_void_p * count)(*[(x[0] if pair(x) else x).data_ptr() for x in xs])
+        xb = (ctypes.c_void_p * count)(*[x[1].data_ptr() if pair(x) else None for x in xs])
         pp = (ctypes.c_void_p * count)(*[None if p is None else p.data_ptr() for p in ps])
-        _lib.check(self.lib.ckks_fused_terms(self.ctx, count, xp, pp, out.data_ptr(), row_slot.data_ptr(),
-                                             xs[0].shape[1], xs[0].shape[2], self.stream()))
+        _lib.check(self.lib.ckks_fused_terms_halves(self.ctx, count, xa, xb, pp, out.data_ptr(), row_slot.data_ptr(),
+                                                    rows, n, self.stream()))
         return out
 
     def fused_terms_multi(self, xs, table, row_slot):
