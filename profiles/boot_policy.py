@@ -18,7 +18,7 @@ from paper_2512_18345_b200.params import ParameterSet  # noqa: E402
 tag = sys.argv[1] if len(sys.argv) > 1 else "r2l"
 policies = [tuple(int(x) for x in a.split(":")) for a in sys.argv[2:]] or [(0, 3), (2, 2), (12, 2), (28, 2), (37, 2), (48, 2), (28, 3)]
 eng = get_engine()
-eng.set_lanes(8)
+eng.set_lanes(int(__import__('os').environ.get('BOOT_LANES', '8')))      # BOOT_LANES: lanes of the graph (default 8)
 p = ParameterSet.builtin("ks48")
 sk, _sparse, boot = standard_setup(p, BootstrapConfig())
 z, ct = standard_input(p, boot, sk, 0)
